@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 pseudo-stereo hot path (BASELINE.json metric: 4K stereo frames/s).
+
+Workload (BASELINE.json configs[1]): synthetic 3840x2160 RGB frames -> depth map ->
+exact FP64 cross-bilateral -> forward DIBR -> inpaint -> red-cyan anaglyph, default
+config (auto base 30, T=150, sigma_s=8, sigma_r=16). One step = one frame through the
+whole pipeline. Inputs cycle through a device-resident ring of distinct frames larger
+than L2 (8 x 24.9 MB = 199 MB > 126 MB), so every step reads its input from HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): frames are independent, so every rank runs
+its own frames with no data-path collective (weak scaling); torch.distributed is used
+only for the start/stop barriers and the max-over-ranks of the device time.
+
+Printed: one JSON line (rank 0). `value` = kernel path with inputs resident in HBM
+(CUDA events on the pipeline stream); `e2e` = the same through the drop-in C ABI
+p3s_convert with host (pinned) frames, H2D + D2H of outputs, depth and filtered depth
+inside the timed region; `roofline` = the dominant kernel (the exact FP64 bilateral)
+against the measured FP64 issue rate; `roofline_hbm` = the fused DIBR+anaglyph kernel
+against measured HBM bandwidth; `cpu_baseline` = the reference's own CPU implementation
+(oracle/_ref, compiled from the reference sources) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W4K, H4K = 3840, 2160
+RING = 8
+SWEEP = [0, 2, 16, 30, 60, 120, 254, 510]
+L2_BYTES = 126 * 2**20
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def taps_1d(n: int, r: int) -> int:
+    # sum over positions of the clipped window length min(x,r) + min(n-1-x,r) + 1
+    return sum(min(x, r) + min(n - 1 - x, r) + 1 for x in range(n))
+
+
+def bilateral_flops(w: int, h: int, sigma_s: float = 8.0) -> float:
+    import math
+    r = int(math.ceil(2.0 * sigma_s))
+    # 4 separately rounded FP64 ops per tap: w*s*R, ws+=, w*d, vs+=
+    return 4.0 * taps_1d(w, r) * taps_1d(h, r)
+
+
+def make_frames(w, h, n, seed0, checker=None):
+    import oracle
+    o = checker or oracle.load("port")
+    return [o.synthetic_frame(w, h, seed0 + i) for i in range(n)]
+
+
+def allreduce_max(vals, world, use_dist):
+    if world == 1 or not use_dist:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_rate(budget_s: float, max_reps: int, frame, kind="best"):
+    """Reference CPU path on all host cores, bounded sample of whole 4K frames."""
+    import oracle
+    o = oracle.load(kind)
+    threads = os.cpu_count() or 1
+    cfg = oracle.Cfg()
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_reps:
+        t0 = time.perf_counter()
+        o.convert(frame, cfg, threads=threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    return o.kind, threads, times
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    frame = make_frames(W4K, H4K, 1, 1)[0]
+    import oracle
+    o = oracle.load("best")
+    threads = os.cpu_count() or 1
+    cfg = oracle.Cfg()
+    for _ in range(min(args.warmup, 1)):
+        o.convert(frame, cfg, threads=threads)
+    budget = args.reference_budget
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.convert(frame, cfg, threads=threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget:
+            break
+    total = sum(times)
+    fps = len(times) / total
+    line = {
+        "impl": "reference", "metric": "4K stereo frames/sec", "value": fps, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": len(times), "steps_requested": args.steps,
+        "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f64",
+        "data": "synthetic", "mpix_per_s": fps * W4K * H4K / 1e6,
+        "config": {"workload": "UHD 3840x2160 synthetic_frame(seed=1) -> anaglyph, default "
+                               "config (auto base 30), reference CPU path", "width": W4K,
+                   "height": H4K, "base": 30, "format": "anaglyph"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads,
+                         "kind": o.kind,
+                         "sample": f"{len(times)} whole UHD frames (time budget {budget:.0f}s), "
+                                   f"convert_image with Executor({threads})"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--reference-budget", type=float, default=150.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import paper_2009_09501_b200 as p3s
+    if not os.path.exists(p3s.LIB_PATH):
+        p3s.build()
+    use_dist = world > 1
+    if use_dist:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p3s.set_device(local)
+
+    cfg = p3s.Config()
+    pipe = p3s.Pipeline(W4K, H4K, cfg)
+    # frames: distinct per rank (frame-sharded video); seeds follow the reference's
+    # video convention seed = 1 + global frame index
+    frames = make_frames(W4K, H4K, RING, 1 + rank * RING)
+    ring = [p3s.DeviceBuffer(pipe.frame_bytes) for _ in range(RING)]
+    for f, d in zip(frames, ring):
+        pipe.upload(f, d.addr)
+    p3s.stream_sync(pipe.stream)
+    stream = pipe.stream
+
+    # ---- kernel path: inputs resident in HBM ----
+    for i in range(args.warmup):
+        pipe.run(ring[i % RING].addr, timed=True)
+    p3s.stream_sync(stream)
+    pipe.timing_sum(reset=True)
+    ev0, ev1 = p3s.Event(), p3s.Event()
+    clocks = ClockSampler(local)
+    barrier(world)
+    p3s.device_sync()
+    clocks.start()
+    time.sleep(0.3)  # let nvidia-smi attach before the region
+    ev0.record(stream)
+    for i in range(args.steps):
+        pipe.run(ring[i % RING].addr, timed=True)
+    ev1.record(stream)
+    p3s.stream_sync(stream)
+    elapsed_ms = ev0.elapsed_ms(ev1)
+    clk = clocks.stop()
+    barrier(world)
+    stage_sum, nruns = pipe.timing_sum(reset=True)
+    (elapsed_max,) = allreduce_max([elapsed_ms], world, use_dist)
+    total_frames = args.steps * world
+    fps = total_frames / (elapsed_max / 1e3)
+
+    # correctness spot check of the last frame against the CPU oracle is done by the
+    # parity tests; here only assert the device produced a plausible output
+    depth, filt, out = pipe.download()
+    assert out.any() and filt.any()
+
+    # ---- e2e through the drop-in C ABI (host pinned frames, H2D + D2H per step) ----
+    L = p3s.lib()
+    images = [p3s.Image(f) for f in frames]
+    res = C.c_void_p()
+    for i in range(max(2, args.warmup // 2)):
+        p3s._check(L.p3s_convert(images[i % RING].h, cfg.h, C.byref(res)))
+        L.p3s_result_free(res)
+    e2e_steps = max(10, min(args.steps, 100))
+    barrier(world)
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        p3s._check(L.p3s_convert(images[i % RING].h, cfg.h, C.byref(res)))
+        L.p3s_result_free(res)
+    e2e_s = time.perf_counter() - t0
+    barrier(world)
+    (e2e_max,) = allreduce_max([e2e_s], world, use_dist)
+    e2e_fps = e2e_steps * world / e2e_max
+    N = W4K * H4K
+
+    # ---- parallax sweep (configs[1]: "max parallax sweep") ----
+    sweep = {}
+    if not args.no_sweep:
+        for b in SWEEP:
+            pb = p3s.Pipeline(W4K, H4K, p3s.Config(base=b))
+            for i in range(3):
+                pb.run(ring[i % RING].addr, timed=True)
+            p3s.stream_sync(pb.stream)
+            pb.timing_sum(reset=True)
+            a, z = p3s.Event(), p3s.Event()
+            ns = 20
+            a.record(pb.stream)
+            for i in range(ns):
+                pb.run(ring[i % RING].addr, timed=True)
+            z.record(pb.stream)
+            p3s.stream_sync(pb.stream)
+            st, n = pb.timing_sum(reset=True)
+            passes = pb.inpaint_stats()
+            sweep[str(b)] = {"frames_per_s": ns / (a.elapsed_ms(z) / 1e3),
+                             "inpaint_ms": (st["inpaint_left_ns"]) / n / 1e6,
+                             "dibr_ms": st["dibr_ns"] / n / 1e6,
+                             "inpaint_passes": [int(passes[0]), int(passes[3])]}
+            del pb
+
+    if rank != 0:
+        if use_dist:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    # ---- rooflines ----
+    peaks, peaks_src = measured_peaks()
+    fp64 = p3s.fp64_peak()
+    per = {k: v / nruns for k, v in stage_sum.items()}
+    bil_ns = per["filter_ns"]
+    flops = bilateral_flops(W4K, H4K)
+    achieved_tf = flops / (bil_ns * 1e-9) / 1e12
+    dibr_ns = per["dibr_ns"]
+    k3_bytes = 7 * N  # 4N read (R, G, B, filtered depth) + 3N anaglyph write
+    k3_gbs = k3_bytes / (dibr_ns * 1e-9) / 1e9
+    prof_traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "bilateral_traffic.json")
+    if os.path.exists(prof_path):
+        with open(prof_path) as f:
+            prof_traffic = json.load(f).get("dram_bytes_per_launch")
+
+    line = {
+        "metric": "4K stereo frames/sec", "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f64",
+        "data": "synthetic", "mpix_per_s": fps * N / 1e6,
+        "config": {"workload": "UHD 3840x2160 synthetic_frame -> depth -> exact FP64 bilateral "
+                               "-> forward DIBR -> inpaint -> anaglyph (BASELINE configs[1]), "
+                               "default config, auto base 30",
+                   "width": W4K, "height": H4K, "base": 30, "format": "anaglyph",
+                   "l2": f"input ring {RING} frames x {3 * N / 1e6:.1f} MB = "
+                         f"{RING * 3 * N / 1e6:.0f} MB > 126 MB L2",
+                   "parallelism": f"frame-sharded x{world}, no collectives"},
+        "stages_ms": {k: v / 1e6 for k, v in per.items()},
+        "roofline": {"kernel": "k_bilateral_tiled (exact FP64 cross-bilateral)",
+                     "bound": "fp64", "achieved": achieved_tf, "peak": fp64 / 1e12,
+                     "unit": "TFLOP/s", "frac": achieved_tf / (fp64 / 1e12),
+                     "traffic": prof_traffic,
+                     "algorithmic": f"4 FP64 ops/tap x {flops / 4:.4g} taps per launch",
+                     "peak_source": "measured in this run: non-FMA DMUL/DADD issue-rate "
+                                    "microbenchmark (p3s_gpu_fp64_peak)"},
+        "roofline_hbm": {"kernel": "k_dibr (forward DIBR fused with anaglyph)", "bound": "hbm",
+                         "achieved": k3_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": k3_gbs / peaks["hbm_gbs"], "algorithmic": "7N bytes per frame",
+                         "peak_source": peaks_src},
+        "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 3 * N,
+                "d2h_bytes_per_step": 5 * N, "steps": e2e_steps,
+                "path": "p3s_convert (C ABI) on pinned p3s_image, outputs+depth+filtered D2H"},
+        "gpu_launches": 6 * args.steps,
+        "clocks": clk,
+        "sweep_base": sweep,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        kind, threads, times = cpu_reference_rate(args.cpu_budget, 3, frames[0])
+        v = len(times) / sum(times)
+        line["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": threads, "kind": kind,
+                                "sample": f"{len(times)} whole UHD frame(s), default config, "
+                                          f"{threads} host threads"}
+        line["speedup_vs_cpu_e2e"] = e2e_fps / v
+    print(json.dumps(line), flush=True)
+    if use_dist:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

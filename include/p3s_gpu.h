@@ -1,0 +1,141 @@
+/* p3s_gpu.h — B200 extensions to the pseudo3d C ABI (libpseudo3d_b200.so).
+ *
+ * pseudo3d.h is the drop-in surface (the reference's 49 functions). This header adds
+ * what a GPU build needs on top, all plain C over host/device pointers:
+ *   - stage entry points over host planes — the reference C++ stage API of
+ *     proj/include/pseudo3d/{depth,bilateral,dibr,inpaint,stereo_format}.hpp as C, used
+ *     by the parity tests to diff every intermediate against the oracle;
+ *   - a device-resident pipeline (frames already in HBM; kernel-only throughput);
+ *   - a multi-stream video converter (pinned host frames in, H2D/compute/D2H overlapped);
+ *   - small device/event/pinned-memory helpers for harnesses.
+ * All functions return p3s_status and set p3s_last_error() like pseudo3d.h.
+ */
+#ifndef P3S_GPU_H
+#define P3S_GPU_H
+
+#include "pseudo3d.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Flat view of p3s_config (reference config.hpp:25-43). base < 0 means auto. */
+typedef struct p3s_params {
+    int base;
+    int pop_threshold;
+    double sigma_spatial;
+    double sigma_range;
+    int depth_block;
+    int inpaint_block;
+    double alpha;
+    double beta;
+    int mode;         /* p3s_dibr_mode */
+    unsigned formats; /* p3s_format bits */
+} p3s_params;
+
+P3S_API p3s_status p3s_config_get_params(const p3s_config* cfg, p3s_params* out);
+/* Validates the whole candidate; on failure the config is unchanged. */
+P3S_API p3s_status p3s_config_set_params(p3s_config* cfg, const p3s_params* params);
+
+P3S_API int p3s_gpu_device_count(void);
+/* Binds the calling thread to a CUDA device (all later calls on this thread use it). */
+P3S_API p3s_status p3s_gpu_set_device(int ordinal);
+P3S_API p3s_status p3s_gpu_device_name(char* buf, size_t cap);
+
+/* ---- stage entry points (host planes in/out, row-major w*h, no pitch) ---- */
+/* image.cpp:13-21 */
+P3S_API p3s_status p3s_gpu_luma(const uint8_t* r, const uint8_t* g, const uint8_t* b, int w,
+                                int h, uint8_t* out);
+/* depth.cpp:21-74: luma -> Sobel -> block values; values: ceil(w/B)*ceil(h/B) doubles */
+P3S_API p3s_status p3s_gpu_block_depth(const uint8_t* r, const uint8_t* g, const uint8_t* b,
+                                       int w, int h, const p3s_config* cfg, double* values);
+/* depth.cpp:76-121 */
+P3S_API p3s_status p3s_gpu_upsample(const double* values, int w, int h, int block, uint8_t* out);
+/* depth.cpp:127-129 */
+P3S_API p3s_status p3s_gpu_generate_depth(const uint8_t* r, const uint8_t* g, const uint8_t* b,
+                                          int w, int h, const p3s_config* cfg, uint8_t* depth);
+/* bilateral.cpp:103-116 (rounded) and :88-101 (raw means, w*h doubles) */
+P3S_API p3s_status p3s_gpu_cross_bilateral(const uint8_t* depth, const uint8_t* guide, int w,
+                                           int h, const p3s_config* cfg, uint8_t* out);
+P3S_API p3s_status p3s_gpu_cross_bilateral_raw(const uint8_t* depth, const uint8_t* guide, int w,
+                                               int h, const p3s_config* cfg, double* out);
+/* dibr.cpp:106-111 (mode from cfg); masks 1 = damaged */
+P3S_API p3s_status p3s_gpu_reconstruct(const uint8_t* r, const uint8_t* g, const uint8_t* b,
+                                       const uint8_t* depth, int w, int h, const p3s_config* cfg,
+                                       uint8_t* lr, uint8_t* lg, uint8_t* lb, uint8_t* rr,
+                                       uint8_t* rg, uint8_t* rb, uint8_t* lmask, uint8_t* rmask);
+/* inpaint.cpp:29-130; stats: passes, repaired, fallback_filled */
+P3S_API p3s_status p3s_gpu_inpaint(const uint8_t* r, const uint8_t* g, const uint8_t* b,
+                                   const uint8_t* mask, int w, int h, const p3s_config* cfg,
+                                   uint8_t* outr, uint8_t* outg, uint8_t* outb, int64_t* stats);
+/* stereo_format.cpp:8-73; half: out w x h, full: out 2w x h */
+P3S_API p3s_status p3s_gpu_anaglyph(const uint8_t* lr, const uint8_t* lg, const uint8_t* lb,
+                                    const uint8_t* rr, const uint8_t* rg, const uint8_t* rb,
+                                    int w, int h, uint8_t* outr, uint8_t* outg, uint8_t* outb);
+P3S_API p3s_status p3s_gpu_side_by_side(const uint8_t* lr, const uint8_t* lg, const uint8_t* lb,
+                                        const uint8_t* rr, const uint8_t* rg, const uint8_t* rb,
+                                        int w, int h, int half, uint8_t* outr, uint8_t* outg,
+                                        uint8_t* outb);
+
+/* ---- device-resident pipeline ----
+ * A plan for one (size, config) on the calling thread's device, with its own stream.
+ * Input frames live in device memory as 3 planes of pitch*h bytes (plane stride pitch*h).
+ * run() only enqueues (returns before the GPU finishes). */
+typedef struct p3s_pipeline p3s_pipeline;
+P3S_API p3s_status p3s_pipeline_create(int w, int h, const p3s_config* cfg, p3s_pipeline** out);
+P3S_API void p3s_pipeline_free(p3s_pipeline* p);
+P3S_API int p3s_pipeline_pitch(const p3s_pipeline* p);
+P3S_API size_t p3s_pipeline_frame_bytes(const p3s_pipeline* p);
+P3S_API void* p3s_pipeline_stream(const p3s_pipeline* p);
+/* timed != 0 records CUDA events between stages (p3s_pipeline_timings). stream may be
+ * NULL (the pipeline's own stream). */
+P3S_API p3s_status p3s_pipeline_run(p3s_pipeline* p, const uint8_t* d_src, int timed, void* stream);
+P3S_API p3s_status p3s_pipeline_timings(p3s_pipeline* p, p3s_timings* out);
+/* Sums the stage times of every timed run since the last reset (each run keeps its own
+ * events, so a timed loop needs no per-step synchronisation); count = runs summed. */
+P3S_API p3s_status p3s_pipeline_timing_sum(p3s_pipeline* p, p3s_timings* sum, int64_t* count,
+                                           int reset);
+/* Copies results of the last run to host planes (any pointer may be NULL), then syncs. */
+P3S_API p3s_status p3s_pipeline_download(p3s_pipeline* p, uint8_t* depth, uint8_t* filtered,
+                                         p3s_format format, uint8_t* outr, uint8_t* outg,
+                                         uint8_t* outb);
+/* stats[6]: left passes, repaired, fallback; right passes, repaired, fallback */
+P3S_API p3s_status p3s_pipeline_inpaint_stats(p3s_pipeline* p, int64_t* stats);
+/* H2D of host planes (w*h each) into a device frame with the pipeline's pitch; async on
+ * `stream` (NULL = pipeline stream). Host planes should be pinned for a true async copy. */
+P3S_API p3s_status p3s_pipeline_upload(p3s_pipeline* p, const uint8_t* r, const uint8_t* g,
+                                       const uint8_t* b, uint8_t* d_dst, void* stream);
+
+/* ---- video: frames pipelined through `streams` plans on the calling thread's device.
+ * frames[i] / outs[i] point at 3 consecutive planes (w*h bytes each; outs of FSBS are
+ * 2w*h each) in host memory, ideally pinned (p3s_host_alloc). Output = the lowest
+ * requested format bit. Frame i runs on stream i % streams: its H2D, kernels and D2H
+ * overlap the neighbouring frames'. Blocks until all n frames are back on the host. */
+typedef struct p3s_video p3s_video;
+P3S_API p3s_status p3s_video_create(int w, int h, const p3s_config* cfg, int streams,
+                                    p3s_video** out);
+P3S_API p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
+                                     uint8_t* const* outs);
+P3S_API void p3s_video_free(p3s_video* v);
+
+/* ---- helpers ---- */
+P3S_API p3s_status p3s_gpu_malloc(size_t bytes, void** out);
+P3S_API void p3s_gpu_free(void* p);
+P3S_API p3s_status p3s_gpu_memset(void* p, int value, size_t bytes);
+P3S_API p3s_status p3s_gpu_stream_sync(void* stream);
+P3S_API p3s_status p3s_gpu_device_sync(void);
+P3S_API p3s_status p3s_gpu_event_create(void** out);
+P3S_API p3s_status p3s_gpu_event_record(void* ev, void* stream);
+P3S_API p3s_status p3s_gpu_event_elapsed_ms(void* start, void* stop, float* ms);
+P3S_API void p3s_gpu_event_destroy(void* ev);
+P3S_API void* p3s_host_alloc(size_t bytes); /* pinned pool */
+/* Measured non-FMA FP64 issue rate of the current device (DADD/DMUL ops per second), the
+ * roofline denominator of the exact bilateral kernel. */
+P3S_API p3s_status p3s_gpu_fp64_peak(double* ops_per_s);
+P3S_API void p3s_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* P3S_GPU_H */

@@ -1,0 +1,891 @@
+// Host orchestrator of the B200 pseudo-stereo pipeline: per-thread device contexts, plans
+// (host-computed exact tables + one device arena per (size, config)), the stage API of
+// include/p3s/pipeline.hpp and the full convert_image (reference pipeline.cpp:29-78).
+//
+// Built with -ffp-contract=off: the tables below must reproduce the reference's double
+// expressions bit for bit (SURVEY.md §7 rules 1, 2, 4, 5).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <deque>
+#include <cmath>
+#include <cstring>
+#include <list>
+#include <mutex>
+#include <sstream>
+#include <string>
+
+#include "p3s/pipeline.hpp"
+#include "p3s_cu.h"
+
+namespace p3s {
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw DeviceError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    }
+}
+#define CK(expr) check((expr), #expr)
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// ---- exact host tables --------------------------------------------------------------------
+
+// bilateral.cpp:22-35: radius ceil(2 sigma_s); spatial exp(-(dx^2+dy^2) * inv_s) with the
+// integer sum formed first; range exp(-(d^2) * inv_r). Only dx >= 0 is stored (the table is
+// symmetric in dx and the kernels index |dx|).
+int bilateral_radius(const ConversionConfig& c) {
+    return static_cast<int>(std::ceil(2.0 * c.sigma_spatial));
+}
+
+std::vector<double> spatial_table(const ConversionConfig& c, int r) {
+    const double inv_s = 1.0 / (2.0 * c.sigma_spatial * c.sigma_spatial);
+    std::vector<double> s(static_cast<std::size_t>(2 * r + 1) * (r + 1));
+    for (int dy = -r; dy <= r; ++dy)
+        for (int dx = 0; dx <= r; ++dx)
+            s[static_cast<std::size_t>(dy + r) * (r + 1) + dx] = std::exp(-(dx * dx + dy * dy) * inv_s);
+    return s;
+}
+
+void range_table(const ConversionConfig& c, double* out) {
+    const double inv_r = 1.0 / (2.0 * c.sigma_range * c.sigma_range);
+    for (int d = 0; d < 256; ++d) out[d] = std::exp(-(d * d) * inv_r);
+}
+
+// dibr.cpp:33-41 as a signed per-depth shift: sigma = +hb*(d/255) when d > T, else
+// -(hb*(1 - d/255)); then p.left = x - sigma and p.right = x + sigma are exactly the
+// reference's x - s / x + s and x + s' / x - s' (negation is exact in IEEE).
+void shift_table(int base, int T, double* out) {
+    const double hb = base / 2.0;
+    for (int d = 0; d < 256; ++d) {
+        if (d > T)
+            out[d] = hb * (d / 255.0);
+        else
+            out[d] = -(hb * (1.0 - d / 255.0));
+    }
+}
+
+// depth.cpp:82-102: centre list and locate(); the running index is monotone in v, so one
+// forward sweep gives the same (i, frac) as the reference's per-pixel linear scan.
+void locate_axis(int count, int blocks, int block, std::vector<int>& i0, std::vector<int>& i1,
+                 std::vector<double>& f) {
+    std::vector<double> c(blocks);
+    for (int i = 0; i < blocks; ++i) {
+        const int lo = i * block;
+        const int hi = std::min(lo + block, count);
+        c[i] = lo + (hi - 1 - lo) / 2.0;
+    }
+    i0.resize(count);
+    i1.resize(count);
+    f.resize(count);
+    int k = 0;
+    for (int p = 0; p < count; ++p) {
+        const double v = p;
+        int i;
+        double frac;
+        if (v <= c.front()) {
+            i = 0;
+            frac = 0.0;
+        } else if (v >= c.back()) {
+            i = blocks - 1;
+            frac = 0.0;
+        } else {
+            while (v > c[k + 1]) ++k;
+            i = k;
+            frac = (v - c[i]) / (c[i + 1] - c[i]);
+        }
+        i0[p] = i;
+        i1[p] = std::min(i + 1, blocks - 1);
+        f[p] = frac;
+    }
+}
+
+struct Arena {
+    std::size_t off = 0;
+    template <class T>
+    std::size_t take(std::size_t count) {
+        off = (off + 255) / 256 * 256;
+        const std::size_t at = off;
+        off += count * sizeof(T);
+        return at;
+    }
+};
+
+std::string plan_key(int w, int h, const ConversionConfig& c) {
+    std::ostringstream os;
+    os.precision(17);
+    os << w << 'x' << h << '|' << c.effective_base(w) << '|' << c.pop_threshold << '|'
+       << c.sigma_spatial << '|' << c.sigma_range << '|' << c.depth_block << '|' << c.alpha
+       << '|' << c.beta << '|' << static_cast<int>(c.dibr_mode) << '|' << c.formats;
+    return os.str();
+}
+
+std::int64_t ms_to_ns(float ms) { return static_cast<std::int64_t>(std::llround(ms * 1.0e6)); }
+
+}  // namespace
+
+// ==========================================================================================
+// Pipeline::Impl — one plan
+// ==========================================================================================
+struct Pipeline::Impl {
+    int dev = 0;
+    int w = 0, h = 0, pitch = 0, fpitch = 0, mwords = 0;
+    ConversionConfig cfg;
+    int base = 0, radius = 0;
+    bool backward = false;
+    unsigned formats = 0;
+    enum Route { kFusedAnaglyph, kDirectFsbs, kEyes } route = kEyes;
+    cu::Geom gm{};
+    cu::DepthTables dt{};
+    std::vector<double> h_spatial;
+    bool tiled = true;
+
+    cudaStream_t stream = nullptr;
+    unsigned char* arena = nullptr;
+    std::size_t arena_bytes = 0;
+
+    uint8_t *src = nullptr, *luma = nullptr, *depth = nullptr, *filt = nullptr;
+    unsigned long long* sums = nullptr;
+    double* values = nullptr;
+    double *range = nullptr, *spatial = nullptr, *shift = nullptr;
+    uint8_t *ana = nullptr, *hsbs = nullptr, *fsbs = nullptr, *eyes = nullptr;
+    uint32_t* mbits = nullptr;
+    uint32_t* lists = nullptr;  // [eye][list|list2|repair][N]
+    uint32_t* counts = nullptr;  // 2
+    uint32_t* ctl = nullptr;     // 64
+    long long* stats = nullptr;  // 6
+    // stage-API extras (allocated on first use)
+    unsigned char* stage_arena = nullptr;
+    uint8_t* stage_masks = nullptr;  // 2 byte masks
+    double* stage_raw = nullptr;
+
+    // Per-run stage events in a ring, so a long timed loop keeps every step's stage
+    // times without synchronising between steps (harvested by accumulated()).
+    static constexpr int kRing = 64;
+    std::vector<std::array<cudaEvent_t, 6>> ring;
+    int ring_next = 0, last_slot = -1;
+    std::deque<int> pending;
+    StageTimings acc;
+    long long acc_n = 0;
+    bool own_stream = false;
+
+    std::size_t plane() const { return static_cast<std::size_t>(pitch) * h; }
+    std::size_t npix() const { return static_cast<std::size_t>(w) * h; }
+
+    Impl(int width, int height, const ConversionConfig& c, int device, cudaStream_t st)
+        : dev(device), w(width), h(height), cfg(c), stream(st) {
+        cfg.validate();
+        pixel_count(w, h);
+        pitch = round_up(w, 16);
+        fpitch = round_up(2 * w, 16);
+        mwords = (w + 31) / 32;
+        base = cfg.effective_base(w);
+        radius = bilateral_radius(cfg);
+        backward = cfg.dibr_mode == DibrMode::kBackwardFallback;
+        formats = cfg.formats;
+        route = formats == kFormatAnaglyph ? kFusedAnaglyph
+                : formats == kFormatFsbs   ? kDirectFsbs
+                                           : kEyes;
+        gm = cu::Geom{w, h, pitch};
+        tiled = radius <= cu::bilateral_tiled_max_radius();
+
+        const int blk = cfg.depth_block;
+        const int bx = (w + blk - 1) / blk, by = (h + blk - 1) / blk;
+        std::vector<int> ci0, ci1, ri0, ri1;
+        std::vector<double> cf, rf;
+        locate_axis(w, bx, blk, ci0, ci1, cf);
+        locate_axis(h, by, blk, ri0, ri1, rf);
+        h_spatial = spatial_table(cfg, radius);
+        double h_range[256], h_shift[256];
+        range_table(cfg, h_range);
+        shift_table(base, cfg.pop_threshold, h_shift);
+
+        const std::size_t P = plane(), N = npix();
+        Arena a;
+        const std::size_t o_src = a.take<uint8_t>(3 * P);
+        const std::size_t o_luma = a.take<uint8_t>(P);
+        const std::size_t o_depth = a.take<uint8_t>(P);
+        const std::size_t o_filt = a.take<uint8_t>(P);
+        const std::size_t o_sums = a.take<unsigned long long>(static_cast<std::size_t>(bx) * by);
+        const std::size_t o_vals = a.take<double>(static_cast<std::size_t>(bx) * by);
+        const std::size_t o_ci0 = a.take<int>(w), o_ci1 = a.take<int>(w), o_cf = a.take<double>(w);
+        const std::size_t o_ri0 = a.take<int>(h), o_ri1 = a.take<int>(h), o_rf = a.take<double>(h);
+        const std::size_t o_range = a.take<double>(256), o_shift = a.take<double>(256);
+        const std::size_t o_spat = a.take<double>(h_spatial.size());
+        const std::size_t o_ana = (formats & kFormatAnaglyph) ? a.take<uint8_t>(3 * P) : 0;
+        const std::size_t o_hsbs = (formats & kFormatHsbs) ? a.take<uint8_t>(3 * P) : 0;
+        const std::size_t o_fsbs =
+            (formats & kFormatFsbs) ? a.take<uint8_t>(3 * static_cast<std::size_t>(fpitch) * h) : 0;
+        const std::size_t o_eyes = a.take<uint8_t>(route == kEyes ? 6 * P : 0);
+        const std::size_t o_mbits = a.take<uint32_t>(2 * static_cast<std::size_t>(mwords) * h);
+        const std::size_t o_lists = a.take<uint32_t>(backward ? 0 : 6 * N);
+        const std::size_t o_cnt = a.take<uint32_t>(2);
+        const std::size_t o_ctl = a.take<uint32_t>(64);
+        const std::size_t o_stats = a.take<long long>(6);
+        arena_bytes = a.off;
+        CK(cudaSetDevice(dev));
+        CK(cudaMalloc(&arena, arena_bytes));
+        src = arena + o_src;
+        luma = arena + o_luma;
+        depth = arena + o_depth;
+        filt = arena + o_filt;
+        sums = reinterpret_cast<unsigned long long*>(arena + o_sums);
+        values = reinterpret_cast<double*>(arena + o_vals);
+        range = reinterpret_cast<double*>(arena + o_range);
+        shift = reinterpret_cast<double*>(arena + o_shift);
+        spatial = reinterpret_cast<double*>(arena + o_spat);
+        if (formats & kFormatAnaglyph) ana = arena + o_ana;
+        if (formats & kFormatHsbs) hsbs = arena + o_hsbs;
+        if (formats & kFormatFsbs) fsbs = arena + o_fsbs;
+        if (route == kEyes) eyes = arena + o_eyes;
+        mbits = reinterpret_cast<uint32_t*>(arena + o_mbits);
+        if (!backward) lists = reinterpret_cast<uint32_t*>(arena + o_lists);
+        counts = reinterpret_cast<uint32_t*>(arena + o_cnt);
+        ctl = reinterpret_cast<uint32_t*>(arena + o_ctl);
+        stats = reinterpret_cast<long long*>(arena + o_stats);
+
+        auto up = [&](std::size_t off, const void* p, std::size_t n) {
+            CK(cudaMemcpyAsync(arena + off, p, n, cudaMemcpyHostToDevice, stream));
+        };
+        up(o_ci0, ci0.data(), w * sizeof(int));
+        up(o_ci1, ci1.data(), w * sizeof(int));
+        up(o_cf, cf.data(), w * sizeof(double));
+        up(o_ri0, ri0.data(), h * sizeof(int));
+        up(o_ri1, ri1.data(), h * sizeof(int));
+        up(o_rf, rf.data(), h * sizeof(double));
+        up(o_range, h_range, sizeof(h_range));
+        up(o_shift, h_shift, sizeof(h_shift));
+        up(o_spat, h_spatial.data(), h_spatial.size() * sizeof(double));
+        CK(cudaMemsetAsync(arena + o_stats, 0, 6 * sizeof(long long), stream));
+        CK(cudaStreamSynchronize(stream));  // host vectors above go out of scope
+
+        dt.col_i0 = reinterpret_cast<int*>(arena + o_ci0);
+        dt.col_i1 = reinterpret_cast<int*>(arena + o_ci1);
+        dt.col_f = reinterpret_cast<double*>(arena + o_cf);
+        dt.row_i0 = reinterpret_cast<int*>(arena + o_ri0);
+        dt.row_i1 = reinterpret_cast<int*>(arena + o_ri1);
+        dt.row_f = reinterpret_cast<double*>(arena + o_rf);
+        dt.bx = bx;
+        dt.by = by;
+        dt.block = blk;
+        dt.alpha255 = cfg.alpha * 255.0;
+        dt.beta = cfg.beta;
+        dt.row_denom = h > 1 ? h - 1 : 1;
+    }
+
+    ~Impl() {
+        cudaSetDevice(dev);
+        if (own_stream && stream) {
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
+        for (auto& set : ring)
+            for (auto& e : set)
+                if (e) cudaEventDestroy(e);
+        if (arena) cudaFree(arena);
+        if (stage_arena) cudaFree(stage_arena);
+    }
+
+    uint8_t* src_plane(const uint8_t* s, int c) const { return const_cast<uint8_t*>(s) + c * plane(); }
+    uint32_t* list_ptr(int eye, int which) const { return lists + (3 * eye + which) * npix(); }
+
+    void ensure_stage() {
+        if (stage_arena) return;
+        const std::size_t bytes = 2 * plane() + 256 + npix() * sizeof(double);
+        CK(cudaMalloc(&stage_arena, bytes));
+        stage_masks = stage_arena;
+        stage_raw = reinterpret_cast<double*>(stage_arena + (2 * plane() + 255) / 256 * 256);
+    }
+
+    // ---- stage launchers ----
+    void enq_depth(const uint8_t* s, cudaStream_t st) {
+        CK(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * dt.bx * dt.by, st));
+        CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
+                           dt.block, dt.bx, st));
+        CK(cu::block_values(sums, gm, dt, values, st));
+        CK(cu::upsample(values, gm, dt, depth, st));
+    }
+
+    void enq_bilateral(const uint8_t* dmap, const uint8_t* guide, uint8_t* out, double* raw,
+                       cudaStream_t st) {
+        if (tiled)
+            CK(cu::bilateral_tiled(dmap, guide, gm, radius, h_spatial.data(), range, out, raw, st));
+        else
+            CK(cu::bilateral(dmap, guide, gm, radius, spatial, range, out, raw, st));
+    }
+
+    void eye_planes(uint8_t* (&L)[3], uint8_t* (&R)[3], int& lp) const {
+        for (int c = 0; c < 3; ++c) L[c] = R[c] = nullptr;
+        if (route == kFusedAnaglyph) {
+            L[0] = ana;
+            R[1] = ana + plane();
+            R[2] = ana + 2 * plane();
+            lp = pitch;
+        } else if (route == kDirectFsbs) {
+            const std::size_t fp = static_cast<std::size_t>(fpitch) * h;
+            for (int c = 0; c < 3; ++c) {
+                L[c] = fsbs + c * fp;
+                R[c] = fsbs + c * fp + w;
+            }
+            lp = fpitch;
+        } else {
+            for (int c = 0; c < 3; ++c) {
+                L[c] = eyes + c * plane();
+                R[c] = eyes + (3 + c) * plane();
+            }
+            lp = pitch;
+        }
+    }
+
+    void enq_dibr_inpaint(const uint8_t* s, cudaStream_t st, cudaEvent_t mid) {
+        uint8_t *L[3], *R[3];
+        int lp = pitch;
+        eye_planes(L, R, lp);
+        cu::EyeOut eo[2];
+        for (int e = 0; e < 2; ++e) {
+            for (int c = 0; c < 3; ++c) eo[e].plane[c] = e ? R[c] : L[c];
+            eo[e].pitch = lp;
+            eo[e].mask_bytes = nullptr;
+            eo[e].mask_bits = backward ? nullptr : mbits + static_cast<std::size_t>(e) * mwords * h;
+            eo[e].mask_pitch = mwords;
+            eo[e].list = backward ? nullptr : list_ptr(e, 0);
+            eo[e].count = counts + e;
+        }
+        if (!backward) CK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), st));
+        CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, backward,
+                    eo[0], eo[1], st));
+        if (mid) CK(cudaEventRecord(mid, st));
+        if (!backward) {
+            cu::InpaintEye ie[2];
+            for (int e = 0; e < 2; ++e) {
+                for (int c = 0; c < 3; ++c) ie[e].plane[c] = eo[e].plane[c];
+                ie[e].pitch = lp;
+                ie[e].mask_bytes = nullptr;
+                ie[e].mask_bits = eo[e].mask_bits;
+                ie[e].mask_pitch = mwords;
+                ie[e].list = list_ptr(e, 0);
+                ie[e].count = counts + e;
+                ie[e].list2 = list_ptr(e, 1);
+                ie[e].repair = list_ptr(e, 2);
+            }
+            CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st));
+        }
+    }
+
+    void enq_formats(cudaStream_t st) {
+        if (route != kEyes) return;
+        const uint8_t* L[3] = {eyes, eyes + plane(), eyes + 2 * plane()};
+        const uint8_t* R[3] = {eyes + 3 * plane(), eyes + 4 * plane(), eyes + 5 * plane()};
+        if (formats & kFormatAnaglyph) {
+            uint8_t* o[3] = {ana, ana + plane(), ana + 2 * plane()};
+            CK(cu::anaglyph(L, R, gm, o, pitch, st));
+        }
+        if (formats & kFormatHsbs) {
+            uint8_t* o[3] = {hsbs, hsbs + plane(), hsbs + 2 * plane()};
+            CK(cu::side_by_side_half(L, R, gm, o, pitch, st));
+        }
+        if (formats & kFormatFsbs) {
+            const std::size_t fp = static_cast<std::size_t>(fpitch) * h;
+            uint8_t* o[3] = {fsbs, fsbs + fp, fsbs + 2 * fp};
+            CK(cu::side_by_side_full(L, R, gm, o, fpitch, st));
+        }
+    }
+
+    StageTimings stage_times(const std::array<cudaEvent_t, 6>& ev) {
+        StageTimings t;
+        CK(cudaEventSynchronize(ev[5]));
+        float ms[5] = {0, 0, 0, 0, 0};
+        for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+        t.depth_gen_ns = ms_to_ns(ms[0]);
+        t.filter_ns = ms_to_ns(ms[1]);
+        t.dibr_ns = ms_to_ns(ms[2]);
+        // both eyes are repaired by one kernel; its time is reported as the left eye's
+        t.inpaint_left_ns = backward ? 0 : ms_to_ns(ms[3]);
+        t.inpaint_right_ns = 0;
+        t.format_ns = ms_to_ns(ms[4]);
+        return t;
+    }
+
+    void harvest_one() {
+        const int slot = pending.front();
+        pending.pop_front();
+        const StageTimings t = stage_times(ring[slot]);
+        acc.depth_gen_ns += t.depth_gen_ns;
+        acc.filter_ns += t.filter_ns;
+        acc.dibr_ns += t.dibr_ns;
+        acc.inpaint_left_ns += t.inpaint_left_ns;
+        acc.inpaint_right_ns += t.inpaint_right_ns;
+        acc.format_ns += t.format_ns;
+        ++acc_n;
+    }
+
+    const std::array<cudaEvent_t, 6>* next_events() {
+        if (ring.empty()) {
+            ring.resize(kRing);
+            for (auto& set : ring)
+                for (auto& e : set) CK(cudaEventCreate(&e));
+        }
+        if (static_cast<int>(pending.size()) == kRing) harvest_one();
+        const int slot = ring_next;
+        ring_next = (ring_next + 1) % kRing;
+        pending.push_back(slot);
+        last_slot = slot;
+        return &ring[slot];
+    }
+
+    void run(const uint8_t* s, cudaStream_t st, bool record) {
+        if ((formats & kFormatHsbs) && (w % 2 != 0))
+            throw std::invalid_argument("side_by_side: half mode requires an even width");
+        const std::array<cudaEvent_t, 6>* ev = record ? next_events() : nullptr;
+        if (ev) CK(cudaEventRecord((*ev)[0], st));
+        enq_depth(s, st);
+        if (ev) CK(cudaEventRecord((*ev)[1], st));
+        enq_bilateral(depth, luma, filt, nullptr, st);
+        if (ev) CK(cudaEventRecord((*ev)[2], st));
+        enq_dibr_inpaint(s, st, ev ? (*ev)[3] : nullptr);
+        if (ev) CK(cudaEventRecord((*ev)[4], st));
+        enq_formats(st);
+        if (ev) CK(cudaEventRecord((*ev)[5], st));
+    }
+
+    StageTimings timings() {
+        if (last_slot < 0) return StageTimings{};
+        return stage_times(ring[last_slot]);
+    }
+
+    StageTimings accumulated(long long* count, bool reset) {
+        while (!pending.empty()) harvest_one();
+        const StageTimings t = acc;
+        if (count) *count = acc_n;
+        if (reset) {
+            acc = StageTimings{};
+            acc_n = 0;
+        }
+        return t;
+    }
+
+    const uint8_t* output(StereoFormat f) const {
+        return f == kFormatAnaglyph ? ana : f == kFormatHsbs ? hsbs : fsbs;
+    }
+    int output_pitch(StereoFormat f) const { return f == kFormatFsbs ? fpitch : pitch; }
+    int output_width(StereoFormat f) const { return f == kFormatFsbs ? 2 * w : w; }
+
+    void d2h_plane(uint8_t* host, const uint8_t* dev_plane, int dpitch, int width,
+                   cudaStream_t st) {
+        CK(cudaMemcpy2DAsync(host, width, dev_plane, dpitch, width, h, cudaMemcpyDeviceToHost, st));
+    }
+    void h2d_plane(uint8_t* dev_plane, const uint8_t* host, cudaStream_t st) {
+        CK(cudaMemcpy2DAsync(dev_plane, pitch, host, w, w, h, cudaMemcpyHostToDevice, st));
+    }
+
+    void download(ConversionResult& out, cudaStream_t st) {
+        out.depth = GrayMap(w, h, false);
+        out.filtered_depth = GrayMap(w, h, false);
+        d2h_plane(out.depth.data.data(), depth, pitch, w, st);
+        d2h_plane(out.filtered_depth.data.data(), filt, pitch, w, st);
+        for (StereoFormat f : {kFormatAnaglyph, kFormatHsbs, kFormatFsbs}) {
+            if (!(formats & f)) continue;
+            const int ow = output_width(f);
+            ImageRGB8 img(ow, h, false);
+            const std::size_t ps = static_cast<std::size_t>(output_pitch(f)) * h;
+            for (int c = 0; c < 3; ++c)
+                d2h_plane(img.plane(c).data(), output(f) + c * ps, output_pitch(f), ow, st);
+            out.outputs[f] = std::move(img);
+        }
+        CK(cudaStreamSynchronize(st));
+    }
+};
+
+// ==========================================================================================
+// Device
+// ==========================================================================================
+struct Device::Impl {
+    int ordinal = 0;
+    cudaStream_t stream = nullptr;
+    std::list<std::pair<std::string, std::shared_ptr<Pipeline::Impl>>> plans;  // LRU
+    static constexpr std::size_t kMaxPlans = 4;
+
+    std::shared_ptr<Pipeline::Impl> plan(int w, int h, const ConversionConfig& cfg) {
+        const std::string key = plan_key(w, h, cfg);
+        for (auto it = plans.begin(); it != plans.end(); ++it) {
+            if (it->first == key) {
+                plans.splice(plans.begin(), plans, it);
+                return plans.front().second;
+            }
+        }
+        auto p = std::make_shared<Pipeline::Impl>(w, h, cfg, ordinal, stream);
+        plans.emplace_front(key, p);
+        while (plans.size() > kMaxPlans) plans.pop_back();
+        return p;
+    }
+};
+
+Device::Device(int ordinal) : impl_(new Impl) {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw DeviceError(std::string("no CUDA device available (") +
+                          (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                          "); the B200 pipeline has no CPU fallback");
+    }
+    if (ordinal < 0 || ordinal >= n) throw DeviceError("CUDA device ordinal out of range");
+    impl_->ordinal = ordinal;
+    CK(cudaSetDevice(ordinal));
+    CK(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
+}
+
+Device::~Device() {
+    if (impl_) {
+        impl_->plans.clear();
+        cudaSetDevice(impl_->ordinal);
+        if (impl_->stream) cudaStreamDestroy(impl_->stream);
+    }
+}
+
+int Device::ordinal() const { return impl_->ordinal; }
+void* Device::stream() const { return impl_->stream; }
+
+Device& Device::current() {
+    thread_local std::map<int, std::unique_ptr<Device>> devices;
+    int ord = 0;
+    const cudaError_t e = cudaGetDevice(&ord);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw DeviceError(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                          "); the B200 pipeline has no CPU fallback");
+    }
+    auto it = devices.find(ord);
+    if (it == devices.end()) it = devices.emplace(ord, std::make_unique<Device>(ord)).first;
+    CK(cudaSetDevice(ord));
+    return *it->second;
+}
+
+
+// ==========================================================================================
+// Pipeline (device-resident; owns its plan and stream, so several pipelines on one
+// device overlap freely)
+// ==========================================================================================
+Pipeline::Pipeline(int width, int height, const ConversionConfig& cfg, Device& dev) {
+    CK(cudaSetDevice(dev.ordinal()));
+    cudaStream_t st = nullptr;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+        impl_ = std::make_shared<Impl>(width, height, cfg, dev.ordinal(), st);
+    } catch (...) {
+        cudaStreamDestroy(st);
+        throw;
+    }
+    impl_->own_stream = true;
+}
+Pipeline::~Pipeline() = default;
+int Pipeline::pitch() const { return impl_->pitch; }
+int Pipeline::width() const { return impl_->w; }
+int Pipeline::height() const { return impl_->h; }
+void* Pipeline::stream() const { return impl_->stream; }
+std::size_t Pipeline::frame_bytes() const { return 3 * impl_->plane(); }
+void Pipeline::run(const std::uint8_t* d_src, void* stream) {
+    impl_->run(d_src, stream ? static_cast<cudaStream_t>(stream) : impl_->stream, false);
+}
+void Pipeline::run_timed(const std::uint8_t* d_src, void* stream) {
+    impl_->run(d_src, stream ? static_cast<cudaStream_t>(stream) : impl_->stream, true);
+}
+StageTimings Pipeline::last_timings() { return impl_->timings(); }
+StageTimings Pipeline::accumulated_timings(long long* count, bool reset) {
+    return impl_->accumulated(count, reset);
+}
+const std::uint8_t* Pipeline::d_depth() const { return impl_->depth; }
+const std::uint8_t* Pipeline::d_filtered() const { return impl_->filt; }
+const std::uint8_t* Pipeline::d_output(StereoFormat f) const { return impl_->output(f); }
+int Pipeline::output_pitch(StereoFormat f) const { return impl_->output_pitch(f); }
+void Pipeline::download(ConversionResult& out, void* stream) {
+    impl_->download(out, stream ? static_cast<cudaStream_t>(stream) : impl_->stream);
+}
+void Pipeline::inpaint_stats(InpaintStats& left, InpaintStats& right) {
+    long long s[6];
+    CK(cudaMemcpyAsync(s, impl_->stats, sizeof(s), cudaMemcpyDeviceToHost, impl_->stream));
+    CK(cudaStreamSynchronize(impl_->stream));
+    left = InpaintStats{static_cast<int>(s[0]), static_cast<std::size_t>(s[1]),
+                        static_cast<std::size_t>(s[2])};
+    right = InpaintStats{static_cast<int>(s[3]), static_cast<std::size_t>(s[4]),
+                         static_cast<std::size_t>(s[5])};
+}
+
+std::uint8_t* Pipeline::d_input() { return impl_->src; }
+void Pipeline::upload(const std::uint8_t* r, const std::uint8_t* g, const std::uint8_t* b,
+                      std::uint8_t* d_dst, void* stream) {
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : impl_->stream;
+    const std::uint8_t* planes[3] = {r, g, b};
+    for (int c = 0; c < 3; ++c) impl_->h2d_plane(d_dst + c * impl_->plane(), planes[c], st);
+}
+void Pipeline::download_to(std::uint8_t* depth, std::uint8_t* filtered, StereoFormat f,
+                           std::uint8_t* const* out, void* stream, bool sync) {
+    Impl& p = *impl_;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
+    if (depth) p.d2h_plane(depth, p.depth, p.pitch, p.w, st);
+    if (filtered) p.d2h_plane(filtered, p.filt, p.pitch, p.w, st);
+    if (out && (p.formats & f)) {
+        const int ow = p.output_width(f);
+        const std::size_t ps = static_cast<std::size_t>(p.output_pitch(f)) * p.h;
+        for (int c = 0; c < 3; ++c)
+            if (out[c]) p.d2h_plane(out[c], p.output(f) + c * ps, p.output_pitch(f), ow, st);
+    }
+    if (sync) CK(cudaStreamSynchronize(st));
+}
+
+// ==========================================================================================
+// Stage API (each call: H2D, the stage's kernels, D2H, on the thread's device stream)
+// ==========================================================================================
+namespace {
+
+std::shared_ptr<Pipeline::Impl> stage_plan(Device& dev, int w, int h, const ConversionConfig& cfg) {
+    return dev.impl().plan(w, h, cfg);
+}
+
+void upload_image(Pipeline::Impl& p, const ImageRGB8& img, cudaStream_t st) {
+    for (int c = 0; c < 3; ++c) p.h2d_plane(p.src + c * p.plane(), img.plane(c).data(), st);
+}
+
+void require_same(int w0, int h0, int w1, int h1, const char* msg) {
+    if (w0 != w1 || h0 != h1) throw std::invalid_argument(msg);
+}
+
+}  // namespace
+
+GrayMap luma(const ImageRGB8& img, Device& dev) {
+    ConversionConfig cfg;
+    auto p = stage_plan(dev, img.width, img.height, cfg);
+    cudaStream_t st = p->stream;
+    upload_image(*p, img, st);
+    p->enq_depth(p->src, st);
+    GrayMap out(img.width, img.height, false);
+    p->d2h_plane(out.data.data(), p->luma, p->pitch, p->w, st);
+    CK(cudaStreamSynchronize(st));
+    return out;
+}
+
+BlockGrid block_depth(const ImageRGB8& img, const ConversionConfig& cfg, Device& dev) {
+    cfg.validate();
+    auto p = stage_plan(dev, img.width, img.height, cfg);
+    cudaStream_t st = p->stream;
+    upload_image(*p, img, st);
+    p->enq_depth(p->src, st);
+    BlockGrid g;
+    g.block = cfg.depth_block;
+    g.width = img.width;
+    g.height = img.height;
+    g.blocks_x = p->dt.bx;
+    g.blocks_y = p->dt.by;
+    g.values.resize(static_cast<std::size_t>(g.blocks_x) * g.blocks_y);
+    CK(cudaMemcpyAsync(g.values.data(), p->values, g.values.size() * sizeof(double),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return g;
+}
+
+GrayMap upsample_block_grid(const BlockGrid& grid, Device& dev) {
+    ConversionConfig cfg;
+    cfg.depth_block = grid.block;
+    auto p = stage_plan(dev, grid.width, grid.height, cfg);
+    cudaStream_t st = p->stream;
+    if (grid.values.size() != static_cast<std::size_t>(p->dt.bx) * p->dt.by)
+        throw std::invalid_argument("upsample_block_grid: grid size mismatch");
+    CK(cudaMemcpyAsync(p->values, grid.values.data(), grid.values.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, st));
+    CK(cu::upsample(p->values, p->gm, p->dt, p->depth, st));
+    GrayMap out(grid.width, grid.height, false);
+    p->d2h_plane(out.data.data(), p->depth, p->pitch, p->w, st);
+    CK(cudaStreamSynchronize(st));
+    return out;
+}
+
+GrayMap generate_depth(const ImageRGB8& img, const ConversionConfig& cfg, Device& dev) {
+    cfg.validate();
+    auto p = stage_plan(dev, img.width, img.height, cfg);
+    cudaStream_t st = p->stream;
+    upload_image(*p, img, st);
+    p->enq_depth(p->src, st);
+    GrayMap out(img.width, img.height, false);
+    p->d2h_plane(out.data.data(), p->depth, p->pitch, p->w, st);
+    CK(cudaStreamSynchronize(st));
+    return out;
+}
+
+static void bilateral_common(const GrayMap& depth, const GrayMap& guide,
+                             const ConversionConfig& cfg, Device& dev, GrayMap* out,
+                             std::vector<double>* raw) {
+    require_same(depth.width, depth.height, guide.width, guide.height,
+                 "cross_bilateral: depth and guide dimensions differ");
+    auto p = stage_plan(dev, depth.width, depth.height, cfg);
+    cudaStream_t st = p->stream;
+    p->h2d_plane(p->depth, depth.data.data(), st);
+    p->h2d_plane(p->luma, guide.data.data(), st);
+    double* d_raw = nullptr;
+    if (raw) {
+        p->ensure_stage();
+        d_raw = p->stage_raw;
+    }
+    p->enq_bilateral(p->depth, p->luma, p->filt, d_raw, st);
+    if (out) {
+        *out = GrayMap(depth.width, depth.height, false);
+        p->d2h_plane(out->data.data(), p->filt, p->pitch, p->w, st);
+    }
+    if (raw) {
+        raw->resize(p->npix());
+        CK(cudaMemcpyAsync(raw->data(), d_raw, p->npix() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+}
+
+GrayMap cross_bilateral(const GrayMap& depth, const GrayMap& guide, const ConversionConfig& cfg,
+                        Device& dev) {
+    GrayMap out;
+    bilateral_common(depth, guide, cfg, dev, &out, nullptr);
+    return out;
+}
+
+std::vector<double> cross_bilateral_raw(const GrayMap& depth, const GrayMap& guide,
+                                        const ConversionConfig& cfg, Device& dev) {
+    std::vector<double> raw;
+    bilateral_common(depth, guide, cfg, dev, nullptr, &raw);
+    return raw;
+}
+
+StereoFrames reconstruct(const ImageRGB8& src, const GrayMap& depth, const ConversionConfig& cfg,
+                         Device& dev) {
+    require_same(src.width, src.height, depth.width, depth.height,
+                 "reconstruct: source and depth dimensions differ");
+    // The stage API materialises both eye frames and byte masks (reference StereoFrames).
+    ConversionConfig c = cfg;
+    c.formats = kFormatAnaglyph | kFormatHsbs;  // forces the materialised-eyes route
+    auto p = stage_plan(dev, src.width, src.height, c);
+    p->ensure_stage();
+    cudaStream_t st = p->stream;
+    upload_image(*p, src, st);
+    p->h2d_plane(p->filt, depth.data.data(), st);
+    cu::EyeOut eo[2];
+    for (int e = 0; e < 2; ++e) {
+        for (int ch = 0; ch < 3; ++ch) eo[e].plane[ch] = p->eyes + (3 * e + ch) * p->plane();
+        eo[e].pitch = p->pitch;
+        eo[e].mask_bytes = p->stage_masks + e * p->plane();
+        eo[e].mask_bits = nullptr;
+        eo[e].mask_pitch = p->pitch;
+        eo[e].list = nullptr;
+        eo[e].count = p->counts + e;
+    }
+    CK(cu::dibr(p->src, p->src + p->plane(), p->src + 2 * p->plane(), p->filt, p->gm, p->shift,
+                p->backward, eo[0], eo[1], st));
+    StereoFrames f;
+    f.left = ImageRGB8(src.width, src.height, false);
+    f.right = ImageRGB8(src.width, src.height, false);
+    f.left_mask = DamageMask(src.width, src.height);
+    f.right_mask = DamageMask(src.width, src.height);
+    for (int ch = 0; ch < 3; ++ch) {
+        p->d2h_plane(f.left.plane(ch).data(), eo[0].plane[ch], p->pitch, p->w, st);
+        p->d2h_plane(f.right.plane(ch).data(), eo[1].plane[ch], p->pitch, p->w, st);
+    }
+    p->d2h_plane(f.left_mask.damaged.data(), eo[0].mask_bytes, p->pitch, p->w, st);
+    p->d2h_plane(f.right_mask.damaged.data(), eo[1].mask_bytes, p->pitch, p->w, st);
+    CK(cudaStreamSynchronize(st));
+    return f;
+}
+
+ImageRGB8 inpaint(const ImageRGB8& frame, const DamageMask& mask, const ConversionConfig& cfg,
+                  Device& dev, InpaintStats* stats) {
+    require_same(frame.width, frame.height, mask.width, mask.height,
+                 "inpaint: frame and mask dimensions differ");
+    ConversionConfig c = cfg;
+    c.dibr_mode = DibrMode::kForwardZBuffer;  // the plan needs its work lists
+    c.formats = kFormatAnaglyph | kFormatHsbs;
+    auto p = stage_plan(dev, frame.width, frame.height, c);
+    p->ensure_stage();
+    cudaStream_t st = p->stream;
+    // left eye = the frame; the right eye gets an empty list
+    for (int ch = 0; ch < 3; ++ch) p->h2d_plane(p->eyes + ch * p->plane(), frame.plane(ch).data(), st);
+    p->h2d_plane(p->stage_masks, mask.damaged.data(), st);
+    CK(cudaMemsetAsync(p->counts, 0, 2 * sizeof(uint32_t), st));
+    CK(cu::mask_to_list(p->stage_masks, p->pitch, p->gm, p->list_ptr(0, 0), p->counts, st));
+    cu::InpaintEye ie[2];
+    for (int e = 0; e < 2; ++e) {
+        for (int ch = 0; ch < 3; ++ch) ie[e].plane[ch] = p->eyes + (3 * e + ch) * p->plane();
+        ie[e].pitch = p->pitch;
+        ie[e].mask_bytes = p->stage_masks + e * p->plane();
+        ie[e].mask_bits = nullptr;
+        ie[e].mask_pitch = p->pitch;
+        ie[e].list = p->list_ptr(e, 0);
+        ie[e].count = p->counts + e;
+        ie[e].list2 = p->list_ptr(e, 1);
+        ie[e].repair = p->list_ptr(e, 2);
+    }
+    CK(cu::inpaint(ie[0], ie[1], p->gm, static_cast<uint32_t>(p->npix()), p->ctl, p->stats, st));
+    ImageRGB8 out(frame.width, frame.height, false);
+    for (int ch = 0; ch < 3; ++ch)
+        p->d2h_plane(out.plane(ch).data(), p->eyes + ch * p->plane(), p->pitch, p->w, st);
+    long long s[6];
+    CK(cudaMemcpyAsync(s, p->stats, sizeof(s), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (stats) *stats = InpaintStats{static_cast<int>(s[0]), static_cast<std::size_t>(s[1]),
+                                     static_cast<std::size_t>(s[2])};
+    return out;
+}
+
+static ImageRGB8 format_common(const ImageRGB8& left, const ImageRGB8& right, unsigned fmt,
+                               Device& dev) {
+    ConversionConfig c;
+    c.formats = kFormatAnaglyph | kFormatHsbs | kFormatFsbs;
+    auto p = stage_plan(dev, left.width, left.height, c);
+    cudaStream_t st = p->stream;
+    for (int ch = 0; ch < 3; ++ch) {
+        p->h2d_plane(p->eyes + ch * p->plane(), left.plane(ch).data(), st);
+        p->h2d_plane(p->eyes + (3 + ch) * p->plane(), right.plane(ch).data(), st);
+    }
+    const unsigned saved = p->formats;
+    p->formats = fmt;
+    try {
+        p->enq_formats(st);
+    } catch (...) {
+        p->formats = saved;
+        throw;
+    }
+    p->formats = saved;
+    const StereoFormat f = static_cast<StereoFormat>(fmt);
+    const int ow = p->output_width(f);
+    ImageRGB8 out(ow, left.height, false);
+    const std::size_t ps = static_cast<std::size_t>(p->output_pitch(f)) * p->h;
+    for (int ch = 0; ch < 3; ++ch)
+        p->d2h_plane(out.plane(ch).data(), p->output(f) + ch * ps, p->output_pitch(f), ow, st);
+    CK(cudaStreamSynchronize(st));
+    return out;
+}
+
+ImageRGB8 anaglyph(const ImageRGB8& left, const ImageRGB8& right, Device& dev) {
+    require_same(left.width, left.height, right.width, right.height,
+                 "anaglyph: eye dimensions differ");
+    return format_common(left, right, kFormatAnaglyph, dev);
+}
+
+ImageRGB8 side_by_side(const ImageRGB8& left, const ImageRGB8& right, bool half, Device& dev) {
+    require_same(left.width, left.height, right.width, right.height,
+                 "side_by_side: eye dimensions differ");
+    if (half && left.width % 2 != 0)
+        throw std::invalid_argument("side_by_side: half mode requires an even width");
+    return format_common(left, right, half ? kFormatHsbs : kFormatFsbs, dev);
+}
+
+ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg, Device& dev) {
+    cfg.validate();
+    auto p = stage_plan(dev, src.width, src.height, cfg);
+    cudaStream_t st = p->stream;
+    upload_image(*p, src, st);
+    p->run(p->src, st, true);
+    ConversionResult res;
+    p->download(res, st);
+    res.timings = p->timings();
+    return res;
+}
+
+}  // namespace p3s

@@ -1,0 +1,249 @@
+// Frame-sequence driver (reference proj/src/sequence.cpp:13-145) around the GPU pipeline.
+//
+// Same contract: frames <pattern> from index 0 (or 1 when frame 0 is missing) up to the
+// first gap, outputs <stem>_<format>.ppm, one CSV row per frame, SequenceError naming the
+// failing frame with every earlier output already on disk. Unlike the reference's strictly
+// serial loop, file read + PPM decode of frame i+1 and encode + write of frame i-1 run on
+// host threads while frame i is on the GPU, so disk/codec time hides behind the device.
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <exception>
+#include <filesystem>
+#include <functional>
+#include <mutex>
+#include <sstream>
+#include <thread>
+
+#include "p3s_host.hpp"
+
+namespace p3s {
+
+std::int64_t SequenceReport::pure_sum_ns() const {
+    std::int64_t s = 0;
+    for (const auto& f : frames) s += f.timings.pure_ns();
+    return s;
+}
+std::int64_t SequenceReport::pure_min_ns() const {
+    std::int64_t best = 0;
+    for (std::size_t i = 0; i < frames.size(); ++i) {
+        const std::int64_t v = frames[i].timings.pure_ns();
+        if (i == 0 || v < best) best = v;
+    }
+    return best;
+}
+std::int64_t SequenceReport::pure_max_ns() const {
+    std::int64_t best = 0;
+    for (const auto& f : frames) best = std::max(best, f.timings.pure_ns());
+    return best;
+}
+double SequenceReport::pure_mean_ns() const {
+    return frames.empty() ? 0.0 : static_cast<double>(pure_sum_ns()) / frames.size();
+}
+std::string SequenceReport::to_csv(int threads) const {
+    std::ostringstream os;
+    os << "frame,width,height,threads,depth_ns,filter_ns,dibr_ns,inpaint_l_ns,inpaint_r_ns,"
+          "format_ns,pure_ns\n";
+    for (const auto& f : frames) {
+        const StageTimings& t = f.timings;
+        os << f.index << ',' << f.width << ',' << f.height << ',' << threads << ','
+           << t.depth_gen_ns << ',' << t.filter_ns << ',' << t.dibr_ns << ',' << t.inpaint_left_ns
+           << ',' << t.inpaint_right_ns << ',' << t.format_ns << ',' << t.pure_ns() << '\n';
+    }
+    return os.str();
+}
+
+// sequence.cpp:85-117
+FramePattern FramePattern::parse(const std::string& pattern) {
+    const std::size_t pct = pattern.find('%');
+    if (pct == std::string::npos)
+        throw std::invalid_argument("frame pattern needs one %d or %0Nd field: " + pattern);
+    std::size_t pos = pct + 1;
+    int pad = 0;
+    while (pos < pattern.size() && pattern[pos] >= '0' && pattern[pos] <= '9')
+        pad = pad * 10 + (pattern[pos++] - '0');
+    if (pos >= pattern.size() || pattern[pos] != 'd')
+        throw std::invalid_argument("frame pattern needs one %d or %0Nd field: " + pattern);
+    if (pattern.find('%', pos) != std::string::npos)
+        throw std::invalid_argument("frame pattern must contain exactly one % field: " + pattern);
+    FramePattern fp;
+    fp.prefix_ = pattern.substr(0, pct);
+    fp.suffix_ = pattern.substr(pos + 1);
+    fp.pad_ = pad;
+    return fp;
+}
+
+std::string FramePattern::filename(std::int64_t index) const {
+    std::string digits = std::to_string(index);
+    if (static_cast<int>(digits.size()) < pad_) digits.insert(0, pad_ - digits.size(), '0');
+    return prefix_ + digits + suffix_;
+}
+
+std::string FramePattern::stem(std::int64_t index) const {
+    const std::string name = filename(index);
+    const std::size_t dot = name.rfind('.');
+    return dot == std::string::npos ? name : name.substr(0, dot);
+}
+
+int resolve_threads(int threads) {
+    if (threads > 0) return threads;
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw > 0 ? static_cast<int>(hw) : 1;
+}
+
+namespace {
+
+// Single-producer single-consumer bounded queue of tasks.
+class Worker {
+public:
+    explicit Worker(std::size_t cap) : cap_(cap), th_([this] { loop(); }) {}
+    ~Worker() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    void push(std::function<void()> f) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return q_.size() < cap_ || err_; });
+        q_.push_back(std::move(f));
+        cv_.notify_all();
+    }
+    void drain() {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return q_.empty() && !busy_; });
+    }
+    std::exception_ptr error() {
+        std::lock_guard<std::mutex> lk(mu_);
+        return err_;
+    }
+
+private:
+    void loop() {
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                if (q_.empty()) return;
+                f = std::move(q_.front());
+                q_.pop_front();
+                busy_ = true;
+            }
+            try {
+                if (!err_) f();
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu_);
+                err_ = std::current_exception();
+            }
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                busy_ = false;
+            }
+            cv_.notify_all();
+        }
+    }
+    std::size_t cap_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    bool stop_ = false, busy_ = false;
+    std::exception_ptr err_;
+    std::thread th_;
+};
+
+struct Loaded {
+    std::int64_t index = 0;
+    bool present = false;
+    std::vector<std::uint8_t> bytes;
+    std::exception_ptr read_error;
+};
+
+}  // namespace
+
+SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string& pattern,
+                                    const std::string& out_dir, const ConversionConfig& cfg,
+                                    int threads) {
+    (void)threads;
+    cfg.validate();
+    namespace fs = std::filesystem;
+    const FramePattern in_pat = FramePattern::parse(pattern);
+    const FramePattern out_pat = FramePattern::parse(pattern);
+    SequenceReport report;
+    const auto wall0 = std::chrono::steady_clock::now();
+
+    std::int64_t next = 0;
+    if (!fs::exists(fs::path(in_dir) / in_pat.filename(0)) &&
+        fs::exists(fs::path(in_dir) / in_pat.filename(1)))
+        next = 1;
+    auto load = [&](std::int64_t idx) {
+        Loaded l;
+        l.index = idx;
+        const fs::path path = fs::path(in_dir) / in_pat.filename(idx);
+        if (!fs::exists(path)) return l;
+        l.present = true;
+        try {
+            l.bytes = read_file(path.string());
+        } catch (...) {
+            l.read_error = std::current_exception();
+        }
+        return l;
+    };
+
+    Device& dev = Device::current();
+    Worker writer(2);
+    std::int64_t written = 0;
+    std::mutex written_mu;
+    Loaded cur = load(next);
+    while (cur.present) {
+        // prefetch the next frame's bytes while this one converts
+        Loaded nxt;
+        std::thread pre([&] { nxt = load(cur.index + 1); });
+        struct Join {
+            std::thread& t;
+            ~Join() {
+                if (t.joinable()) t.join();
+            }
+        } join{pre};
+        if (cur.read_error) {
+            writer.drain();
+            std::rethrow_exception(cur.read_error);
+        }
+        ImageRGB8 frame;
+        try {
+            frame = decode_ppm(cur.bytes.data(), cur.bytes.size());
+        } catch (const PnmError& e) {
+            writer.drain();
+            if (auto err = writer.error()) std::rethrow_exception(err);
+            std::lock_guard<std::mutex> lk(written_mu);
+            throw SequenceError(cur.index, written,
+                                "frame " + std::to_string(cur.index) + ": " + e.what());
+        }
+        auto result = std::make_shared<ConversionResult>(convert_image(frame, cfg, dev));
+        report.frames.push_back({cur.index, frame.width, frame.height, result->timings});
+        if (auto err = writer.error()) std::rethrow_exception(err);
+        const std::int64_t idx = cur.index;
+        writer.push([&, result, idx] {
+            for (const auto& [fmt, img] : result->outputs) {
+                const std::string name = out_pat.stem(idx) + "_" + format_name(fmt) + ".ppm";
+                const std::vector<std::uint8_t> bytes = encode_ppm(img);
+                write_file((fs::path(out_dir) / name).string(), bytes.data(), bytes.size());
+                std::lock_guard<std::mutex> lk(written_mu);
+                ++written;
+            }
+        });
+        pre.join();
+        cur = std::move(nxt);
+    }
+    writer.drain();
+    if (auto err = writer.error()) std::rethrow_exception(err);
+    report.wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                         std::chrono::steady_clock::now() - wall0)
+                         .count();
+    return report;
+}
+
+}  // namespace p3s

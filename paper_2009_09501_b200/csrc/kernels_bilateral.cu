@@ -1,0 +1,283 @@
+// K2: exact FP64 cross-bilateral filter on sm_100a (reference proj/src/bilateral.cpp:40-116).
+//
+// Bit-exactness contract (SURVEY.md §7 rule 3): for every output pixel the taps are
+// accumulated in the reference's order — window rows dy ascending over the clipped
+// window, in each row the centre tap, then dx = 1..r as a mirrored pair
+// (ws += wl + wr; vs += wl*dL + wr*dR) or a single side at the image border — with every
+// multiply and add separately rounded (__dmul_rn/__dadd_rn; no FMA). The spatial and
+// range tables are computed on the host with the reference's libm exp (engine.cpp).
+//
+// Layout: a CTA is 8 warps; a warp owns 32 adjacent columns x P rows and each thread one
+// column of P outputs (vertical register blocking). A (32+2r) x (8P+2r) tile of packed
+// (depth<<8 | guide) u16 is staged in shared memory, so every loaded neighbour pair is
+// reused by all P outputs of the thread (guide/depth loads amortised P-fold). The range
+// table lives in shared memory replicated 16 ways ([d][lane & 15]) so the per-tap
+// random-index LDS.64 is bank-conflict free. The spatial table is a __grid_constant__
+// kernel parameter indexed with warp-uniform offsets (constant-bank operands), so each
+// launch carries its own table and concurrent configs cannot race. Persistent CTAs walk
+// the tile list so the range table is staged once per CTA.
+//
+// Image-border clipping in x uses a zero-weight sentinel: out-of-image taps read range
+// entry 256 (= 0.0), and 0.0*x + y == y exactly, so a half-clipped pair reproduces the
+// reference's single-sided update bit for bit. Clipping in y is done by the row loop
+// bounds. Rows of a warp's window where only some outputs are inside their window are
+// run with warp-uniform per-output predicates; the bulk rows run branch-free.
+#include "p3s_cu.h"
+
+namespace p3s {
+namespace cu {
+namespace {
+
+constexpr int kTX = 32;
+constexpr int kNW = 8;
+constexpr int kP = 8;  // outputs per thread (rows)
+constexpr int kTY = kNW * kP;
+constexpr int kRangeCopies = 16;
+constexpr int kRangeEntries = 257;  // 256 + zero sentinel
+
+template <int N>
+struct __align__(8) SpatialParam {
+    double s[N];
+};
+
+__device__ __forceinline__ uint8_t round_half_up_u8(double v) {
+    const double r = floor(__dadd_rn(v, 0.5));
+    if (r <= 0.0) return 0;
+    if (r >= 255.0) return 255;
+    return static_cast<uint8_t>(static_cast<int>(r));
+}
+
+// One window row (t = yq - yb + R) for the P outputs of this thread. Output i is inside
+// its window iff 0 <= t - i <= 2R. ALL: every output is (the bulk rows), no predicates.
+template <bool ALL, bool EDGE, int N>
+__device__ __forceinline__ void bil_row(const SpatialParam<N>& sp, const uint16_t* __restrict__ row,
+                                        const double* __restrict__ rng, int t, int R, int x,
+                                        int w, const int (&gi)[kP], double (&ws)[kP],
+                                        double (&vs)[kP]) {
+    const int side = R + 1;
+    {
+        const unsigned c = row[0];
+        const int gc = c & 0xFF;
+        const double dc = static_cast<double>(c >> 8);
+#pragma unroll
+        for (int i = 0; i < kP; ++i) {
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const double s = sp.s[(t - i) * side];
+            const double wc = __dmul_rn(s, rng[__usad(gi[i], gc, 0) * kRangeCopies]);
+            ws[i] = __dadd_rn(ws[i], wc);
+            vs[i] = __dadd_rn(vs[i], __dmul_rn(wc, dc));
+        }
+    }
+#pragma unroll 2
+    for (int dx = 1; dx <= R; ++dx) {
+        const unsigned a = row[-dx], b = row[dx];
+        const int ga = a & 0xFF, gb = b & 0xFF;
+        const double da = static_cast<double>(a >> 8), db = static_cast<double>(b >> 8);
+        const bool oob_l = EDGE && (x - dx < 0);
+        const bool oob_r = EDGE && (x + dx >= w);
+#pragma unroll
+        for (int i = 0; i < kP; ++i) {
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const double s = sp.s[(t - i) * side + dx];
+            const int il = oob_l ? 256 : static_cast<int>(__usad(gi[i], ga, 0));
+            const int ir = oob_r ? 256 : static_cast<int>(__usad(gi[i], gb, 0));
+            const double wl = __dmul_rn(s, rng[il * kRangeCopies]);
+            const double wr = __dmul_rn(s, rng[ir * kRangeCopies]);
+            ws[i] = __dadd_rn(ws[i], __dadd_rn(wl, wr));
+            vs[i] = __dadd_rn(vs[i], __dadd_rn(__dmul_rn(wl, da), __dmul_rn(wr, db)));
+        }
+    }
+}
+
+template <bool EDGE, int N>
+__device__ __forceinline__ void bil_rows(const SpatialParam<N>& sp, const uint16_t* tile_col,
+                                         int SW, const double* rng, int R, int x, int w, int tlo,
+                                         int thi, const int (&gi)[kP], double (&ws)[kP],
+                                         double (&vs)[kP]) {
+    // Rows t in [P-1, 2R] have every output inside its window; the ramps before and after
+    // (and everything when 2R < P-1) run predicated. t ascends throughout, which is the
+    // reference's dy-ascending order for every output.
+    const int full_lo = kP - 1, full_hi = 2 * R;
+    int t = tlo;
+    for (; t <= min(full_lo - 1, thi); ++t)
+        bil_row<false, EDGE>(sp, tile_col + t * SW, rng, t, R, x, w, gi, ws, vs);
+    for (; t <= min(full_hi, thi); ++t)
+        bil_row<true, EDGE>(sp, tile_col + t * SW, rng, t, R, x, w, gi, ws, vs);
+    for (; t <= thi; ++t)
+        bil_row<false, EDGE>(sp, tile_col + t * SW, rng, t, R, x, w, gi, ws, vs);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kNW * 32) k_bilateral_tiled(
+    const __grid_constant__ SpatialParam<N> sp, const uint8_t* __restrict__ depth,
+    const uint8_t* __restrict__ guide, int pitch, int w, int h, int R,
+    const double* __restrict__ range_g, uint8_t* __restrict__ out, double* __restrict__ raw,
+    int tiles_x, int ntiles) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* s_rng = reinterpret_cast<double*>(smem);
+    uint16_t* s_tile = reinterpret_cast<uint16_t*>(smem + kRangeEntries * kRangeCopies * 8);
+    const int SW = kTX + 2 * R;
+    const int SH = kTY + 2 * R;
+
+    for (int i = threadIdx.x; i < kRangeEntries * kRangeCopies; i += blockDim.x) {
+        const int d = i / kRangeCopies;
+        s_rng[i] = d < 256 ? range_g[d] : 0.0;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* rng = s_rng + (lane & (kRangeCopies - 1));
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tx0 = (tile % tiles_x) * kTX;
+        const int ty0 = (tile / tiles_x) * kTY;
+        __syncthreads();
+        for (int sy = warp; sy < SH; sy += kNW) {
+            const int gy = ty0 - R + sy;
+            const bool yin = gy >= 0 && gy < h;
+            const uint8_t* grow = guide + static_cast<size_t>(yin ? gy : 0) * pitch;
+            const uint8_t* drow = depth + static_cast<size_t>(yin ? gy : 0) * pitch;
+            for (int sx = lane; sx < SW; sx += 32) {
+                const int gx = tx0 - R + sx;
+                unsigned v = 0;
+                if (yin && gx >= 0 && gx < w) v = grow[gx] | (static_cast<unsigned>(drow[gx]) << 8);
+                s_tile[sy * SW + sx] = static_cast<uint16_t>(v);
+            }
+        }
+        __syncthreads();
+
+        const int x = tx0 + lane;
+        const int yb = ty0 + warp * kP;
+        if (yb >= h) continue;
+        const bool edge = (tx0 - R < 0) || (tx0 + kTX - 1 + R >= w);
+        // tile column of this thread, at the smem row of t = 0 (yq = yb - R)
+        const uint16_t* tile_col = s_tile + (warp * kP) * SW + lane + R;
+        int gi[kP];
+        double ws[kP], vs[kP];
+#pragma unroll
+        for (int i = 0; i < kP; ++i) {
+            gi[i] = tile_col[(i + R) * SW] & 0xFF;
+            ws[i] = 0.0;
+            vs[i] = 0.0;
+        }
+        const int tlo = max(0, R - yb);
+        const int thi = min(kP - 1 + 2 * R, h - 1 - yb + R);
+        if (edge)
+            bil_rows<true>(sp, tile_col, SW, rng, R, x, w, tlo, thi, gi, ws, vs);
+        else
+            bil_rows<false>(sp, tile_col, SW, rng, R, x, w, tlo, thi, gi, ws, vs);
+        if (x < w) {
+#pragma unroll
+            for (int i = 0; i < kP; ++i) {
+                const int y = yb + i;
+                if (y < h) {
+                    const double v = __ddiv_rn(vs[i], ws[i]);
+                    out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(v);
+                    if (raw) raw[static_cast<size_t>(y) * w + x] = v;
+                }
+            }
+        }
+    }
+}
+
+// Any radius: one thread per output, tables and pixels read through the L1 path.
+__global__ void __launch_bounds__(256) k_bilateral_generic(
+    const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
+    int h, int R, const double* __restrict__ spatial, const double* __restrict__ range_g,
+    uint8_t* __restrict__ out, double* __restrict__ raw) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= w) return;
+    const int side = R + 1;
+    const int gp = guide[static_cast<size_t>(y) * pitch + x];
+    double ws = 0.0, vs = 0.0;
+    const int dy0 = y - R < 0 ? -y : -R;
+    const int dy1 = y + R >= h ? h - 1 - y : R;
+    for (int dy = dy0; dy <= dy1; ++dy) {
+        const uint8_t* grow = guide + static_cast<size_t>(y + dy) * pitch;
+        const uint8_t* drow = depth + static_cast<size_t>(y + dy) * pitch;
+        const double* s = spatial + static_cast<size_t>(dy + R) * side;
+        {
+            const double wc = __dmul_rn(s[0], range_g[__usad(gp, grow[x], 0)]);
+            ws = __dadd_rn(ws, wc);
+            vs = __dadd_rn(vs, __dmul_rn(wc, static_cast<double>(drow[x])));
+        }
+        for (int dx = 1; dx <= R; ++dx) {
+            const bool lin = x - dx >= 0, rin = x + dx < w;
+            if (lin && rin) {
+                const double wl = __dmul_rn(s[dx], range_g[__usad(gp, grow[x - dx], 0)]);
+                const double wr = __dmul_rn(s[dx], range_g[__usad(gp, grow[x + dx], 0)]);
+                ws = __dadd_rn(ws, __dadd_rn(wl, wr));
+                vs = __dadd_rn(vs, __dadd_rn(__dmul_rn(wl, static_cast<double>(drow[x - dx])),
+                                             __dmul_rn(wr, static_cast<double>(drow[x + dx]))));
+            } else if (lin) {
+                const double wl = __dmul_rn(s[dx], range_g[__usad(gp, grow[x - dx], 0)]);
+                ws = __dadd_rn(ws, wl);
+                vs = __dadd_rn(vs, __dmul_rn(wl, static_cast<double>(drow[x - dx])));
+            } else if (rin) {
+                const double wr = __dmul_rn(s[dx], range_g[__usad(gp, grow[x + dx], 0)]);
+                ws = __dadd_rn(ws, wr);
+                vs = __dadd_rn(vs, __dmul_rn(wr, static_cast<double>(drow[x + dx])));
+            }
+        }
+    }
+    const double v = __ddiv_rn(vs, ws);
+    out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(v);
+    if (raw) raw[static_cast<size_t>(y) * w + x] = v;
+}
+
+template <int N>
+cudaError_t launch_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm, int R,
+                         const double* spatial_host_order, const double* range, uint8_t* out,
+                         double* raw, cudaStream_t st) {
+    SpatialParam<N> sp;
+    const int n = (2 * R + 1) * (R + 1);
+    for (int i = 0; i < n; ++i) sp.s[i] = spatial_host_order[i];
+    for (int i = n; i < N; ++i) sp.s[i] = 0.0;
+    const int SW = kTX + 2 * R, SH = kTY + 2 * R;
+    const size_t smem = kRangeEntries * kRangeCopies * 8 + static_cast<size_t>(SW) * SH * 2;
+    static int configured_dev[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured_dev[dev]) {
+        cudaFuncSetAttribute(k_bilateral_tiled<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        configured_dev[dev] = 1;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_tiled<N>, kNW * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int tiles_x = (gm.w + kTX - 1) / kTX;
+    const int tiles_y = (gm.h + kTY - 1) / kTY;
+    const int ntiles = tiles_x * tiles_y;
+    const int grid = min(ntiles, per_sm * sm_count());
+    k_bilateral_tiled<N><<<grid, kNW * 32, smem, st>>>(sp, depth, guide, gm.pitch, gm.w, gm.h, R,
+                                                       range, out, raw, tiles_x, ntiles);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// spatial: device table for the generic kernel, in the layout s[(dy+R)*(R+1)+dx] (dx>=0).
+// The tiled kernels take the same table by value; engine.cpp passes the host copy via
+// bilateral_tiled_host below.
+cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                      const double* spatial, const double* range, uint8_t* out, double* raw,
+                      cudaStream_t st) {
+    dim3 grid((gm.w + 127) / 128, gm.h);
+    k_bilateral_generic<<<grid, 128, 0, st>>>(depth, guide, gm.pitch, gm.w, gm.h, radius,
+                                              spatial, range, out, raw);
+    return cudaGetLastError();
+}
+
+cudaError_t bilateral_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                            const double* spatial_host, const double* range, uint8_t* out,
+                            double* raw, cudaStream_t st) {
+    const int n = (2 * radius + 1) * (radius + 1);
+    if (n <= 1024)
+        return launch_tiled<1024>(depth, guide, gm, radius, spatial_host, range, out, raw, st);
+    return launch_tiled<4000>(depth, guide, gm, radius, spatial_host, range, out, raw, st);
+}
+
+int bilateral_tiled_max_radius() { return 43; }  // (2r+1)(r+1) <= 4000
+
+}  // namespace cu
+}  // namespace p3s

@@ -1,0 +1,233 @@
+// Depth-map stage on sm_100a (reference proj/src/depth.cpp + image.cpp:13-21).
+//
+// K1 depth_front: one CTA per 128x16 pixel tile. R,G,B are read once with 8-byte vector
+// loads (plus a 1-pixel clamped halo), luma is formed in shared memory and written out
+// (it is also the bilateral guide), the 3x3 Sobel magnitude is evaluated from shared
+// memory and reduced straight into per-block edge sums. The edge map itself never
+// touches HBM. Algorithmic traffic: 3N read + N write.
+//
+// Integer arithmetic only in K1, so it is exact by construction. block_values/upsample
+// reproduce the reference's double expressions with explicit round-to-nearest intrinsics
+// (no FMA contraction regardless of compiler flags).
+#include "p3s_cu.h"
+
+namespace p3s {
+namespace cu {
+namespace {
+
+constexpr int kTW = 128;  // tile width (pixels)
+constexpr int kTH = 16;   // tile height
+constexpr int kSW = kTW + 2 + 6;  // smem row stride (halo + pad)
+constexpr int kMaxBX = kTW / 4 + 2;  // local block columns a tile can touch (block >= 4)
+constexpr int kMaxBY = kTH / 4 + 2;
+
+__device__ __forceinline__ int clampi(int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
+
+__device__ __forceinline__ uint8_t luma_px(unsigned r, unsigned g, unsigned b) {
+    return static_cast<uint8_t>((77u * r + 150u * g + 29u * b + 128u) >> 8);
+}
+
+__global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__ R,
+                                                     const uint8_t* __restrict__ G,
+                                                     const uint8_t* __restrict__ B, int pitch,
+                                                     int w, int h, uint8_t* __restrict__ luma,
+                                                     unsigned long long* __restrict__ sums,
+                                                     int block, int bx_total) {
+    __shared__ uint8_t s_y[kTH + 2][kSW];
+    __shared__ unsigned s_sum[kMaxBY][kMaxBX];
+
+    const int x0 = blockIdx.x * kTW;
+    const int y0 = blockIdx.y * kTH;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kMaxBY * kMaxBX; i += blockDim.x) (&s_sum[0][0])[i] = 0u;
+
+    // ---- load R,G,B (tile + clamped 1-px halo) and form luma in smem ----
+    const bool interior_x = x0 >= 1 && x0 + kTW + 1 <= w && (pitch % 8) == 0;
+    if (interior_x) {
+        // 18 rows x 16 chunks of 8 pixels, 8-byte vector loads
+        for (int item = tid; item < (kTH + 2) * 16; item += blockDim.x) {
+            const int sr = item >> 4, c8 = item & 15;
+            const int gy = clampi(y0 - 1 + sr, h - 1);
+            const size_t off = static_cast<size_t>(gy) * pitch + x0 + 8 * c8;
+            const uint2 vr = __ldg(reinterpret_cast<const uint2*>(R + off));
+            const uint2 vg = __ldg(reinterpret_cast<const uint2*>(G + off));
+            const uint2 vb = __ldg(reinterpret_cast<const uint2*>(B + off));
+            const uint8_t* pr = reinterpret_cast<const uint8_t*>(&vr);
+            const uint8_t* pg = reinterpret_cast<const uint8_t*>(&vg);
+            const uint8_t* pb = reinterpret_cast<const uint8_t*>(&vb);
+            uint8_t yv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                yv[k] = luma_px(pr[k], pg[k], pb[k]);
+                s_y[sr][1 + 8 * c8 + k] = yv[k];
+            }
+            const int oy = y0 - 1 + sr;
+            if (sr >= 1 && sr <= kTH && oy < h)
+                *reinterpret_cast<uint2*>(luma + static_cast<size_t>(oy) * pitch + x0 + 8 * c8) =
+                    *reinterpret_cast<const uint2*>(yv);
+        }
+        for (int item = tid; item < (kTH + 2) * 2; item += blockDim.x) {
+            const int sr = item >> 1, side = item & 1;
+            const int gy = clampi(y0 - 1 + sr, h - 1);
+            const int gx = side ? x0 + kTW : x0 - 1;
+            const size_t off = static_cast<size_t>(gy) * pitch + gx;
+            s_y[sr][side ? kTW + 1 : 0] = luma_px(R[off], G[off], B[off]);
+        }
+        __syncthreads();
+    } else {
+        for (int item = tid; item < (kTH + 2) * (kTW + 2); item += blockDim.x) {
+            const int sr = item / (kTW + 2), sc = item % (kTW + 2);
+            const int gy = clampi(y0 - 1 + sr, h - 1);
+            const int gx = clampi(x0 - 1 + sc, w - 1);
+            const size_t off = static_cast<size_t>(gy) * pitch + gx;
+            s_y[sr][sc] = luma_px(R[off], G[off], B[off]);
+        }
+        __syncthreads();
+        for (int item = tid; item < kTH * kTW; item += blockDim.x) {
+            const int r = item / kTW, c = item % kTW;
+            const int oy = y0 + r, ox = x0 + c;
+            if (oy < h && ox < w) luma[static_cast<size_t>(oy) * pitch + ox] = s_y[1 + r][1 + c];
+        }
+    }
+
+    // ---- Sobel magnitude (depth.cpp:21-41) and block sums (depth.cpp:64-67) ----
+    // thread -> row ty, 8 consecutive pixels starting at column 8*c8
+    {
+        const int ty = tid >> 4, c8 = tid & 15;
+        const int oy = y0 + ty;
+        if (oy < h) {
+            const int bx0 = x0 / block, by0 = y0 / block;
+            const int lby = oy / block - by0;
+            unsigned run = 0;
+            int run_bx = -1;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int c = 1 + 8 * c8 + k;  // smem column of this pixel
+                const int ox = x0 + c - 1;
+                if (ox < w) {
+                    const int p00 = s_y[ty][c - 1], p10 = s_y[ty][c], p20 = s_y[ty][c + 1];
+                    const int p01 = s_y[ty + 1][c - 1], p21 = s_y[ty + 1][c + 1];
+                    const int p02 = s_y[ty + 2][c - 1], p12 = s_y[ty + 2][c],
+                              p22 = s_y[ty + 2][c + 1];
+                    const int gx = (p20 + 2 * p21 + p22) - (p00 + 2 * p01 + p02);
+                    const int gy = (p02 + 2 * p12 + p22) - (p00 + 2 * p10 + p20);
+                    int mag = (abs(gx) + abs(gy)) / 4;
+                    mag = mag < 255 ? mag : 255;
+                    const int lbx = ox / block - bx0;
+                    if (lbx != run_bx) {
+                        if (run_bx >= 0 && run) atomicAdd(&s_sum[lby][run_bx], run);
+                        run_bx = lbx;
+                        run = 0;
+                    }
+                    run += static_cast<unsigned>(mag);
+                }
+            }
+            if (run_bx >= 0 && run) atomicAdd(&s_sum[lby][run_bx], run);
+        }
+    }
+    __syncthreads();
+    {
+        const int bx0 = x0 / block, by0 = y0 / block;
+        const int nbx = (min(x0 + kTW, w) - 1) / block - bx0 + 1;
+        const int nby = (min(y0 + kTH, h) - 1) / block - by0 + 1;
+        for (int i = tid; i < nbx * nby; i += blockDim.x) {
+            const int ly = i / nbx, lx = i % nbx;
+            const unsigned v = s_sum[ly][lx];
+            if (v)
+                atomicAdd(&sums[static_cast<size_t>(by0 + ly) * bx_total + bx0 + lx],
+                          static_cast<unsigned long long>(v));
+        }
+    }
+}
+
+// depth.cpp:55-71: value = (alpha*255.0) * (centre/row_denom) + beta * (sum / count).
+__global__ void k_block_values(const unsigned long long* __restrict__ sums, int w, int h,
+                               int block, int bx, int by, double alpha255, double beta,
+                               double row_denom, double* __restrict__ values) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= bx * by) return;
+    const int iy = i / bx, ix = i % bx;
+    const int y0 = iy * block, y1 = min(y0 + block, h);
+    const int xa = ix * block, xb = min(xa + block, w);
+    const double centre = __dadd_rn(static_cast<double>(y0),
+                                    __ddiv_rn(static_cast<double>(y1 - 1 - y0), 2.0));
+    const double ramp = __dmul_rn(alpha255, __ddiv_rn(centre, row_denom));
+    const double mean = __ddiv_rn(static_cast<double>(sums[i]),
+                                  static_cast<double>((y1 - y0) * (xb - xa)));
+    values[i] = __dadd_rn(ramp, __dmul_rn(beta, mean));
+}
+
+__device__ __forceinline__ uint8_t round_half_up_u8(double v) {
+    const double r = floor(__dadd_rn(v, 0.5));
+    if (r <= 0.0) return 0;
+    if (r >= 255.0) return 255;
+    return static_cast<uint8_t>(static_cast<int>(r));
+}
+
+__device__ __forceinline__ double lerp_ref(double a, double b, double f) {
+    // a * (1.0 - f) + b * f, each operation separately rounded (depth.cpp:115-117)
+    return __dadd_rn(__dmul_rn(a, __dsub_rn(1.0, f)), __dmul_rn(b, f));
+}
+
+// depth.cpp:104-120. Thread = 16 consecutive pixels of a row (one 16-byte store).
+__global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ values, int bx,
+                                                  const int* __restrict__ ci0,
+                                                  const int* __restrict__ ci1,
+                                                  const double* __restrict__ cf,
+                                                  const int* __restrict__ ri0,
+                                                  const int* __restrict__ ri1,
+                                                  const double* __restrict__ rf, int w, int h,
+                                                  int pitch, uint8_t* __restrict__ depth) {
+    const int y = blockIdx.y;
+    const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
+    if (x0 >= w) return;
+    const double* top = values + static_cast<size_t>(ri0[y]) * bx;
+    const double* bot = values + static_cast<size_t>(ri1[y]) * bx;
+    const double fy = rf[y];
+    alignas(16) uint8_t px[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int x = min(x0 + k, w - 1);
+        const int a = ci0[x], b = ci1[x];
+        const double fx = cf[x];
+        const double t = lerp_ref(__ldg(top + a), __ldg(top + b), fx);
+        const double u = lerp_ref(__ldg(bot + a), __ldg(bot + b), fx);
+        px[k] = round_half_up_u8(lerp_ref(t, u, fy));
+    }
+    uint8_t* dst = depth + static_cast<size_t>(y) * pitch + x0;
+    if (x0 + 16 <= pitch) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(px);
+    } else {
+        for (int k = 0; k < 16 && x0 + k < w; ++k) dst[k] = px[k];
+    }
+}
+
+}  // namespace
+
+cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
+                        uint8_t* luma, unsigned long long* sums, int block, int bx,
+                        cudaStream_t st) {
+    dim3 grid((gm.w + kTW - 1) / kTW, (gm.h + kTH - 1) / kTH);
+    k_depth_front<<<grid, 256, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, sums, block, bx);
+    return cudaGetLastError();
+}
+
+cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTables& t,
+                         double* values, cudaStream_t st) {
+    const int n = t.bx * t.by;
+    k_block_values<<<(n + 255) / 256, 256, 0, st>>>(sums, gm.w, gm.h, t.block, t.bx, t.by,
+                                                    t.alpha255, t.beta, t.row_denom, values);
+    return cudaGetLastError();
+}
+
+cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_t* depth,
+                     cudaStream_t st) {
+    const int threads = 256;
+    dim3 grid((gm.w + threads * 16 - 1) / (threads * 16), gm.h);
+    k_upsample<<<grid, threads, 0, st>>>(values, t.bx, t.col_i0, t.col_i1, t.col_f, t.row_i0,
+                                         t.row_i1, t.row_f, gm.w, gm.h, gm.pitch, depth);
+    return cudaGetLastError();
+}
+
+}  // namespace cu
+}  // namespace p3s

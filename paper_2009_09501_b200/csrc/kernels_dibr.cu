@@ -1,0 +1,285 @@
+// K3a: DIBR left/right reconstruction on sm_100a (reference proj/src/dibr.cpp:33-111),
+// optionally fused with the anaglyph composition (stereo_format.cpp:8-21).
+//
+// One CTA per image row. The source row (R, G, B) and its filtered depth are staged in
+// shared memory with 16-byte vector loads. Forward mode splats every source pixel into a
+// per-eye shared-memory z-buffer with atomicMax on a packed key
+//     key = (d + 1) << 22 | (0x3FFFFF - x)
+// whose maximum is "largest depth, then smallest source column" — exactly the winner of
+// the reference's ascending-x scan with strict '>' (dibr.cpp:88-99) — and independent of
+// the order atomics land in. The resolve phase gathers each destination's winning colour
+// from shared memory and writes 16 pixels per thread with 16-byte stores; a destination
+// without a key is damaged. Output routing (EyeOut) writes only the planes a format
+// needs: the fused anaglyph writes left.R and right.G/B straight into the output image,
+// so the two eye frames never exist in HBM (4N read + 3N write + N/4 mask bits).
+//
+// Shift arithmetic is the reference's: sigma[d] = +s (d > T) or -s' (d <= T) is tabulated
+// on the host; p.left = x - sigma, p.right = x + sigma are single IEEE adds (__dadd_rn /
+// __dsub_rn, never contracted), truncated toward zero (__double2int_rz), so (-1, 0)
+// maps to column 0 as in dibr.hpp:35.
+#include "p3s_cu.h"
+
+namespace p3s {
+namespace cu {
+namespace {
+
+constexpr unsigned kXMask = 0x3FFFFFu;
+
+__device__ __forceinline__ void store16(uint8_t* dst, const uint8_t (&v)[16], int x0, int w) {
+    if (x0 + 16 <= w && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+    } else {
+        for (int k = 0; k < 16 && x0 + k < w; ++k) dst[k] = v[k];
+    }
+}
+
+// Appends the set bits of `m` (pixel x0+k for bit k) to a damaged list, one global
+// atomic per warp. Every lane of the warp must call it.
+__device__ __forceinline__ void append_list(uint32_t* list, uint32_t* count, unsigned m,
+                                            uint32_t base_index, int lane) {
+    const int n = __popc(m);
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    uint32_t start = 0;
+    if (lane == 31 && total) start = atomicAdd(count, static_cast<uint32_t>(total));
+    start = __shfl_sync(0xFFFFFFFFu, start, 31);
+    uint32_t pos = start + static_cast<uint32_t>(incl - n);
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        list[pos++] = base_index + static_cast<uint32_t>(k);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
+                                              const uint8_t* __restrict__ G,
+                                              const uint8_t* __restrict__ B,
+                                              const uint8_t* __restrict__ D, int pitch, int w,
+                                              const double* __restrict__ shift_g, int backward,
+                                              EyeOut L, EyeOut Rt) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ double s_shift[256];
+    const int y = blockIdx.x;
+    const int wpad = (w + 15) & ~15;
+    const int nvec = wpad >> 4;
+    uint8_t* s_r = smem;
+    uint8_t* s_g = s_r + wpad;
+    uint8_t* s_b = s_g + wpad;
+    uint8_t* s_d = s_b + wpad;
+    uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 4 * wpad);
+    uint32_t* keyR = keyL + wpad;
+    const int tid = threadIdx.x, lane = tid & 31;
+
+    for (int i = tid; i < 256; i += blockDim.x) s_shift[i] = shift_g[i];
+    const size_t row = static_cast<size_t>(y) * pitch;
+    for (int c = tid; c < nvec; c += blockDim.x) {
+        reinterpret_cast<uint4*>(s_r)[c] = __ldg(reinterpret_cast<const uint4*>(R + row) + c);
+        reinterpret_cast<uint4*>(s_g)[c] = __ldg(reinterpret_cast<const uint4*>(G + row) + c);
+        reinterpret_cast<uint4*>(s_b)[c] = __ldg(reinterpret_cast<const uint4*>(B + row) + c);
+        reinterpret_cast<uint4*>(s_d)[c] = __ldg(reinterpret_cast<const uint4*>(D + row) + c);
+        if (!backward) {
+            const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                reinterpret_cast<uint4*>(keyL)[4 * c + q] = z;
+                reinterpret_cast<uint4*>(keyR)[4 * c + q] = z;
+            }
+        }
+    }
+    __syncthreads();
+
+    if (!backward) {
+        for (int c = tid; c < nvec; c += blockDim.x) {
+            const uint4 dv = reinterpret_cast<const uint4*>(s_d)[c];
+            const uint8_t* dp = reinterpret_cast<const uint8_t*>(&dv);
+#pragma unroll 4
+            for (int k = 0; k < 16; ++k) {
+                const int x = 16 * c + k;
+                if (x >= w) break;
+                const int d = dp[k];
+                const double sigma = s_shift[d];
+                const double xd = static_cast<double>(x);
+                const int dst_l = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
+                const int dst_r = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
+                const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
+                if (static_cast<unsigned>(dst_l) < static_cast<unsigned>(w)) atomicMax(&keyL[dst_l], key);
+                if (static_cast<unsigned>(dst_r) < static_cast<unsigned>(w)) atomicMax(&keyR[dst_r], key);
+            }
+        }
+        __syncthreads();
+    }
+
+    for (int cb = tid - lane; cb < nvec; cb += blockDim.x) {
+        const int c = cb + lane;
+        const bool active = c < nvec;
+        const int x0 = 16 * c;
+        uint8_t lr[16], lg[16], lb[16], rr[16], rg[16], rb[16];
+        unsigned mL = 0, mR = 0;
+        if (active) {
+#pragma unroll 4
+            for (int k = 0; k < 16; ++k) {
+                const int x = x0 + k;
+                int sl, sr;
+                if (x >= w) {
+                    sl = sr = w - 1;
+                } else if (backward) {
+                    const double sigma = s_shift[s_d[x]];
+                    const double xd = static_cast<double>(x);
+                    const int xl = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
+                    const int xr = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
+                    sl = static_cast<unsigned>(xl) < static_cast<unsigned>(w) ? xl : x;
+                    sr = static_cast<unsigned>(xr) < static_cast<unsigned>(w) ? xr : x;
+                } else {
+                    const unsigned kl = keyL[x], kr = keyR[x];
+                    sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
+                    sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
+                    if (sl < 0) mL |= 1u << k;
+                    if (sr < 0) mR |= 1u << k;
+                }
+                lr[k] = sl >= 0 ? s_r[sl] : 0;
+                lg[k] = sl >= 0 ? s_g[sl] : 0;
+                lb[k] = sl >= 0 ? s_b[sl] : 0;
+                rr[k] = sr >= 0 ? s_r[sr] : 0;
+                rg[k] = sr >= 0 ? s_g[sr] : 0;
+                rb[k] = sr >= 0 ? s_b[sr] : 0;
+            }
+            const size_t lo = static_cast<size_t>(y) * L.pitch + x0;
+            const size_t ro = static_cast<size_t>(y) * Rt.pitch + x0;
+            if (L.plane[0]) store16(L.plane[0] + lo, lr, x0, w);
+            if (L.plane[1]) store16(L.plane[1] + lo, lg, x0, w);
+            if (L.plane[2]) store16(L.plane[2] + lo, lb, x0, w);
+            if (Rt.plane[0]) store16(Rt.plane[0] + ro, rr, x0, w);
+            if (Rt.plane[1]) store16(Rt.plane[1] + ro, rg, x0, w);
+            if (Rt.plane[2]) store16(Rt.plane[2] + ro, rb, x0, w);
+            if (L.mask_bytes || Rt.mask_bytes) {
+                uint8_t ml[16], mr[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    ml[k] = (mL >> k) & 1u;
+                    mr[k] = (mR >> k) & 1u;
+                }
+                if (L.mask_bytes) store16(L.mask_bytes + static_cast<size_t>(y) * L.mask_pitch + x0, ml, x0, w);
+                if (Rt.mask_bytes) store16(Rt.mask_bytes + static_cast<size_t>(y) * Rt.mask_pitch + x0, mr, x0, w);
+            }
+        }
+        // bit masks: lanes (2j, 2j+1) hold the two 16-pixel halves of one 32-bit word
+        const unsigned pL = __shfl_xor_sync(0xFFFFFFFFu, mL, 1);
+        const unsigned pR = __shfl_xor_sync(0xFFFFFFFFu, mR, 1);
+        if (active && !(lane & 1)) {
+            if (L.mask_bits) L.mask_bits[static_cast<size_t>(y) * L.mask_pitch + (c >> 1)] = mL | (pL << 16);
+            if (Rt.mask_bits) Rt.mask_bits[static_cast<size_t>(y) * Rt.mask_pitch + (c >> 1)] = mR | (pR << 16);
+        }
+        const uint32_t base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w) + x0;
+        if (L.list) append_list(L.list, L.count, mL, base, lane);
+        if (Rt.list) append_list(Rt.list, Rt.count, mR, base, lane);
+    }
+}
+
+// Byte mask -> damaged list (stage-level inpaint entry point).
+__global__ void k_mask_to_list(const uint8_t* __restrict__ mask, int mpitch, int w, int h,
+                               uint32_t* list, uint32_t* count) {
+    const int lane = threadIdx.x & 31;
+    const int y = blockIdx.y;
+    const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
+    unsigned m = 0;
+    for (int k = 0; k < 16; ++k)
+        if (x0 + k < w && mask[static_cast<size_t>(y) * mpitch + x0 + k]) m |= 1u << k;
+    append_list(list, count, m, static_cast<uint32_t>(y) * w + x0, lane);
+}
+
+// HSBS squeeze (stereo_format.cpp:47-71): (a + b + 1) / 2 over column pairs; left eye to
+// [0, w/2), right eye to [w/2, w). Thread = 16 output pixels of one half.
+__global__ void k_hsbs(const uint8_t* __restrict__ l0, const uint8_t* __restrict__ l1,
+                       const uint8_t* __restrict__ l2, const uint8_t* __restrict__ r0,
+                       const uint8_t* __restrict__ r1, const uint8_t* __restrict__ r2,
+                       int pitch, int w, uint8_t* o0, uint8_t* o1, uint8_t* o2, int opitch) {
+    const int y = blockIdx.y;
+    const int hw = w / 2;
+    const int nchunk = (hw + 15) / 16;
+    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= 2 * nchunk) return;
+    const int eye = item / nchunk;
+    const int x0 = (item % nchunk) * 16;
+    const uint8_t* src[3] = {eye ? r0 : l0, eye ? r1 : l1, eye ? r2 : l2};
+    uint8_t* dst[3] = {o0, o1, o2};
+    for (int ch = 0; ch < 3; ++ch) {
+        const uint8_t* s = src[ch] + static_cast<size_t>(y) * pitch;
+        uint8_t v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int x = min(x0 + k, hw - 1);
+            v[k] = static_cast<uint8_t>((s[2 * x] + s[2 * x + 1] + 1u) / 2u);
+        }
+        store16(dst[ch] + static_cast<size_t>(y) * opitch + eye * hw + x0, v, x0, hw);
+    }
+}
+
+}  // namespace
+
+cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
+                 Geom gm, const double* shift, bool backward, EyeOut left, EyeOut right,
+                 cudaStream_t st) {
+    const int wpad = (gm.w + 15) & ~15;
+    const size_t smem = static_cast<size_t>(wpad) * (backward ? 4 : 12);
+    static bool configured[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured[dev]) {
+        cudaFuncSetAttribute(k_dibr, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        configured[dev] = true;
+    }
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
+    k_dibr<<<gm.h, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, shift, backward ? 1 : 0,
+                                    left, right);
+    return cudaGetLastError();
+}
+
+cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* list,
+                         uint32_t* count, cudaStream_t st) {
+    const int chunks = (gm.w + 15) / 16;
+    dim3 grid((chunks + 127) / 128, gm.h);
+    k_mask_to_list<<<grid, 128, 0, st>>>(mask, mpitch, gm.w, gm.h, list, count);
+    return cudaGetLastError();
+}
+
+cudaError_t anaglyph(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
+                     uint8_t* const* out, int out_pitch, cudaStream_t st) {
+    const uint8_t* src[3] = {left[0], right[1], right[2]};
+    for (int ch = 0; ch < 3; ++ch) {
+        cudaError_t e = cudaMemcpy2DAsync(out[ch], out_pitch, src[ch], gm.pitch, gm.w, gm.h,
+                                          cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t side_by_side_half(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
+                              uint8_t* const* out, int out_pitch, cudaStream_t st) {
+    const int hw = gm.w / 2;
+    const int items = 2 * ((hw + 15) / 16);
+    dim3 grid((items + 127) / 128, gm.h);
+    k_hsbs<<<grid, 128, 0, st>>>(left[0], left[1], left[2], right[0], right[1], right[2],
+                                 gm.pitch, gm.w, out[0], out[1], out[2], out_pitch);
+    return cudaGetLastError();
+}
+
+cudaError_t side_by_side_full(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
+                              uint8_t* const* out, int out_pitch, cudaStream_t st) {
+    for (int ch = 0; ch < 3; ++ch) {
+        cudaError_t e = cudaMemcpy2DAsync(out[ch], out_pitch, left[ch], gm.pitch, gm.w, gm.h,
+                                          cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemcpy2DAsync(out[ch] + gm.w, out_pitch, right[ch], gm.pitch, gm.w, gm.h,
+                              cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace cu
+}  // namespace p3s

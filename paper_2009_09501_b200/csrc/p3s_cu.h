@@ -1,0 +1,115 @@
+// p3s_cu.h — the thin internal layer between the host orchestrator (engine.cpp) and the
+// sm_100a kernels (*.cu). Plain functions over device pointers, sizes, POD parameters
+// and a cudaStream_t; each enqueues work and returns a cudaError_t. No torch, no STL.
+//
+// Device image layout: planar u8, row-major, `pitch` bytes per row (pitch % 16 == 0 so
+// every kernel can use 16-byte vector accesses), plane stride = pitch * h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace p3s {
+namespace cu {
+
+// Reference pseudo3d.h:43-47 format bits.
+enum : unsigned { kAnaglyph = 1u, kHsbs = 2u, kFsbs = 4u };
+
+struct Geom {
+    int w, h, pitch;
+};
+
+// Per-(size, config) constant tables, computed on the host with the reference's exact
+// double expressions (engine.cpp) and uploaded once per plan.
+struct DepthTables {
+    const int* col_i0;     // [w]  left block-centre index  (depth.cpp:96-102 locate)
+    const int* col_i1;     // [w]  min(i0+1, bx-1)
+    const double* col_f;   // [w]  interpolation fraction
+    const int* row_i0;     // [h]
+    const int* row_i1;     // [h]
+    const double* row_f;   // [h]
+    int bx, by, block;
+    double alpha255;       // alpha * 255.0 (left-to-right as depth.cpp:60)
+    double beta;
+    double row_denom;      // h > 1 ? h - 1 : 1
+};
+
+// K1: luma plane + per-block Sobel-magnitude sums (image.cpp:13-21, depth.cpp:21-74).
+// sums must be zeroed (bx*by u64) before the call.
+cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
+                        uint8_t* luma, unsigned long long* sums, int block, int bx,
+                        cudaStream_t st);
+// Block values (depth.cpp:55-71) from the sums.
+cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTables& t,
+                         double* values, cudaStream_t st);
+// Bilinear upsample to the u8 depth map (depth.cpp:104-120).
+cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_t* depth,
+                     cudaStream_t st);
+
+// K2: exact FP64 cross-bilateral (bilateral.cpp:40-116). spatial: (2r+1) x (r+1) doubles,
+// s[(dy+r)*(r+1) + dx] for dx >= 0; range: 256 doubles. raw (optional, w-strided)
+// receives the unrounded means (cross_bilateral_raw), out the rounded u8 map.
+// bilateral_tiled takes the spatial table from HOST memory (it travels as a kernel
+// parameter) and handles radius <= bilateral_tiled_max_radius(); bilateral (generic,
+// any radius) reads a DEVICE copy.
+cudaError_t bilateral_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                            const double* spatial_host, const double* range, uint8_t* out,
+                            double* raw, cudaStream_t st);
+int bilateral_tiled_max_radius();
+cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                      const double* spatial, const double* range, uint8_t* out, double* raw,
+                      cudaStream_t st);
+
+// DIBR output routing. Each eye writes up to three planes (nullptr = channel not needed,
+// e.g. anaglyph needs only left.R and right.G/B). Planes of one eye share a pitch.
+struct EyeOut {
+    uint8_t* plane[3];
+    int pitch;
+    uint8_t* mask_bytes;   // byte mask (reference DamageMask layout), pitch = mask_pitch
+    uint32_t* mask_bits;   // or bit mask: ceil(w/32) words per row, bit x%32, 1 = damaged
+    int mask_pitch;        // bytes per row (bytes) or words per row (bits)
+    uint32_t* list;        // damaged pixel indices (y*w + x), appended
+    uint32_t* count;       // list length (device counter, zeroed before the call)
+};
+
+// DIBR (dibr.cpp:43-104). shift: 256 doubles sigma[d] (p.left = x - sigma, p.right =
+// x + sigma; see engine.cpp). backward = cfg.dibr_mode == kBackwardFallback.
+cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
+                 Geom gm, const double* shift, bool backward, EyeOut left, EyeOut right,
+                 cudaStream_t st);
+
+// Byte mask -> damaged list (stage-level inpaint entry point).
+cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* list,
+                         uint32_t* count, cudaStream_t st);
+
+// Inpaint (inpaint.cpp:29-130) on both eyes at once, in place on the EyeOut planes.
+// Work lists come from dibr(). stats (device, 6 x i64): passes/repaired/fallback per eye.
+struct InpaintEye {
+    uint8_t* plane[3];
+    int pitch;
+    uint8_t* mask_bytes;
+    uint32_t* mask_bits;
+    int mask_pitch;
+    uint32_t* list;        // in: damaged indices (length *count)
+    uint32_t* count;
+    uint32_t* list2;       // scratch, same capacity
+    uint32_t* repair;      // scratch, same capacity
+};
+cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
+                    uint32_t* scratch /* 64 words, zeroed by the call */, long long* stats,
+                    cudaStream_t st);
+
+// Formats from materialised eyes (stereo_format.cpp:8-73).
+cudaError_t anaglyph(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
+                     uint8_t* const* out, int out_pitch, cudaStream_t st);
+cudaError_t side_by_side_half(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
+                              uint8_t* const* out, int out_pitch, cudaStream_t st);
+cudaError_t side_by_side_full(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
+                              uint8_t* const* out, int out_pitch, cudaStream_t st);
+
+int sm_count();
+// Non-FMA FP64 issue-rate microbenchmark (independent DMUL/DADD chains), ops per second.
+cudaError_t fp64_peak(double* ops_per_s);
+
+}  // namespace cu
+}  // namespace p3s

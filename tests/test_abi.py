@@ -1,0 +1,203 @@
+"""CPU: the drop-in C-ABI library loads, exports every symbol its headers declare, and
+its host-side behaviour (config validation, error strings, PNM codec, ownership) matches
+the reference's own C ABI (reference pseudo3d.h / capi.cpp), compared live against the
+compiled reference's libp3s_ref.so when present. No compute calls here."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADERS = [os.path.join(ROOT, "include", "pseudo3d.h"), os.path.join(ROOT, "include", "p3s_gpu.h")]
+
+
+def declared(path):
+    text = open(path).read()
+    return re.findall(r"P3S_API[^;]*?\b(p3s_\w+)\s*\(", text)
+
+
+def test_exports_every_declared_symbol(p3s):
+    syms = subprocess.check_output(["nm", "-D", "--defined-only", p3s.LIB_PATH]).decode()
+    exported = {line.split()[-1] for line in syms.splitlines()}
+    names = [n for h in HEADERS for n in declared(h)]
+    assert len(declared(HEADERS[0])) == 49  # the reference's surface
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    # nothing but the C ABI leaks out of the library
+    leaked = [s for s in exported if not s.startswith("p3s_") and not s.startswith("_")]
+    assert not leaked, leaked[:10]
+
+
+def test_header_matches_reference_surface():
+    ref = "/root/reference/proj/include/pseudo3d.h"
+    if not os.path.exists(ref):
+        pytest.skip("reference tree not mounted")
+    assert sorted(declared(ref)) == sorted(declared(HEADERS[0]))
+
+
+def test_version_and_status_names(p3s):
+    L = p3s.lib()
+    assert p3s.version() == "1.0.0"
+    names = [L.p3s_status_name(i).decode() for i in range(5)]
+    assert names == ["ok", "invalid argument", "io error", "decode error", "internal error"]
+
+
+def _abi(lib_path):
+    L = C.CDLL(lib_path)
+    L.p3s_config_create.restype = C.c_void_p
+    L.p3s_last_error.restype = C.c_char_p
+    for n in ("p3s_config_set_base", "p3s_config_set_formats", "p3s_config_set_mode",
+              "p3s_config_set_pop_threshold", "p3s_config_set_depth_block",
+              "p3s_config_set_inpaint_block", "p3s_config_set_threads"):
+        getattr(L, n).argtypes = [C.c_void_p, C.c_int]
+    L.p3s_config_set_sigma_spatial.argtypes = [C.c_void_p, C.c_double]
+    L.p3s_config_set_sigma_range.argtypes = [C.c_void_p, C.c_double]
+    L.p3s_config_set_depth_weights.argtypes = [C.c_void_p, C.c_double, C.c_double]
+    L.p3s_config_set_auto_base.argtypes = [C.c_void_p]
+    L.p3s_config_free.argtypes = [C.c_void_p]
+    L.p3s_image_create.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    L.p3s_image_free.argtypes = [C.c_void_p]
+    L.p3s_image_decode_ppm.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]
+    L.p3s_image_encode_ppm.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    L.p3s_image_load_ppm.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    L.p3s_graymap_decode_pgm.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]
+    L.p3s_buffer_data.restype = C.c_void_p
+    L.p3s_buffer_data.argtypes = [C.c_void_p]
+    L.p3s_buffer_size.restype = C.c_size_t
+    L.p3s_buffer_size.argtypes = [C.c_void_p]
+    L.p3s_buffer_free.argtypes = [C.c_void_p]
+    L.p3s_image_plane.restype = C.c_void_p
+    L.p3s_image_plane.argtypes = [C.c_void_p, C.c_int]
+    L.p3s_image_width.argtypes = [C.c_void_p]
+    L.p3s_image_height.argtypes = [C.c_void_p]
+    L.p3s_convert_sequence.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p]
+    return L
+
+
+SCRIPT = [
+    ("p3s_config_set_base", 3), ("p3s_config_set_base", -1), ("p3s_config_set_base", -4),
+    ("p3s_config_set_base", 30), ("p3s_config_set_formats", 8), ("p3s_config_set_formats", 0),
+    ("p3s_config_set_formats", 7), ("p3s_config_set_mode", 5), ("p3s_config_set_mode", 1),
+    ("p3s_config_set_pop_threshold", 256), ("p3s_config_set_pop_threshold", -1),
+    ("p3s_config_set_depth_block", 3), ("p3s_config_set_inpaint_block", 2),
+    ("p3s_config_set_sigma_spatial", 0.0), ("p3s_config_set_sigma_range", -1.0),
+    ("p3s_config_set_sigma_spatial", float("nan")), ("p3s_config_set_depth_weights", (0.8, 0.3)),
+    ("p3s_config_set_depth_weights", (-0.1, 0.3)), ("p3s_config_set_depth_weights", (0.5, 0.5)),
+    ("p3s_config_set_threads", -3), ("p3s_config_set_auto_base", None),
+]
+
+
+def run_script(L):
+    cfg = L.p3s_config_create()
+    log = []
+    for fn, arg in SCRIPT:
+        f = getattr(L, fn)
+        if arg is None:
+            st = f(cfg)
+        elif isinstance(arg, tuple):
+            st = f(cfg, *arg)
+        else:
+            st = f(cfg, arg)
+        log.append((fn, st, L.p3s_last_error().decode()))
+    L.p3s_config_free(cfg)
+    return log
+
+
+PPM_CASES = [b"P6\n2 1\n255\n\x01\x02\x03\x04\x05\x06", b"P6\n2 2\n255\n\x01",
+             b"P6 # c\n2 1 # x\n255\n" + bytes(6), b"P6\n1 1\n65535\n" + bytes(6),
+             b"P5\n1 1\n255\n\x00", b"P6\n0 1\n255\n", b"P6\n2 1\n255\n" + bytes(7),
+             b"P6\n2 1\n255", b"P6\nx 1\n255\n", b"P6\n99999999999 1\n255\n"]
+
+
+def decode_log(L):
+    out = []
+    for data in PPM_CASES:
+        h = C.c_void_p()
+        st = L.p3s_image_decode_ppm(data, len(data), C.byref(h))
+        msg = L.p3s_last_error().decode()
+        pixels = None
+        if st == 0:
+            w, hh = L.p3s_image_width(h), L.p3s_image_height(h)
+            pixels = [C.string_at(L.p3s_image_plane(h, c), w * hh) for c in range(3)]
+            buf = C.c_void_p()
+            assert L.p3s_image_encode_ppm(h, C.byref(buf)) == 0
+            enc = C.string_at(L.p3s_buffer_data(buf), L.p3s_buffer_size(buf))
+            L.p3s_buffer_free(buf)
+            pixels.append(enc)
+            L.p3s_image_free(h)
+        out.append((st, msg, pixels))
+    return out
+
+
+def test_config_and_errors_match_reference(p3s, reference):
+    import oracle
+    mine = run_script(_abi(p3s.LIB_PATH))
+    ref = run_script(_abi(oracle.REF_SO))
+    assert mine == ref
+
+
+def test_pnm_matches_reference(p3s, reference):
+    import oracle
+    assert decode_log(_abi(p3s.LIB_PATH)) == decode_log(_abi(oracle.REF_SO))
+
+
+def test_known_error_strings(p3s):
+    L = _abi(p3s.LIB_PATH)
+    cfg = L.p3s_config_create()
+    assert L.p3s_config_set_base(cfg, 3) == 1
+    assert L.p3s_last_error() == b"base must be even"
+    assert L.p3s_config_set_base(cfg, -1) == 0 and L.p3s_last_error() == b""
+    assert L.p3s_config_set_formats(cfg, 8) == 1
+    assert L.p3s_last_error() == b"unknown output format bit"
+    assert L.p3s_config_set_mode(cfg, 5) == 1 and L.p3s_last_error() == b"unknown dibr mode"
+    h = C.c_void_p()
+    assert L.p3s_image_create(0, 5, C.byref(h)) == 1
+    assert L.p3s_last_error() == b"image dimensions must be >= 1"
+    data = b"P6\n2 2\n255\n\x01"
+    assert L.p3s_image_decode_ppm(data, len(data), C.byref(h)) == 3
+    assert L.p3s_last_error() == b"pixel data truncated: expected 12 bytes, got 1"
+    assert L.p3s_image_load_ppm(b"/nonexistent/x.ppm", C.byref(h)) == 2
+    assert L.p3s_last_error() == b"cannot open for reading: /nonexistent/x.ppm"
+    assert L.p3s_convert_sequence(b"/nonexistent_dir", b"f_%d_%d.ppm", b"/tmp", cfg, None,
+                                  None) == 1
+    L.p3s_config_free(cfg)
+
+
+def test_image_roundtrip_and_zero_init(p3s, tmp_path):
+    arr = np.random.default_rng(0).integers(0, 256, (3, 5, 7), dtype=np.uint8)
+    im = p3s.Image(arr)
+    assert np.array_equal(im.numpy(), arr)
+    L = p3s.lib()
+    h = C.c_void_p()
+    assert L.p3s_image_create(4, 3, C.byref(h)) == 0
+    z = p3s.Image(handle=h).numpy()
+    assert z.shape == (3, 3, 4) and not z.any()
+    path = str(tmp_path / "a.ppm").encode()
+    assert L.p3s_image_save_ppm(path, im.h) == 0
+    h2 = C.c_void_p()
+    assert L.p3s_image_load_ppm(path, C.byref(h2)) == 0
+    assert np.array_equal(p3s.Image(handle=h2).numpy(), arr)
+
+
+def test_params_roundtrip(p3s):
+    cfg = p3s.Config(base=12, pop_threshold=99, sigma_spatial=3.5, formats=5, mode=1)
+    p = cfg.params()
+    assert (p.base, p.pop_threshold, p.sigma_spatial, p.formats, p.mode) == (12, 99, 3.5, 5, 1)
+    with pytest.raises(p3s.P3SError) as e:
+        cfg.set(base=5)
+    assert e.value.status == 1 and e.value.message == "base must be even"
+    assert cfg.params().base == 12  # rolled back
+
+
+def test_no_cpu_fallback_without_gpu(p3s):
+    if p3s.device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    img = np.zeros((3, 4, 4), np.uint8)
+    with pytest.raises(p3s.P3SError) as e:
+        p3s.convert(img, p3s.Config())
+    assert e.value.status == 4 and "no CUDA device" in e.value.message

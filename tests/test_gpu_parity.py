@@ -1,0 +1,166 @@
+"""GPU parity: every stage and the full p3s_convert of the CUDA path, through the C ABI,
+byte-exact (and bit-exact for FP64 raw means) against the reference's golden vectors and
+the live CPU oracle (compiled reference when present, else the C port)."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_case
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN_CASES = ["default_48x32", "params_67x33", "backward_64x40", "wide_base_40x30",
+                "sigma_big_50x44", "tiny_1x1", "tiny_1x7", "tiny_9x1", "thin_2x31"]
+NCPU = os.cpu_count() or 1
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def pcfg(p3s, d):
+    return p3s.Config(**d)
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_stages_match_golden(p3s, manifest, name):
+    entry = manifest["cases"][name]
+    cfg = pcfg(p3s, entry["cfg"])
+    g = load_case(name)
+    img = g["input"]
+    assert np.array_equal(p3s.luma(img), g["luma"])
+    vals = p3s.block_depth(img, cfg)
+    assert np.array_equal(vals.view(np.uint64), g["block_values"].view(np.uint64))
+    assert np.array_equal(p3s.upsample(g["block_values"], entry["w"], entry["h"],
+                                       entry["cfg"]["depth_block"]), g["depth"])
+    assert np.array_equal(p3s.generate_depth(img, cfg), g["depth"])
+    assert np.array_equal(p3s.cross_bilateral(g["depth"], g["luma"], cfg), g["filtered"])
+    raw = p3s.cross_bilateral_raw(g["depth"], g["luma"], cfg)
+    assert np.array_equal(raw.view(np.uint64), g["filtered_raw"].view(np.uint64))
+    left, right, lm, rm = p3s.reconstruct(img, g["filtered"], cfg)
+    for k, v in dict(left=left, right=right, left_mask=lm, right_mask=rm).items():
+        assert np.array_equal(v, g[k]), k
+    li, ls = p3s.inpaint(g["left"], g["left_mask"], cfg)
+    ri, rs = p3s.inpaint(g["right"], g["right_mask"], cfg)
+    assert np.array_equal(li, g["left_inpainted"]) and ls == tuple(g["left_stats"])
+    assert np.array_equal(ri, g["right_inpainted"]) and rs == tuple(g["right_stats"])
+    assert np.array_equal(p3s.anaglyph(li, ri), g["anaglyph_stage"])
+    assert np.array_equal(p3s.side_by_side(li, ri, False), g["fsbs_stage"])
+    if "hsbs_stage" in g:
+        assert np.array_equal(p3s.side_by_side(li, ri, True), g["hsbs_stage"])
+    out = p3s.convert(img, cfg)
+    assert np.array_equal(out["depth"], g["depth"])
+    assert np.array_equal(out["filtered"], g["filtered"])
+    for k in ("anaglyph", "hsbs", "fsbs"):
+        if "convert_" + k in g:
+            assert np.array_equal(out[k], g["convert_" + k]), k
+
+
+def test_1080p_matches_reference_digest(p3s, manifest):
+    d = manifest["digests"]["default_1920x1080"]
+    import oracle
+    img = oracle.load("port").synthetic_frame(d["w"], d["h"], d["seed"])
+    assert sha(img) == d["input"]
+    out = p3s.convert(img, pcfg(p3s, d["cfg"]))
+    assert sha(out["depth"]) == d["depth"]
+    assert sha(out["filtered"]) == d["filtered"]
+    assert sha(out["anaglyph"]) == d["anaglyph"]
+
+
+def compare_convert(p3s, checker, img, over):
+    import oracle
+    ref = checker.convert(img, oracle.Cfg(**over), threads=NCPU)
+    out = p3s.convert(img, p3s.Config(**over))
+    for k in ("depth", "filtered", "anaglyph", "hsbs", "fsbs"):
+        if k in ref:
+            if not np.array_equal(out[k], ref[k]):
+                diff = np.argwhere(out[k] != ref[k])
+                raise AssertionError(f"{k} differs at {len(diff)} px, first {diff[:3]} cfg={over}")
+    return out
+
+
+def test_random_sizes_and_configs(p3s, checker):
+    rng = np.random.default_rng(7)
+    for i in range(24):
+        w, h = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+        over = dict(base=int(rng.choice([-1, 0, 2, 8, 16, 30, 64])),
+                    pop_threshold=int(rng.integers(0, 256)),
+                    sigma_spatial=float(rng.choice([0.4, 1.0, 2.5, 3.3, 8.0, 12.0])),
+                    sigma_range=float(rng.choice([2.0, 16.0, 50.0])),
+                    depth_block=int(rng.integers(4, 40)), alpha=float(rng.choice([0.0, 0.7])),
+                    beta=0.3, mode=int(rng.integers(0, 2)), formats=int(rng.choice([1, 3, 4, 5, 7])))
+        if over["formats"] & 2 and w % 2:
+            over["formats"] &= ~2
+        img = checker.synthetic_frame(w, h, i + 1)
+        compare_convert(p3s, checker, img, over)
+
+
+@pytest.mark.parametrize("base", [0, 2, 16, 30, 60, 120, 254, 510])
+def test_parallax_sweep_540p(p3s, checker, base):
+    img = checker.synthetic_frame(960, 540, 3)
+    compare_convert(p3s, checker, img, dict(base=base))
+
+
+def test_large_radius_generic_kernel(p3s, checker):
+    # sigma_s = 23 -> r = 46 > the tiled kernel's 43: exercises the generic path
+    img = checker.synthetic_frame(130, 90, 5)
+    compare_convert(p3s, checker, img, dict(sigma_spatial=23.0, formats=7, base=20))
+
+
+def test_4k_default_full(p3s, checker):
+    img = checker.synthetic_frame(3840, 2160, 1)
+    out = compare_convert(p3s, checker, img, {})
+    t = out["timings"]
+    assert t["pure_ns"] == t["filter_ns"] + t["dibr_ns"] + t["inpaint_left_ns"] + \
+        t["inpaint_right_ns"] + t["format_ns"]
+
+
+def test_b0_identity_and_backward_has_no_holes(p3s, checker):
+    img = checker.synthetic_frame(321, 177, 9)
+    out = p3s.convert(img, p3s.Config(base=0))
+    assert np.array_equal(out["anaglyph"], img)
+    out = p3s.convert(img, p3s.Config(mode=1, formats=7))
+    assert out["timings"]["inpaint_left_ns"] == 0 and out["timings"]["inpaint_right_ns"] == 0
+
+
+def test_odd_width_hsbs_is_invalid(p3s):
+    img = np.zeros((3, 4, 5), np.uint8)
+    with pytest.raises(p3s.P3SError) as e:
+        p3s.convert(img, p3s.Config(formats=2))
+    assert e.value.status == 1
+    assert e.value.message == "side_by_side: half mode requires an even width"
+
+
+def test_device_pipeline_and_video_match_convert(p3s, checker):
+    w, h = 640, 360
+    cfg = p3s.Config(base=24)
+    frames = [checker.synthetic_frame(w, h, s) for s in range(1, 7)]
+    expect = [p3s.convert(f, cfg)["anaglyph"] for f in frames]
+    pipe = p3s.Pipeline(w, h, cfg)
+    dbuf = p3s.DeviceBuffer(pipe.frame_bytes)
+    for f, e in zip(frames, expect):
+        pipe.upload(f, dbuf.addr)
+        pipe.run(dbuf.addr, timed=True)
+        _, _, out = pipe.download()
+        assert np.array_equal(out, e)
+    vid = p3s.Video(w, h, cfg, streams=3)
+    n = w * h * 3
+    src = [p3s.PinnedBuffer(n) for _ in frames]
+    dst = [p3s.PinnedBuffer(n) for _ in frames]
+    for b, f in zip(src, frames):
+        b.array[:] = f.reshape(-1)
+    vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst])
+    for b, e in zip(dst, expect):
+        assert np.array_equal(b.array.reshape(3, h, w), e)
+
+
+def test_stream_and_plan_invariance(p3s, checker):
+    # bytes do not depend on which plan/stream ran them (GPU analogue of AC-1)
+    img = checker.synthetic_frame(500, 300, 4)
+    a = p3s.convert(img, p3s.Config(formats=7, base=22))
+    b = p3s.convert(img, p3s.Config(formats=1, base=22))
+    c = p3s.convert(img, p3s.Config(formats=4, base=22))
+    assert np.array_equal(a["anaglyph"], b["anaglyph"])
+    assert np.array_equal(a["fsbs"], c["fsbs"])
