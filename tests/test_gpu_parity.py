@@ -118,7 +118,7 @@ def test_4k_default_full(p3s, checker):
 
 
 def test_b0_identity_and_backward_has_no_holes(p3s, checker):
-    img = checker.synthetic_frame(321, 177, 9)
+    img = checker.synthetic_frame(322, 177, 9)
     out = p3s.convert(img, p3s.Config(base=0))
     assert np.array_equal(out["anaglyph"], img)
     out = p3s.convert(img, p3s.Config(mode=1, formats=7))

@@ -1,0 +1,31 @@
+"""Minimal driver for ncu: runs the device-resident pipeline for a few steps on
+synthetic frames (no e2e / sweep / CPU legs), so a profiler sees only the kernels."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402  (synthetic frame generator only)
+import paper_2009_09501_b200 as p3s  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--w", type=int, default=3840)
+ap.add_argument("--h", type=int, default=2160)
+ap.add_argument("--steps", type=int, default=4)
+ap.add_argument("--base", type=int, default=-1)
+ap.add_argument("--formats", type=int, default=1)
+ap.add_argument("--frames", type=int, default=2)
+a = ap.parse_args()
+p3s.set_device(0)
+cfg = p3s.Config(base=a.base, formats=a.formats)
+pipe = p3s.Pipeline(a.w, a.h, cfg)
+port = oracle.load("port")
+bufs = []
+for i in range(a.frames):
+    d = p3s.DeviceBuffer(pipe.frame_bytes)
+    pipe.upload(port.synthetic_frame(a.w, a.h, 1 + i), d.addr)
+    bufs.append(d)
+for i in range(a.steps):
+    pipe.run(bufs[i % len(bufs)].addr)
+p3s.stream_sync(pipe.stream)
+print("done", a.steps, "steps")
