@@ -22,6 +22,8 @@
 // reference's single-sided update bit for bit. Clipping in y is done by the row loop
 // bounds. Rows of a warp's window where only some outputs are inside their window are
 // run with warp-uniform per-output predicates; the bulk rows run branch-free.
+#include <cstdlib>
+
 #include "p3s_cu.h"
 
 namespace p3s {
@@ -178,6 +180,147 @@ __global__ void __launch_bounds__(kNW * 32) k_bilateral_tiled(
     }
 }
 
+// ---- compile-time-radius variant (the default sigma_s = 8 -> R = 16) ----------------------
+// Same schedule and accumulation order as k_bilateral_tiled, with the per-tap overhead cut:
+//  * the radius is a compile-time constant (dx loop unrolled by 4: a full unroll overflows
+//    the instruction cache — measured no_instruction stalls 1.7/issue);
+//  * the range table is stored by SIGNED guide difference, k = gq - gi + 255, replicated
+//    16 ways: the tile keeps gq*128 and each output keeps base_i = (255-gi)*128 + lane8,
+//    so a lookup is one IADD + one conflict-free LDS.64 (no |.|, no scaling);
+//  * the tile packs (depth << 16) | gq*128 in a u32.
+// Edge tiles route out-of-image taps to the zero sentinel entry with a select.
+constexpr int kSignedEntries = 512;  // k = 0..510, entry 511 = 0.0 sentinel
+
+template <int R, int P, bool ALL, bool EDGE, int N>
+__device__ __forceinline__ void bilr_row(const SpatialParam<N>& sp, const uint32_t* __restrict__ row,
+                                         const char* __restrict__ tbl, int t, int x, int w,
+                                         const int (&base)[P], double (&ws)[P],
+                                         double (&vs)[P]) {
+    constexpr int side = R + 1;
+    constexpr int kZero = 511 * 128;
+    {
+        const uint32_t c = row[0];
+        const int gc = static_cast<int>(c & 0xFFFFu);
+        const double dc = static_cast<double>(c >> 16);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const double s = sp.s[(t - i) * side];
+            const double wc = __dmul_rn(s, *reinterpret_cast<const double*>(tbl + base[i] + gc));
+            ws[i] = __dadd_rn(ws[i], wc);
+            vs[i] = __dadd_rn(vs[i], __dmul_rn(wc, dc));
+        }
+    }
+#pragma unroll 4
+    for (int dx = 1; dx <= R; ++dx) {
+        const uint32_t a = row[-dx], b = row[dx];
+        const int ga = static_cast<int>(a & 0xFFFFu), gb = static_cast<int>(b & 0xFFFFu);
+        const double da = static_cast<double>(a >> 16), db = static_cast<double>(b >> 16);
+        const bool oob_l = EDGE && (x - dx < 0);
+        const bool oob_r = EDGE && (x + dx >= w);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const double s = sp.s[(t - i) * side + dx];
+            const int ol = oob_l ? kZero + (base[i] & 127) : base[i] + ga;
+            const int orr = oob_r ? kZero + (base[i] & 127) : base[i] + gb;
+            const double wl = __dmul_rn(s, *reinterpret_cast<const double*>(tbl + ol));
+            const double wr = __dmul_rn(s, *reinterpret_cast<const double*>(tbl + orr));
+            ws[i] = __dadd_rn(ws[i], __dadd_rn(wl, wr));
+            vs[i] = __dadd_rn(vs[i], __dadd_rn(__dmul_rn(wl, da), __dmul_rn(wr, db)));
+        }
+    }
+}
+
+template <int R, int P, bool EDGE, int N>
+__device__ __forceinline__ void bilr_rows(const SpatialParam<N>& sp, const uint32_t* tile_col,
+                                          const char* tbl, int x, int w, int tlo, int thi,
+                                          const int (&base)[P], double (&ws)[P],
+                                          double (&vs)[P]) {
+    constexpr int SW = kTX + 2 * R;
+    int t = tlo;
+    for (; t <= min(P - 2, thi); ++t)
+        bilr_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= min(2 * R, thi); ++t)
+        bilr_row<R, P, true, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= thi; ++t)
+        bilr_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+}
+
+template <int R, int P, int NW, int MINB, int N>
+__global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_r(
+    const __grid_constant__ SpatialParam<N> sp, const uint8_t* __restrict__ depth,
+    const uint8_t* __restrict__ guide, int pitch, int w, int h,
+    const double* __restrict__ range_g, uint8_t* __restrict__ out, double* __restrict__ raw,
+    int tiles_x, int ntiles) {
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R;
+    constexpr int SH = TY + 2 * R;
+    extern __shared__ __align__(16) unsigned char smem[];
+    char* tbl = reinterpret_cast<char*>(smem);  // [512][16] doubles
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + kSignedEntries * kRangeCopies * 8);
+
+    for (int i = threadIdx.x; i < kSignedEntries * kRangeCopies; i += blockDim.x) {
+        const int k = i / kRangeCopies;
+        const int d = k < 511 ? abs(k - 255) : 256;
+        reinterpret_cast<double*>(tbl)[i] = d < 256 ? range_g[d] : 0.0;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane8 = (lane & (kRangeCopies - 1)) * 8;
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tx0 = (tile % tiles_x) * kTX;
+        const int ty0 = (tile / tiles_x) * TY;
+        __syncthreads();
+        for (int sy = warp; sy < SH; sy += NW) {
+            const int gy = ty0 - R + sy;
+            const bool yin = gy >= 0 && gy < h;
+            const uint8_t* grow = guide + static_cast<size_t>(yin ? gy : 0) * pitch;
+            const uint8_t* drow = depth + static_cast<size_t>(yin ? gy : 0) * pitch;
+            for (int sx = lane; sx < SW; sx += 32) {
+                const int gx = tx0 - R + sx;
+                uint32_t v = 0;
+                if (yin && gx >= 0 && gx < w)
+                    v = (static_cast<uint32_t>(grow[gx]) << 7) | (static_cast<uint32_t>(drow[gx]) << 16);
+                s_tile[sy * SW + sx] = v;
+            }
+        }
+        __syncthreads();
+
+        const int x = tx0 + lane;
+        const int yb = ty0 + warp * P;
+        if (yb >= h) continue;
+        const bool edge = (tx0 - R < 0) || (tx0 + kTX - 1 + R >= w);
+        const uint32_t* tile_col = s_tile + (warp * P) * SW + lane + R;
+        int base[P];
+        double ws[P], vs[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int gi = static_cast<int>((tile_col[(i + R) * SW] & 0xFFFFu) >> 7);
+            base[i] = (255 - gi) * 128 + lane8;
+            ws[i] = 0.0;
+            vs[i] = 0.0;
+        }
+        const int tlo = max(0, R - yb);
+        const int thi = min(P - 1 + 2 * R, h - 1 - yb + R);
+        if (edge)
+            bilr_rows<R, P, true>(sp, tile_col, tbl, x, w, tlo, thi, base, ws, vs);
+        else
+            bilr_rows<R, P, false>(sp, tile_col, tbl, x, w, tlo, thi, base, ws, vs);
+        if (x < w) {
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                const int y = yb + i;
+                if (y < h) {
+                    const double v = __ddiv_rn(vs[i], ws[i]);
+                    out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(v);
+                    if (raw) raw[static_cast<size_t>(y) * w + x] = v;
+                }
+            }
+        }
+    }
+}
+
 // Any radius: one thread per output, tables and pixels read through the L1 path.
 __global__ void __launch_bounds__(256) k_bilateral_generic(
     const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
@@ -254,6 +397,37 @@ cudaError_t launch_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm, in
     return cudaGetLastError();
 }
 
+template <int R, int P, int NW, int MINB>
+cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
+                     const double* spatial_host, const double* range, uint8_t* out, double* raw,
+                     cudaStream_t st) {
+    constexpr int N = (2 * R + 1) * (R + 1);
+    SpatialParam<N> sp;
+    for (int i = 0; i < N; ++i) sp.s[i] = spatial_host[i];
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
+    const size_t smem = kSignedEntries * kRangeCopies * 8 + static_cast<size_t>(SW) * SH * 4;
+    static int configured_dev[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured_dev[dev]) {
+        cudaFuncSetAttribute(k_bilateral_r<R, P, NW, MINB, N>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured_dev[dev] = 1;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_r<R, P, NW, MINB, N>,
+                                                  NW * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int tiles_x = (gm.w + kTX - 1) / kTX;
+    const int tiles_y = (gm.h + TY - 1) / TY;
+    const int ntiles = tiles_x * tiles_y;
+    const int grid = min(ntiles, per_sm * sm_count());
+    k_bilateral_r<R, P, NW, MINB, N><<<grid, NW * 32, smem, st>>>(sp, depth, guide, gm.pitch, gm.w, gm.h,
+                                                      range, out, raw, tiles_x, ntiles);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 // spatial: device table for the generic kernel, in the layout s[(dy+R)*(R+1)+dx] (dx>=0).
@@ -271,6 +445,17 @@ cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int r
 cudaError_t bilateral_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                             const double* spatial_host, const double* range, uint8_t* out,
                             double* raw, cudaStream_t st) {
+    if (radius == 16) {
+        // variant selection for tuning experiments (default chosen from measurements)
+        const char* v = getenv("P3S_BIL_VARIANT");
+        const int var = v ? atoi(v) : 3;  // 3 = P4 x 16 warps, measured best (3.19 ms at 4K)
+        if (var == 1) return launch_r<16, 8, 8, 2>(depth, guide, gm, spatial_host, range, out, raw, st);
+        if (var == 2) return launch_r<16, 8, 16, 1>(depth, guide, gm, spatial_host, range, out, raw, st);
+        if (var == 3 || var == 0) return launch_r<16, 4, 16, 2>(depth, guide, gm, spatial_host, range, out, raw, st);
+        if (var == 4) return launch_r<16, 4, 12, 2>(depth, guide, gm, spatial_host, range, out, raw, st);
+        if (var == 5) return launch_r<16, 6, 16, 1>(depth, guide, gm, spatial_host, range, out, raw, st);
+        if (var == 6) return launch_r<16, 2, 32, 1>(depth, guide, gm, spatial_host, range, out, raw, st);
+    }
     const int n = (2 * radius + 1) * (radius + 1);
     if (n <= 1024)
         return launch_tiled<1024>(depth, guide, gm, radius, spatial_host, range, out, raw, st);

@@ -169,36 +169,61 @@ __device__ __forceinline__ double lerp_ref(double a, double b, double f) {
     return __dadd_rn(__dmul_rn(a, __dsub_rn(1.0, f)), __dmul_rn(b, f));
 }
 
-// depth.cpp:104-120. Thread = 16 consecutive pixels of a row (one 16-byte store).
-__global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ values, int bx,
-                                                  const int* __restrict__ ci0,
-                                                  const int* __restrict__ ci1,
-                                                  const double* __restrict__ cf,
-                                                  const int* __restrict__ ri0,
-                                                  const int* __restrict__ ri1,
-                                                  const double* __restrict__ rf, int w, int h,
-                                                  int pitch, uint8_t* __restrict__ depth) {
-    const int y = blockIdx.y;
-    const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
+// depth.cpp:104-120. A CTA covers 1024 columns x 16 rows; a thread owns 4 adjacent columns
+// (one 4-byte store per row). Within a band of rows sharing the same (iy, iy1) pair the
+// horizontal lerps top(x) / bottom(x) are identical, so they are computed once per band and
+// only the vertical lerp + rounding runs per pixel. Every double operation is the
+// reference's, separately rounded, so the bytes are unchanged.
+constexpr int kUpCols = 4, kUpThreads = 256, kUpRows = 16;
+
+__global__ void __launch_bounds__(kUpThreads) k_upsample(const double* __restrict__ values, int bx,
+                                                         const int* __restrict__ ci0,
+                                                         const int* __restrict__ ci1,
+                                                         const double* __restrict__ cf,
+                                                         const int* __restrict__ ri0,
+                                                         const int* __restrict__ ri1,
+                                                         const double* __restrict__ rf, int w,
+                                                         int h, int pitch,
+                                                         uint8_t* __restrict__ depth) {
+    const int x0 = (blockIdx.x * kUpThreads + threadIdx.x) * kUpCols;
+    const int y0 = blockIdx.y * kUpRows;
     if (x0 >= w) return;
-    const double* top = values + static_cast<size_t>(ri0[y]) * bx;
-    const double* bot = values + static_cast<size_t>(ri1[y]) * bx;
-    const double fy = rf[y];
-    alignas(16) uint8_t px[16];
+    int a[kUpCols], b[kUpCols];
+    double fx[kUpCols];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < kUpCols; ++k) {
         const int x = min(x0 + k, w - 1);
-        const int a = ci0[x], b = ci1[x];
-        const double fx = cf[x];
-        const double t = lerp_ref(__ldg(top + a), __ldg(top + b), fx);
-        const double u = lerp_ref(__ldg(bot + a), __ldg(bot + b), fx);
-        px[k] = round_half_up_u8(lerp_ref(t, u, fy));
+        a[k] = __ldg(ci0 + x);
+        b[k] = __ldg(ci1 + x);
+        fx[k] = __ldg(cf + x);
     }
-    uint8_t* dst = depth + static_cast<size_t>(y) * pitch + x0;
-    if (x0 + 16 <= pitch) {
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(px);
-    } else {
-        for (int k = 0; k < 16 && x0 + k < w; ++k) dst[k] = px[k];
+    int cur0 = -1, cur1 = -1;
+    double top[kUpCols], bot[kUpCols];
+    const int y1 = min(y0 + kUpRows, h);
+    for (int y = y0; y < y1; ++y) {
+        const int i0 = __ldg(ri0 + y), i1 = __ldg(ri1 + y);
+        if (i0 != cur0 || i1 != cur1) {
+            const double* vt = values + static_cast<size_t>(i0) * bx;
+            const double* vb = values + static_cast<size_t>(i1) * bx;
+#pragma unroll
+            for (int k = 0; k < kUpCols; ++k) {
+                top[k] = lerp_ref(__ldg(vt + a[k]), __ldg(vt + b[k]), fx[k]);
+                bot[k] = lerp_ref(__ldg(vb + a[k]), __ldg(vb + b[k]), fx[k]);
+            }
+            cur0 = i0;
+            cur1 = i1;
+        }
+        const double fy = __ldg(rf + y);
+        uint32_t packed = 0;
+#pragma unroll
+        for (int k = 0; k < kUpCols; ++k)
+            packed |= static_cast<uint32_t>(round_half_up_u8(lerp_ref(top[k], bot[k], fy))) << (8 * k);
+        uint8_t* dst = depth + static_cast<size_t>(y) * pitch + x0;
+        if (x0 + kUpCols <= pitch) {  // pitch % 16 == 0: 4-byte aligned, padding is scratch
+            *reinterpret_cast<uint32_t*>(dst) = packed;
+        } else {
+            for (int k = 0; k < kUpCols && x0 + k < w; ++k) dst[k] = static_cast<uint8_t>(packed >> (8 * k));
+        }
     }
 }
 
@@ -222,10 +247,10 @@ cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTab
 
 cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_t* depth,
                      cudaStream_t st) {
-    const int threads = 256;
-    dim3 grid((gm.w + threads * 16 - 1) / (threads * 16), gm.h);
-    k_upsample<<<grid, threads, 0, st>>>(values, t.bx, t.col_i0, t.col_i1, t.col_f, t.row_i0,
-                                         t.row_i1, t.row_f, gm.w, gm.h, gm.pitch, depth);
+    dim3 grid((gm.w + kUpThreads * kUpCols - 1) / (kUpThreads * kUpCols),
+              (gm.h + kUpRows - 1) / kUpRows);
+    k_upsample<<<grid, kUpThreads, 0, st>>>(values, t.bx, t.col_i0, t.col_i1, t.col_f, t.row_i0,
+                                            t.row_i1, t.row_f, gm.w, gm.h, gm.pitch, depth);
     return cudaGetLastError();
 }
 

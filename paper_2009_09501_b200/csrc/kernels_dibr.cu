@@ -56,6 +56,10 @@ __device__ __forceinline__ void append_list(uint32_t* list, uint32_t* count, uns
     }
 }
 
+// Shared-memory phases use a lane-interleaved mapping (lane l of a warp handles pixel
+// base + l), so row-buffer accesses are consecutive bytes / words across a warp and
+// conflict-free; the damage mask of 32 consecutive pixels is one __ballot_sync word.
+// HBM traffic stays 16-byte vectorised through the staging buffers.
 __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
                                               const uint8_t* __restrict__ G,
                                               const uint8_t* __restrict__ B,
@@ -67,116 +71,114 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
     const int y = blockIdx.x;
     const int wpad = (w + 15) & ~15;
     const int nvec = wpad >> 4;
-    uint8_t* s_r = smem;
-    uint8_t* s_g = s_r + wpad;
-    uint8_t* s_b = s_g + wpad;
-    uint8_t* s_d = s_b + wpad;
-    uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 4 * wpad);
+    uint8_t* s_src = smem;                  // [4][wpad]: R, G, B, depth
+    uint8_t* s_out = smem + 4 * wpad;       // [6][wpad]: left R,G,B, right R,G,B
+    uint8_t* s_msk = smem + 10 * wpad;      // [2][wpad]: byte masks (stage API only)
+    uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 12 * wpad);
     uint32_t* keyR = keyL + wpad;
     const int tid = threadIdx.x, lane = tid & 31;
+    const bool bytes_mask = L.mask_bytes || Rt.mask_bytes;
 
     for (int i = tid; i < 256; i += blockDim.x) s_shift[i] = shift_g[i];
     const size_t row = static_cast<size_t>(y) * pitch;
-    for (int c = tid; c < nvec; c += blockDim.x) {
-        reinterpret_cast<uint4*>(s_r)[c] = __ldg(reinterpret_cast<const uint4*>(R + row) + c);
-        reinterpret_cast<uint4*>(s_g)[c] = __ldg(reinterpret_cast<const uint4*>(G + row) + c);
-        reinterpret_cast<uint4*>(s_b)[c] = __ldg(reinterpret_cast<const uint4*>(B + row) + c);
-        reinterpret_cast<uint4*>(s_d)[c] = __ldg(reinterpret_cast<const uint4*>(D + row) + c);
-        if (!backward) {
-            const uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                reinterpret_cast<uint4*>(keyL)[4 * c + q] = z;
-                reinterpret_cast<uint4*>(keyR)[4 * c + q] = z;
-            }
-        }
+    const uint8_t* planes_in[4] = {R + row, G + row, B + row, D + row};
+    for (int c = tid; c < 4 * nvec; c += blockDim.x) {
+        const int pl = c / nvec, v = c - pl * nvec;
+        reinterpret_cast<uint4*>(s_src + pl * wpad)[v] =
+            __ldg(reinterpret_cast<const uint4*>(planes_in[pl]) + v);
+    }
+    if (!backward) {
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        for (int c = tid; c < 2 * wpad / 4; c += blockDim.x) reinterpret_cast<uint4*>(keyL)[c] = z;
     }
     __syncthreads();
+    const uint8_t* s_r = s_src;
+    const uint8_t* s_g = s_src + wpad;
+    const uint8_t* s_b = s_src + 2 * wpad;
+    const uint8_t* s_d = s_src + 3 * wpad;
 
     if (!backward) {
-        for (int c = tid; c < nvec; c += blockDim.x) {
-            const uint4 dv = reinterpret_cast<const uint4*>(s_d)[c];
-            const uint8_t* dp = reinterpret_cast<const uint8_t*>(&dv);
-#pragma unroll 4
-            for (int k = 0; k < 16; ++k) {
-                const int x = 16 * c + k;
-                if (x >= w) break;
-                const int d = dp[k];
-                const double sigma = s_shift[d];
-                const double xd = static_cast<double>(x);
-                const int dst_l = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
-                const int dst_r = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
-                const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
-                if (static_cast<unsigned>(dst_l) < static_cast<unsigned>(w)) atomicMax(&keyL[dst_l], key);
-                if (static_cast<unsigned>(dst_r) < static_cast<unsigned>(w)) atomicMax(&keyR[dst_r], key);
-            }
+        for (int x = tid; x < w; x += blockDim.x) {
+            const int d = s_d[x];
+            const double sigma = s_shift[d];
+            const double xd = static_cast<double>(x);
+            const int dst_l = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
+            const int dst_r = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
+            const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
+            if (static_cast<unsigned>(dst_l) < static_cast<unsigned>(w)) atomicMax(&keyL[dst_l], key);
+            if (static_cast<unsigned>(dst_r) < static_cast<unsigned>(w)) atomicMax(&keyR[dst_r], key);
         }
         __syncthreads();
     }
 
-    for (int cb = tid - lane; cb < nvec; cb += blockDim.x) {
-        const int c = cb + lane;
-        const bool active = c < nvec;
-        const int x0 = 16 * c;
-        uint8_t lr[16], lg[16], lb[16], rr[16], rg[16], rb[16];
-        unsigned mL = 0, mR = 0;
-        if (active) {
-#pragma unroll 4
-            for (int k = 0; k < 16; ++k) {
-                const int x = x0 + k;
-                int sl, sr;
-                if (x >= w) {
-                    sl = sr = w - 1;
-                } else if (backward) {
-                    const double sigma = s_shift[s_d[x]];
-                    const double xd = static_cast<double>(x);
-                    const int xl = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
-                    const int xr = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
-                    sl = static_cast<unsigned>(xl) < static_cast<unsigned>(w) ? xl : x;
-                    sr = static_cast<unsigned>(xr) < static_cast<unsigned>(w) ? xr : x;
-                } else {
-                    const unsigned kl = keyL[x], kr = keyR[x];
-                    sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
-                    sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
-                    if (sl < 0) mL |= 1u << k;
-                    if (sr < 0) mR |= 1u << k;
-                }
-                lr[k] = sl >= 0 ? s_r[sl] : 0;
-                lg[k] = sl >= 0 ? s_g[sl] : 0;
-                lb[k] = sl >= 0 ? s_b[sl] : 0;
-                rr[k] = sr >= 0 ? s_r[sr] : 0;
-                rg[k] = sr >= 0 ? s_g[sr] : 0;
-                rb[k] = sr >= 0 ? s_b[sr] : 0;
+    // resolve: lane-interleaved, whole warps iterate together (ballots need all lanes)
+    const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
+    for (int xb = tid - lane; xb < w; xb += blockDim.x) {
+        const int x = xb + lane;
+        const bool act = x < w;
+        int sl = -1, sr = -1;
+        if (act) {
+            if (backward) {
+                const double sigma = s_shift[s_d[x]];
+                const double xd = static_cast<double>(x);
+                const int xl = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
+                const int xr = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
+                sl = static_cast<unsigned>(xl) < static_cast<unsigned>(w) ? xl : x;
+                sr = static_cast<unsigned>(xr) < static_cast<unsigned>(w) ? xr : x;
+            } else {
+                const unsigned kl = keyL[x], kr = keyR[x];
+                sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
+                sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
             }
-            const size_t lo = static_cast<size_t>(y) * L.pitch + x0;
-            const size_t ro = static_cast<size_t>(y) * Rt.pitch + x0;
-            if (L.plane[0]) store16(L.plane[0] + lo, lr, x0, w);
-            if (L.plane[1]) store16(L.plane[1] + lo, lg, x0, w);
-            if (L.plane[2]) store16(L.plane[2] + lo, lb, x0, w);
-            if (Rt.plane[0]) store16(Rt.plane[0] + ro, rr, x0, w);
-            if (Rt.plane[1]) store16(Rt.plane[1] + ro, rg, x0, w);
-            if (Rt.plane[2]) store16(Rt.plane[2] + ro, rb, x0, w);
-            if (L.mask_bytes || Rt.mask_bytes) {
-                uint8_t ml[16], mr[16];
+            s_out[x] = sl >= 0 ? s_r[sl] : 0;
+            s_out[wpad + x] = sl >= 0 ? s_g[sl] : 0;
+            s_out[2 * wpad + x] = sl >= 0 ? s_b[sl] : 0;
+            s_out[3 * wpad + x] = sr >= 0 ? s_r[sr] : 0;
+            s_out[4 * wpad + x] = sr >= 0 ? s_g[sr] : 0;
+            s_out[5 * wpad + x] = sr >= 0 ? s_b[sr] : 0;
+            if (bytes_mask) {
+                s_msk[x] = sl < 0;
+                s_msk[wpad + x] = sr < 0;
+            }
+        }
+        const unsigned mL = __ballot_sync(0xFFFFFFFFu, act && sl < 0);
+        const unsigned mR = __ballot_sync(0xFFFFFFFFu, act && sr < 0);
+        if (lane == 0) {
+            if (L.mask_bits) L.mask_bits[static_cast<size_t>(y) * L.mask_pitch + (xb >> 5)] = mL;
+            if (Rt.mask_bits) Rt.mask_bits[static_cast<size_t>(y) * Rt.mask_pitch + (xb >> 5)] = mR;
+        }
+        if (L.list && mL) {
+            uint32_t start = 0;
+            if (lane == 0) start = atomicAdd(L.count, static_cast<uint32_t>(__popc(mL)));
+            start = __shfl_sync(0xFFFFFFFFu, start, 0);
+            if ((mL >> lane) & 1u) L.list[start + __popc(mL & ((1u << lane) - 1u))] = row_base + x;
+        }
+        if (Rt.list && mR) {
+            uint32_t start = 0;
+            if (lane == 0) start = atomicAdd(Rt.count, static_cast<uint32_t>(__popc(mR)));
+            start = __shfl_sync(0xFFFFFFFFu, start, 0);
+            if ((mR >> lane) & 1u) Rt.list[start + __popc(mR & ((1u << lane) - 1u))] = row_base + x;
+        }
+    }
+    __syncthreads();
+
+    // vectorised stores of the staged rows (only the planes this route needs)
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    ml[k] = (mL >> k) & 1u;
-                    mr[k] = (mR >> k) & 1u;
-                }
-                if (L.mask_bytes) store16(L.mask_bytes + static_cast<size_t>(y) * L.mask_pitch + x0, ml, x0, w);
-                if (Rt.mask_bytes) store16(Rt.mask_bytes + static_cast<size_t>(y) * Rt.mask_pitch + x0, mr, x0, w);
+    for (int pl = 0; pl < 8; ++pl) {
+        uint8_t* base = pl < 3 ? L.plane[pl] : pl < 6 ? Rt.plane[pl - 3] : pl == 6 ? L.mask_bytes : Rt.mask_bytes;
+        if (!base) continue;
+        const int dp = pl < 3 ? L.pitch : pl < 6 ? Rt.pitch : pl == 6 ? L.mask_pitch : Rt.mask_pitch;
+        const uint8_t* srcrow = pl < 6 ? s_out + pl * wpad : s_msk + (pl - 6) * wpad;
+        uint8_t* orow = base + static_cast<size_t>(y) * dp;
+        for (int v = tid; v < nvec; v += blockDim.x) {
+            const int x0 = 16 * v;
+            uint8_t* o = orow + x0;
+            if (x0 + 16 <= w && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+                *reinterpret_cast<uint4*>(o) = reinterpret_cast<const uint4*>(srcrow)[v];
+            } else {
+                for (int k = 0; k < 16 && x0 + k < w; ++k) o[k] = srcrow[x0 + k];
             }
         }
-        // bit masks: lanes (2j, 2j+1) hold the two 16-pixel halves of one 32-bit word
-        const unsigned pL = __shfl_xor_sync(0xFFFFFFFFu, mL, 1);
-        const unsigned pR = __shfl_xor_sync(0xFFFFFFFFu, mR, 1);
-        if (active && !(lane & 1)) {
-            if (L.mask_bits) L.mask_bits[static_cast<size_t>(y) * L.mask_pitch + (c >> 1)] = mL | (pL << 16);
-            if (Rt.mask_bits) Rt.mask_bits[static_cast<size_t>(y) * Rt.mask_pitch + (c >> 1)] = mR | (pR << 16);
-        }
-        const uint32_t base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w) + x0;
-        if (L.list) append_list(L.list, L.count, mL, base, lane);
-        if (Rt.list) append_list(Rt.list, Rt.count, mR, base, lane);
     }
 }
 
@@ -225,7 +227,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                  Geom gm, const double* shift, bool backward, EyeOut left, EyeOut right,
                  cudaStream_t st) {
     const int wpad = (gm.w + 15) & ~15;
-    const size_t smem = static_cast<size_t>(wpad) * (backward ? 4 : 12);
+    const size_t smem = static_cast<size_t>(wpad) * (backward ? 12 : 20);
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
