@@ -156,6 +156,8 @@ struct Pipeline::Impl {
     uint32_t* mbits = nullptr;
     uint32_t* lists = nullptr;  // [eye][list|list2|repair][N]
     uint32_t* counts = nullptr;  // 2
+    uint32_t* bil_list = nullptr;   // bilateral fast path: uncertified pixels (N)
+    uint32_t* bil_count = nullptr;  // 1
     uint32_t* ctl = nullptr;     // 64
     long long* stats = nullptr;  // 6
     // stage-API extras (allocated on first use)
@@ -224,6 +226,7 @@ struct Pipeline::Impl {
         const std::size_t o_mbits = a.take<uint32_t>(2 * static_cast<std::size_t>(mwords) * h);
         const std::size_t o_lists = a.take<uint32_t>(backward ? 0 : 6 * N);
         const std::size_t o_cnt = a.take<uint32_t>(2);
+        const std::size_t o_bil = a.take<uint32_t>(N + 1);
         const std::size_t o_ctl = a.take<uint32_t>(64);
         const std::size_t o_stats = a.take<long long>(6);
         arena_bytes = a.off;
@@ -245,6 +248,8 @@ struct Pipeline::Impl {
         mbits = reinterpret_cast<uint32_t*>(arena + o_mbits);
         if (!backward) lists = reinterpret_cast<uint32_t*>(arena + o_lists);
         counts = reinterpret_cast<uint32_t*>(arena + o_cnt);
+        bil_count = reinterpret_cast<uint32_t*>(arena + o_bil);
+        bil_list = bil_count + 1;
         ctl = reinterpret_cast<uint32_t*>(arena + o_ctl);
         stats = reinterpret_cast<long long*>(arena + o_stats);
 
@@ -312,7 +317,10 @@ struct Pipeline::Impl {
 
     void enq_bilateral(const uint8_t* dmap, const uint8_t* guide, uint8_t* out, double* raw,
                        cudaStream_t st) {
-        if (tiled)
+        if (!raw && cu::bilateral_fast_available(radius))
+            CK(cu::bilateral_fast(dmap, guide, gm, radius, h_spatial.data(), spatial, range, out,
+                                  bil_list, bil_count, st));
+        else if (tiled)
             CK(cu::bilateral_tiled(dmap, guide, gm, radius, h_spatial.data(), range, out, raw, st));
         else
             CK(cu::bilateral(dmap, guide, gm, radius, spatial, range, out, raw, st));

@@ -23,6 +23,7 @@
 // bounds. Rows of a warp's window where only some outputs are inside their window are
 // run with warp-uniform per-output predicates; the bulk rows run branch-free.
 #include <cstdlib>
+#include <cstring>
 
 #include "p3s_cu.h"
 
@@ -321,6 +322,272 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_r(
     }
 }
 
+// ---- certified FP32 fast path (radius 16) ------------------------------------------------
+// Computes every output approximately and proves, per pixel, that the approximation rounds
+// to the same byte as the reference's exact FP64 sequence; pixels it cannot prove are
+// recomputed exactly (k_bilateral_fixup, reference order). The output bytes are therefore
+// identical to the reference's — only the arithmetic that decides them changes.
+//
+// Arithmetic: per window row, the left and right half-rows are accumulated as FP32 pairs
+// with packed sm_100 instructions — W = (s,s) * (R[kl], R[kr]) (FMUL2), SW += W (FADD2),
+// SV = W * (dl, dr) + SV (FFMA2) — then folded into FP64 totals per row.
+// Error bound (u = 2^-24, terms are non-negative): every weight carries <= 3 roundings
+// (float(s), float(R), product), a half-row sum <= 17 more, the half-row combine 1, the FP64
+// row accumulation and division < 1e-13 relative. So N~ = N(1+eN), D~ = D(1+eD) with
+// |eN| <= 21u+, |eD| <= 20u+, hence |v~ - v| <= v * 42u (+ FP64 slack). The reference's
+// own FP64 result is within v * 2200 * 2^-53 of v. Taps whose FP32 weight underflows add
+// an absolute error < 1e-33 against D >= 1 (the centre tap has weight exactly 1). We use
+// bound(v) = 44u * v + 1e-9 and accept floor(v~ + 0.5) only when v~ + 0.5 is farther than
+// bound(v) from every integer.
+template <int N>
+struct __align__(8) Spatial2Param {
+    unsigned long long s2[N];  // (float(s), float(s)) pairs
+};
+
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
+constexpr int kF32Copies = 32;  // LDS.32, one copy per lane: conflict-free
+
+template <int R, int P, bool ALL, bool EDGE, int N>
+__device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint32_t* __restrict__ row,
+                                         const char* __restrict__ tbl, int t, int x, int w,
+                                         const int (&base)[P], double (&ws)[P], double (&vs)[P]) {
+    constexpr int side = R + 1;
+    constexpr int kZero = 511 * 128;
+    unsigned long long SW[P], SV[P];
+    {
+        const uint32_t c = row[0];
+        const int gc = static_cast<int>(c & 0xFFFFu);
+        const float dc = static_cast<float>(c >> 16);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            SW[i] = 0ull;
+            SV[i] = 0ull;
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            float s, s_;
+            unpack2(sp.s2[(t - i) * side], s, s_);
+            const float wc = __fmul_rn(s, *reinterpret_cast<const float*>(tbl + base[i] + gc));
+            SW[i] = pack2(wc, 0.0f);
+            SV[i] = pack2(__fmul_rn(wc, dc), 0.0f);
+        }
+    }
+#pragma unroll 4
+    for (int dx = 1; dx <= R; ++dx) {
+        const uint32_t a = row[-dx], b = row[dx];
+        const int ga = static_cast<int>(a & 0xFFFFu), gb = static_cast<int>(b & 0xFFFFu);
+        const unsigned long long D2 =
+            pack2(static_cast<float>(a >> 16), static_cast<float>(b >> 16));
+        const bool oob_l = EDGE && (x - dx < 0);
+        const bool oob_r = EDGE && (x + dx >= w);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const unsigned long long S2 = sp.s2[(t - i) * side + dx];
+            const int ol = oob_l ? kZero + (base[i] & 127) : base[i] + ga;
+            const int orr = oob_r ? kZero + (base[i] & 127) : base[i] + gb;
+            const unsigned long long R2 = pack2(*reinterpret_cast<const float*>(tbl + ol),
+                                                *reinterpret_cast<const float*>(tbl + orr));
+            const unsigned long long W2 = fmul2(S2, R2);
+            SW[i] = fadd2(SW[i], W2);
+            SV[i] = ffma2(W2, D2, SV[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+        float a0, a1, b0, b1;
+        unpack2(SW[i], a0, a1);
+        unpack2(SV[i], b0, b1);
+        ws[i] = __dadd_rn(ws[i], static_cast<double>(__fadd_rn(a0, a1)));
+        vs[i] = __dadd_rn(vs[i], static_cast<double>(__fadd_rn(b0, b1)));
+    }
+}
+
+template <int R, int P, bool EDGE, int N>
+__device__ __forceinline__ void bilf_rows(const Spatial2Param<N>& sp, const uint32_t* tile_col,
+                                          const char* tbl, int x, int w, int tlo, int thi,
+                                          const int (&base)[P], double (&ws)[P],
+                                          double (&vs)[P]) {
+    constexpr int SW = kTX + 2 * R;
+    int t = tlo;
+    for (; t <= min(P - 2, thi); ++t)
+        bilf_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= min(2 * R, thi); ++t)
+        bilf_row<R, P, true, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= thi; ++t)
+        bilf_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+}
+
+template <int R, int P, int NW, int MINB, int N>
+__global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_f32(
+    const __grid_constant__ Spatial2Param<N> sp, const uint8_t* __restrict__ depth,
+    const uint8_t* __restrict__ guide, int pitch, int w, int h,
+    const double* __restrict__ range_g, uint8_t* __restrict__ out, uint32_t* __restrict__ list,
+    uint32_t* __restrict__ count, int tiles_x, int ntiles) {
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R;
+    constexpr int SH = TY + 2 * R;
+    extern __shared__ __align__(16) unsigned char smem[];
+    char* tbl = reinterpret_cast<char*>(smem);  // [512][32] floats
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + kSignedEntries * kF32Copies * 4);
+
+    for (int i = threadIdx.x; i < kSignedEntries * kF32Copies; i += blockDim.x) {
+        const int k = i / kF32Copies;
+        const int d = k < 511 ? abs(k - 255) : 256;
+        reinterpret_cast<float*>(tbl)[i] = d < 256 ? static_cast<float>(range_g[d]) : 0.0f;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane4 = lane * 4;
+    constexpr double kRel = 44.0 / 16777216.0;  // 44 u, u = 2^-24
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tx0 = (tile % tiles_x) * kTX;
+        const int ty0 = (tile / tiles_x) * TY;
+        __syncthreads();
+        for (int sy = warp; sy < SH; sy += NW) {
+            const int gy = ty0 - R + sy;
+            const bool yin = gy >= 0 && gy < h;
+            const uint8_t* grow = guide + static_cast<size_t>(yin ? gy : 0) * pitch;
+            const uint8_t* drow = depth + static_cast<size_t>(yin ? gy : 0) * pitch;
+            for (int sx = lane; sx < SW; sx += 32) {
+                const int gx = tx0 - R + sx;
+                uint32_t v = 0;
+                if (yin && gx >= 0 && gx < w)
+                    v = (static_cast<uint32_t>(grow[gx]) << 7) | (static_cast<uint32_t>(drow[gx]) << 16);
+                s_tile[sy * SW + sx] = v;
+            }
+        }
+        __syncthreads();
+
+        const int x = tx0 + lane;
+        const int yb = ty0 + warp * P;
+        if (yb >= h) continue;
+        const bool edge = (tx0 - R < 0) || (tx0 + kTX - 1 + R >= w);
+        const uint32_t* tile_col = s_tile + (warp * P) * SW + lane + R;
+        int base[P];
+        double ws[P], vs[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int gi = static_cast<int>((tile_col[(i + R) * SW] & 0xFFFFu) >> 7);
+            base[i] = (255 - gi) * 128 + lane4;
+            ws[i] = 0.0;
+            vs[i] = 0.0;
+        }
+        const int tlo = max(0, R - yb);
+        const int thi = min(P - 1 + 2 * R, h - 1 - yb + R);
+        if (edge)
+            bilf_rows<R, P, true>(sp, tile_col, tbl, x, w, tlo, thi, base, ws, vs);
+        else
+            bilf_rows<R, P, false>(sp, tile_col, tbl, x, w, tlo, thi, base, ws, vs);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int y = yb + i;
+            const bool valid = x < w && y < h;
+            bool uncertain = false;
+            if (valid) {
+                const double v = __ddiv_rn(vs[i], ws[i]);
+                const double f = __dadd_rn(v, 0.5);
+                const double r = floor(f);
+                const double dist = fmin(f - r, r + 1.0 - f);
+                const double bound = v * kRel + 1e-9;
+                uncertain = !(dist > bound);
+                out[static_cast<size_t>(y) * pitch + x] =
+                    uncertain ? 0 : (r <= 0.0 ? 0 : (r >= 255.0 ? 255 : static_cast<uint8_t>(static_cast<int>(r))));
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, uncertain);
+            if (m) {
+                uint32_t start = 0;
+                if (lane == 0) start = atomicAdd(count, static_cast<uint32_t>(__popc(m)));
+                start = __shfl_sync(0xFFFFFFFFu, start, 0);
+                if (uncertain)
+                    list[start + __popc(m & ((1u << lane) - 1u))] =
+                        static_cast<uint32_t>(y) * static_cast<uint32_t>(w) + static_cast<uint32_t>(x);
+            }
+        }
+    }
+}
+
+// Exact recompute of the uncertified pixels, one thread per pixel, the reference's order.
+__device__ __forceinline__ double bilateral_exact_px(const uint8_t* __restrict__ depth,
+                                                     const uint8_t* __restrict__ guide, int pitch,
+                                                     int w, int h, int R,
+                                                     const double* __restrict__ spatial,
+                                                     const double* __restrict__ range_g, int x,
+                                                     int y) {
+    const int side = R + 1;
+    const int gp = guide[static_cast<size_t>(y) * pitch + x];
+    double ws = 0.0, vs = 0.0;
+    const int dy0 = y - R < 0 ? -y : -R;
+    const int dy1 = y + R >= h ? h - 1 - y : R;
+    for (int dy = dy0; dy <= dy1; ++dy) {
+        const uint8_t* grow = guide + static_cast<size_t>(y + dy) * pitch;
+        const uint8_t* drow = depth + static_cast<size_t>(y + dy) * pitch;
+        const double* s = spatial + static_cast<size_t>(dy + R) * side;
+        {
+            const double wc = __dmul_rn(s[0], range_g[__usad(gp, grow[x], 0)]);
+            ws = __dadd_rn(ws, wc);
+            vs = __dadd_rn(vs, __dmul_rn(wc, static_cast<double>(drow[x])));
+        }
+        for (int dx = 1; dx <= R; ++dx) {
+            const bool lin = x - dx >= 0, rin = x + dx < w;
+            if (lin && rin) {
+                const double wl = __dmul_rn(s[dx], range_g[__usad(gp, grow[x - dx], 0)]);
+                const double wr = __dmul_rn(s[dx], range_g[__usad(gp, grow[x + dx], 0)]);
+                ws = __dadd_rn(ws, __dadd_rn(wl, wr));
+                vs = __dadd_rn(vs, __dadd_rn(__dmul_rn(wl, static_cast<double>(drow[x - dx])),
+                                             __dmul_rn(wr, static_cast<double>(drow[x + dx]))));
+            } else if (lin) {
+                const double wl = __dmul_rn(s[dx], range_g[__usad(gp, grow[x - dx], 0)]);
+                ws = __dadd_rn(ws, wl);
+                vs = __dadd_rn(vs, __dmul_rn(wl, static_cast<double>(drow[x - dx])));
+            } else if (rin) {
+                const double wr = __dmul_rn(s[dx], range_g[__usad(gp, grow[x + dx], 0)]);
+                ws = __dadd_rn(ws, wr);
+                vs = __dadd_rn(vs, __dmul_rn(wr, static_cast<double>(drow[x + dx])));
+            }
+        }
+    }
+    return __ddiv_rn(vs, ws);
+}
+
+__global__ void __launch_bounds__(128) k_bilateral_fixup(
+    const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
+    int h, int R, const double* __restrict__ spatial, const double* __restrict__ range_g,
+    uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
+    const uint32_t* __restrict__ count) {
+    const uint32_t n = *count;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t idx = list[k];
+        const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
+        const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
+        const double v = bilateral_exact_px(depth, guide, pitch, w, h, R, spatial, range_g, x, y);
+        out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(v);
+    }
+}
+
 // Any radius: one thread per output, tables and pixels read through the L1 path.
 __global__ void __launch_bounds__(256) k_bilateral_generic(
     const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
@@ -428,7 +695,69 @@ cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
     return cudaGetLastError();
 }
 
+template <int R, int P, int NW, int MINB>
+cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
+                       const double* spatial_host, const double* spatial_dev, const double* range,
+                       uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
+    constexpr int N = (2 * R + 1) * (R + 1);
+    Spatial2Param<N> sp;
+    for (int i = 0; i < N; ++i) {
+        const float f = static_cast<float>(spatial_host[i]);
+        unsigned u;
+        memcpy(&u, &f, 4);
+        sp.s2[i] = (static_cast<unsigned long long>(u) << 32) | u;
+    }
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
+    const size_t smem = kSignedEntries * kF32Copies * 4 + static_cast<size_t>(SW) * SH * 4;
+    static int configured_dev[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured_dev[dev]) {
+        cudaFuncSetAttribute(k_bilateral_f32<R, P, NW, MINB, N>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured_dev[dev] = 1;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_f32<R, P, NW, MINB, N>,
+                                                  NW * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int tiles_x = (gm.w + kTX - 1) / kTX;
+    const int tiles_y = (gm.h + TY - 1) / TY;
+    const int ntiles = tiles_x * tiles_y;
+    const int grid = min(ntiles, per_sm * sm_count());
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    k_bilateral_f32<R, P, NW, MINB, N><<<grid, NW * 32, smem, st>>>(
+        sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_bilateral_fixup<<<sm_count() * 4, 128, 0, st>>>(depth, guide, gm.pitch, gm.w, gm.h, R,
+                                                      spatial_dev, range, out, list, count);
+    return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                           const double* spatial_host, const double* spatial_dev,
+                           const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
+                           cudaStream_t st) {
+    const char* v = getenv("P3S_BIL_FAST");
+    const int var = v ? atoi(v) : 1;
+    if (radius == 16 && var == 1)
+        return launch_f32<16, 4, 16, 2>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                        list, count, st);
+    if (radius == 16 && var == 2)
+        return launch_f32<16, 8, 8, 2>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                       list, count, st);
+    return bilateral_tiled(depth, guide, gm, radius, spatial_host, range, out, nullptr, st);
+}
+
+bool bilateral_fast_available(int radius) {
+    const char* v = getenv("P3S_BIL_FAST");
+    return radius == 16 && !(v && atoi(v) == 0);
+}
 
 // spatial: device table for the generic kernel, in the layout s[(dy+R)*(R+1)+dx] (dx>=0).
 // The tiled kernels take the same table by value; engine.cpp passes the host copy via

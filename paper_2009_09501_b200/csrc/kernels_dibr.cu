@@ -7,7 +7,8 @@
 //     key = (d + 1) << 22 | (0x3FFFFF - x)
 // whose maximum is "largest depth, then smallest source column" — exactly the winner of
 // the reference's ascending-x scan with strict '>' (dibr.cpp:88-99) — and independent of
-// the order atomics land in. The resolve phase gathers each destination's winning colour
+// the order atomics land in (plain stores first, atomicMax only for the few sources that
+// lost a slot; see the splat phase). The resolve phase gathers each destination's winning colour
 // from shared memory and writes 16 pixels per thread with 16-byte stores; a destination
 // without a key is damaged. Output routing (EyeOut) writes only the planes a format
 // needs: the fused anaglyph writes left.R and right.G/B straight into the output image,
@@ -98,15 +99,33 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
     const uint8_t* s_d = s_src + 3 * wpad;
 
     if (!backward) {
+        // Splat in two phases. (1) Every source stores its key with a plain store; where
+        // several sources hit one destination an arbitrary one survives. (2) Every source
+        // whose key did not survive (only at depth discontinuities) re-applies it with
+        // atomicMax, so each slot ends at the maximum key — the same winner as a full
+        // atomicMax splat — at a fraction of the shared-memory atomics.
         for (int x = tid; x < w; x += blockDim.x) {
             const int d = s_d[x];
             const double sigma = s_shift[d];
             const double xd = static_cast<double>(x);
-            const int dst_l = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
-            const int dst_r = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
+            const int a = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
+            const int b = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
             const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
-            if (static_cast<unsigned>(dst_l) < static_cast<unsigned>(w)) atomicMax(&keyL[dst_l], key);
-            if (static_cast<unsigned>(dst_r) < static_cast<unsigned>(w)) atomicMax(&keyR[dst_r], key);
+            if (static_cast<unsigned>(a) < static_cast<unsigned>(w)) keyL[a] = key;
+            if (static_cast<unsigned>(b) < static_cast<unsigned>(w)) keyR[b] = key;
+        }
+        __syncthreads();
+        for (int x = tid; x < w; x += blockDim.x) {
+            const int d = s_d[x];
+            const double sigma = s_shift[d];
+            const double xd = static_cast<double>(x);
+            const int a = __double2int_rz(__dadd_rn(xd, sigma));
+            const int b = __double2int_rz(__dsub_rn(xd, sigma));
+            const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
+            if (static_cast<unsigned>(a) < static_cast<unsigned>(w) && keyL[a] != key)
+                atomicMax(&keyL[a], key);
+            if (static_cast<unsigned>(b) < static_cast<unsigned>(w) && keyR[b] != key)
+                atomicMax(&keyR[b], key);
         }
         __syncthreads();
     }

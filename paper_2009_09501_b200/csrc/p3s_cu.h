@@ -56,6 +56,14 @@ cudaError_t bilateral_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm,
                             const double* spatial_host, const double* range, uint8_t* out,
                             double* raw, cudaStream_t st);
 int bilateral_tiled_max_radius();
+// Certified FP32 fast path (same output bytes): approximate every pixel, prove the byte,
+// recompute the unprovable ones exactly. `list`/`count`: device scratch for the fallback
+// pixel list (capacity w*h). Falls back to bilateral_tiled for radii it does not cover.
+cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                           const double* spatial_host, const double* spatial_dev,
+                           const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
+                           cudaStream_t st);
+bool bilateral_fast_available(int radius);
 cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                       const double* spatial, const double* range, uint8_t* out, double* raw,
                       cudaStream_t st);
