@@ -192,7 +192,11 @@ __global__ void __launch_bounds__(kNW * 32) k_bilateral_tiled(
 // Edge tiles route out-of-image taps to the zero sentinel entry with a select.
 constexpr int kSignedEntries = 512;  // k = 0..510, entry 511 = 0.0 sentinel
 
-template <int R, int P, bool ALL, bool EDGE, int N>
+// Spatial table zero-padded by P-1 rows on each side (row index t - i + P - 1): an output
+// outside its window adds wl = wr = 0, and ws + (0 + 0) == ws, vs + (0*d + 0*d) == vs
+// exactly for the non-negative running sums, so every row is branch-free and the result is
+// still the reference's bit pattern.
+template <int R, int P, bool EDGE, int N>
 __device__ __forceinline__ void bilr_row(const SpatialParam<N>& sp, const uint32_t* __restrict__ row,
                                          const char* __restrict__ tbl, int t, int x, int w,
                                          const int (&base)[P], double (&ws)[P],
@@ -205,8 +209,7 @@ __device__ __forceinline__ void bilr_row(const SpatialParam<N>& sp, const uint32
         const double dc = static_cast<double>(c >> 16);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
-            const double s = sp.s[(t - i) * side];
+            const double s = sp.s[(t - i + P - 1) * side];
             const double wc = __dmul_rn(s, *reinterpret_cast<const double*>(tbl + base[i] + gc));
             ws[i] = __dadd_rn(ws[i], wc);
             vs[i] = __dadd_rn(vs[i], __dmul_rn(wc, dc));
@@ -221,8 +224,7 @@ __device__ __forceinline__ void bilr_row(const SpatialParam<N>& sp, const uint32
         const bool oob_r = EDGE && (x + dx >= w);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
-            const double s = sp.s[(t - i) * side + dx];
+            const double s = sp.s[(t - i + P - 1) * side + dx];
             const int ol = oob_l ? kZero + (base[i] & 127) : base[i] + ga;
             const int orr = oob_r ? kZero + (base[i] & 127) : base[i] + gb;
             const double wl = __dmul_rn(s, *reinterpret_cast<const double*>(tbl + ol));
@@ -239,13 +241,8 @@ __device__ __forceinline__ void bilr_rows(const SpatialParam<N>& sp, const uint3
                                           const int (&base)[P], double (&ws)[P],
                                           double (&vs)[P]) {
     constexpr int SW = kTX + 2 * R;
-    int t = tlo;
-    for (; t <= min(P - 2, thi); ++t)
-        bilr_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
-    for (; t <= min(2 * R, thi); ++t)
-        bilr_row<R, P, true, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
-    for (; t <= thi; ++t)
-        bilr_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (int t = tlo; t <= thi; ++t)
+        bilr_row<R, P, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
 }
 
 template <int R, int P, int NW, int MINB, int N>
@@ -371,7 +368,10 @@ __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsign
 
 constexpr int kF32Copies = 32;  // LDS.32, one copy per lane: conflict-free
 
-template <int R, int P, bool ALL, bool EDGE, int N>
+// The spatial table is zero-padded to dy in [-(R+P-1), R+P-1] (row index t - i + P - 1),
+// so every window row runs the same branch-free body: outputs outside their window add
+// exact zeros.
+template <int R, int P, bool EDGE, int N>
 __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint32_t* __restrict__ row,
                                          const char* __restrict__ tbl, int t, int x, int w,
                                          const int (&base)[P], double (&ws)[P], double (&vs)[P]) {
@@ -386,9 +386,8 @@ __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint3
         for (int i = 0; i < P; ++i) {
             SW[i] = 0ull;
             SV[i] = 0ull;
-            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
             float s, s_;
-            unpack2(sp.s2[(t - i) * side], s, s_);
+            unpack2(sp.s2[(t - i + P - 1) * side], s, s_);
             const float wc = __fmul_rn(s, *reinterpret_cast<const float*>(tbl + base[i] + gc));
             SW[i] = pack2(wc, 0.0f);
             SV[i] = pack2(__fmul_rn(wc, dc), 0.0f);
@@ -404,8 +403,7 @@ __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint3
         const bool oob_r = EDGE && (x + dx >= w);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
-            const unsigned long long S2 = sp.s2[(t - i) * side + dx];
+            const unsigned long long S2 = sp.s2[(t - i + P - 1) * side + dx];
             const int ol = oob_l ? kZero + (base[i] & 127) : base[i] + ga;
             const int orr = oob_r ? kZero + (base[i] & 127) : base[i] + gb;
             const unsigned long long R2 = pack2(*reinterpret_cast<const float*>(tbl + ol),
@@ -417,7 +415,6 @@ __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint3
     }
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-        if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
         float a0, a1, b0, b1;
         unpack2(SW[i], a0, a1);
         unpack2(SV[i], b0, b1);
@@ -432,13 +429,8 @@ __device__ __forceinline__ void bilf_rows(const Spatial2Param<N>& sp, const uint
                                           const int (&base)[P], double (&ws)[P],
                                           double (&vs)[P]) {
     constexpr int SW = kTX + 2 * R;
-    int t = tlo;
-    for (; t <= min(P - 2, thi); ++t)
-        bilf_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
-    for (; t <= min(2 * R, thi); ++t)
-        bilf_row<R, P, true, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
-    for (; t <= thi; ++t)
-        bilf_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (int t = tlo; t <= thi; ++t)
+        bilf_row<R, P, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
 }
 
 template <int R, int P, int NW, int MINB, int N>
@@ -573,6 +565,58 @@ __device__ __forceinline__ double bilateral_exact_px(const uint8_t* __restrict__
     return __ddiv_rn(vs, ws);
 }
 
+// Radius-specialised exact recompute: pixels at least R from the left/right borders load
+// each window row's 2R+1 guide/depth bytes up front (dx unrolled, loads independent of the
+// accumulation chains), then run the reference-order FP64 updates; others take the
+// generic path. One thread per listed pixel.
+template <int R>
+__global__ void __launch_bounds__(128) k_bilateral_fixup_r(
+    const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
+    int h, const double* __restrict__ spatial, const double* __restrict__ range_g,
+    uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
+    const uint32_t* __restrict__ count) {
+    const uint32_t n = *count;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t idx = list[k];
+        const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
+        const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
+        double v;
+        if (x < R || x + R >= w) {
+            v = bilateral_exact_px(depth, guide, pitch, w, h, R, spatial, range_g, x, y);
+        } else {
+            const int gp = __ldg(guide + static_cast<size_t>(y) * pitch + x);
+            double ws = 0.0, vs = 0.0;
+            const int dy0 = y - R < 0 ? -y : -R;
+            const int dy1 = y + R >= h ? h - 1 - y : R;
+            for (int dy = dy0; dy <= dy1; ++dy) {
+                const uint8_t* grow = guide + static_cast<size_t>(y + dy) * pitch + x;
+                const uint8_t* drow = depth + static_cast<size_t>(y + dy) * pitch + x;
+                const double* srow = spatial + static_cast<size_t>(dy + R) * (R + 1);
+                int g[2 * R + 1], d[2 * R + 1];
+#pragma unroll
+                for (int j = 0; j <= 2 * R; ++j) {
+                    g[j] = __ldg(grow + j - R);
+                    d[j] = __ldg(drow + j - R);
+                }
+                const double wc = __dmul_rn(__ldg(srow), __ldg(range_g + __usad(gp, g[R], 0)));
+                ws = __dadd_rn(ws, wc);
+                vs = __dadd_rn(vs, __dmul_rn(wc, static_cast<double>(d[R])));
+#pragma unroll
+                for (int dx = 1; dx <= R; ++dx) {
+                    const double sdx = __ldg(srow + dx);
+                    const double wl = __dmul_rn(sdx, __ldg(range_g + __usad(gp, g[R - dx], 0)));
+                    const double wr = __dmul_rn(sdx, __ldg(range_g + __usad(gp, g[R + dx], 0)));
+                    ws = __dadd_rn(ws, __dadd_rn(wl, wr));
+                    vs = __dadd_rn(vs, __dadd_rn(__dmul_rn(wl, static_cast<double>(d[R - dx])),
+                                                 __dmul_rn(wr, static_cast<double>(d[R + dx]))));
+                }
+            }
+            v = __ddiv_rn(vs, ws);
+        }
+        out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(v);
+    }
+}
+
 __global__ void __launch_bounds__(128) k_bilateral_fixup(
     const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
     int h, int R, const double* __restrict__ spatial, const double* __restrict__ range_g,
@@ -668,9 +712,10 @@ template <int R, int P, int NW, int MINB>
 cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
                      const double* spatial_host, const double* range, uint8_t* out, double* raw,
                      cudaStream_t st) {
-    constexpr int N = (2 * R + 1) * (R + 1);
+    constexpr int N = (2 * R + 2 * P - 1) * (R + 1);  // zero-padded by P-1 rows each side
     SpatialParam<N> sp;
-    for (int i = 0; i < N; ++i) sp.s[i] = spatial_host[i];
+    for (int i = 0; i < N; ++i) sp.s[i] = 0.0;
+    for (int i = 0; i < (2 * R + 1) * (R + 1); ++i) sp.s[i + (P - 1) * (R + 1)] = spatial_host[i];
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
     const size_t smem = kSignedEntries * kRangeCopies * 8 + static_cast<size_t>(SW) * SH * 4;
@@ -699,13 +744,14 @@ template <int R, int P, int NW, int MINB>
 cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
                        const double* spatial_host, const double* spatial_dev, const double* range,
                        uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
-    constexpr int N = (2 * R + 1) * (R + 1);
+    constexpr int N = (2 * R + 2 * P - 1) * (R + 1);  // zero-padded by P-1 rows each side
     Spatial2Param<N> sp;
-    for (int i = 0; i < N; ++i) {
+    for (int i = 0; i < N; ++i) sp.s2[i] = 0ull;
+    for (int i = 0; i < (2 * R + 1) * (R + 1); ++i) {
         const float f = static_cast<float>(spatial_host[i]);
         unsigned u;
         memcpy(&u, &f, 4);
-        sp.s2[i] = (static_cast<unsigned long long>(u) << 32) | u;
+        sp.s2[i + (P - 1) * (R + 1)] = (static_cast<unsigned long long>(u) << 32) | u;
     }
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
@@ -732,8 +778,8 @@ cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_bilateral_fixup<<<sm_count() * 4, 128, 0, st>>>(depth, guide, gm.pitch, gm.w, gm.h, R,
-                                                      spatial_dev, range, out, list, count);
+    k_bilateral_fixup_r<R><<<sm_count() * 4, 128, 0, st>>>(depth, guide, gm.pitch, gm.w, gm.h,
+                                                           spatial_dev, range, out, list, count);
     return cudaGetLastError();
 }
 

@@ -29,3 +29,16 @@ for i in range(a.steps):
     pipe.run(bufs[i % len(bufs)].addr)
 p3s.stream_sync(pipe.stream)
 print("done", a.steps, "steps")
+if os.environ.get("P3S_REPORT_FIXUP"):
+    import ctypes as C
+    # count of uncertified pixels of the last bilateral (read through the stage API)
+    chk = oracle.load("port")
+    img = chk.synthetic_frame(a.w, a.h, 1)
+    import numpy as np
+    luma = p3s.luma(img)
+    depth = p3s.generate_depth(img, cfg)
+    raw = p3s.cross_bilateral_raw(depth, luma, cfg)
+    f = raw + 0.5
+    dist = np.minimum(f - np.floor(f), np.floor(f) + 1 - f)
+    bound = raw * 44.0 / 2**24 + 1e-9
+    print("uncertified pixels (predicted from raw):", int((dist <= bound).sum()), "of", raw.size)
