@@ -192,11 +192,7 @@ __global__ void __launch_bounds__(kNW * 32) k_bilateral_tiled(
 // Edge tiles route out-of-image taps to the zero sentinel entry with a select.
 constexpr int kSignedEntries = 512;  // k = 0..510, entry 511 = 0.0 sentinel
 
-// Spatial table zero-padded by P-1 rows on each side (row index t - i + P - 1): an output
-// outside its window adds wl = wr = 0, and ws + (0 + 0) == ws, vs + (0*d + 0*d) == vs
-// exactly for the non-negative running sums, so every row is branch-free and the result is
-// still the reference's bit pattern.
-template <int R, int P, bool EDGE, int N>
+template <int R, int P, bool ALL, bool EDGE, int N>
 __device__ __forceinline__ void bilr_row(const SpatialParam<N>& sp, const uint32_t* __restrict__ row,
                                          const char* __restrict__ tbl, int t, int x, int w,
                                          const int (&base)[P], double (&ws)[P],
@@ -209,7 +205,8 @@ __device__ __forceinline__ void bilr_row(const SpatialParam<N>& sp, const uint32
         const double dc = static_cast<double>(c >> 16);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            const double s = sp.s[(t - i + P - 1) * side];
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const double s = sp.s[(t - i) * side];
             const double wc = __dmul_rn(s, *reinterpret_cast<const double*>(tbl + base[i] + gc));
             ws[i] = __dadd_rn(ws[i], wc);
             vs[i] = __dadd_rn(vs[i], __dmul_rn(wc, dc));
@@ -224,7 +221,8 @@ __device__ __forceinline__ void bilr_row(const SpatialParam<N>& sp, const uint32
         const bool oob_r = EDGE && (x + dx >= w);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            const double s = sp.s[(t - i + P - 1) * side + dx];
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const double s = sp.s[(t - i) * side + dx];
             const int ol = oob_l ? kZero + (base[i] & 127) : base[i] + ga;
             const int orr = oob_r ? kZero + (base[i] & 127) : base[i] + gb;
             const double wl = __dmul_rn(s, *reinterpret_cast<const double*>(tbl + ol));
@@ -241,8 +239,13 @@ __device__ __forceinline__ void bilr_rows(const SpatialParam<N>& sp, const uint3
                                           const int (&base)[P], double (&ws)[P],
                                           double (&vs)[P]) {
     constexpr int SW = kTX + 2 * R;
-    for (int t = tlo; t <= thi; ++t)
-        bilr_row<R, P, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    int t = tlo;
+    for (; t <= min(P - 2, thi); ++t)
+        bilr_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= min(2 * R, thi); ++t)
+        bilr_row<R, P, true, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= thi; ++t)
+        bilr_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
 }
 
 template <int R, int P, int NW, int MINB, int N>
@@ -368,10 +371,7 @@ __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsign
 
 constexpr int kF32Copies = 32;  // LDS.32, one copy per lane: conflict-free
 
-// The spatial table is zero-padded to dy in [-(R+P-1), R+P-1] (row index t - i + P - 1),
-// so every window row runs the same branch-free body: outputs outside their window add
-// exact zeros.
-template <int R, int P, bool EDGE, int N>
+template <int R, int P, bool ALL, bool EDGE, int N>
 __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint32_t* __restrict__ row,
                                          const char* __restrict__ tbl, int t, int x, int w,
                                          const int (&base)[P], double (&ws)[P], double (&vs)[P]) {
@@ -386,8 +386,9 @@ __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint3
         for (int i = 0; i < P; ++i) {
             SW[i] = 0ull;
             SV[i] = 0ull;
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
             float s, s_;
-            unpack2(sp.s2[(t - i + P - 1) * side], s, s_);
+            unpack2(sp.s2[(t - i) * side], s, s_);
             const float wc = __fmul_rn(s, *reinterpret_cast<const float*>(tbl + base[i] + gc));
             SW[i] = pack2(wc, 0.0f);
             SV[i] = pack2(__fmul_rn(wc, dc), 0.0f);
@@ -403,7 +404,8 @@ __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint3
         const bool oob_r = EDGE && (x + dx >= w);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            const unsigned long long S2 = sp.s2[(t - i + P - 1) * side + dx];
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const unsigned long long S2 = sp.s2[(t - i) * side + dx];
             const int ol = oob_l ? kZero + (base[i] & 127) : base[i] + ga;
             const int orr = oob_r ? kZero + (base[i] & 127) : base[i] + gb;
             const unsigned long long R2 = pack2(*reinterpret_cast<const float*>(tbl + ol),
@@ -415,6 +417,7 @@ __device__ __forceinline__ void bilf_row(const Spatial2Param<N>& sp, const uint3
     }
 #pragma unroll
     for (int i = 0; i < P; ++i) {
+        if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
         float a0, a1, b0, b1;
         unpack2(SW[i], a0, a1);
         unpack2(SV[i], b0, b1);
@@ -429,8 +432,13 @@ __device__ __forceinline__ void bilf_rows(const Spatial2Param<N>& sp, const uint
                                           const int (&base)[P], double (&ws)[P],
                                           double (&vs)[P]) {
     constexpr int SW = kTX + 2 * R;
-    for (int t = tlo; t <= thi; ++t)
-        bilf_row<R, P, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    int t = tlo;
+    for (; t <= min(P - 2, thi); ++t)
+        bilf_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= min(2 * R, thi); ++t)
+        bilf_row<R, P, true, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
+    for (; t <= thi; ++t)
+        bilf_row<R, P, false, EDGE>(sp, tile_col + t * SW, tbl, t, x, w, base, ws, vs);
 }
 
 template <int R, int P, int NW, int MINB, int N>
@@ -565,55 +573,93 @@ __device__ __forceinline__ double bilateral_exact_px(const uint8_t* __restrict__
     return __ddiv_rn(vs, ws);
 }
 
-// Radius-specialised exact recompute: pixels at least R from the left/right borders load
-// each window row's 2R+1 guide/depth bytes up front (dx unrolled, loads independent of the
-// accumulation chains), then run the reference-order FP64 updates; others take the
-// generic path. One thread per listed pixel.
+// Exact recompute of the uncertified pixels, one warp per pixel. The warp stages the
+// pixel's (2R+1)^2 window in shared memory, then for each window row (dy ascending) lanes
+// 0..R compute that row's terms in parallel — lane 0 the centre (wc, wc*d), lane dx the
+// mirrored pair (wl + wr, wl*dl + wr*dr) or the single in-image side — with the
+// reference's separately rounded operations, and lane 0 adds them to the running sums in
+// the reference order (centre, then dx = 1..R). A pair with both sides outside the image
+// contributes +0, which leaves the non-negative sums unchanged, exactly like the
+// reference's skipped update. The serial FP64 chain is the only latency left.
 template <int R>
-__global__ void __launch_bounds__(128) k_bilateral_fixup_r(
+__global__ void __launch_bounds__(128) k_bilateral_fixup_warp(
     const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
     int h, const double* __restrict__ spatial, const double* __restrict__ range_g,
     uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
     const uint32_t* __restrict__ count) {
+    constexpr int S = 2 * R + 1;
+    __shared__ uint8_t s_g[4][S * S];
+    __shared__ uint8_t s_d[4][S * S];
+    __shared__ double s_t[4][R + 1], s_u[4][R + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t n = *count;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t k = blockIdx.x * (blockDim.x >> 5) + wib; k < n; k += nwarps) {
         const uint32_t idx = list[k];
         const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
         const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
-        double v;
-        if (x < R || x + R >= w) {
-            v = bilateral_exact_px(depth, guide, pitch, w, h, R, spatial, range_g, x, y);
-        } else {
-            const int gp = __ldg(guide + static_cast<size_t>(y) * pitch + x);
-            double ws = 0.0, vs = 0.0;
-            const int dy0 = y - R < 0 ? -y : -R;
-            const int dy1 = y + R >= h ? h - 1 - y : R;
-            for (int dy = dy0; dy <= dy1; ++dy) {
-                const uint8_t* grow = guide + static_cast<size_t>(y + dy) * pitch + x;
-                const uint8_t* drow = depth + static_cast<size_t>(y + dy) * pitch + x;
-                const double* srow = spatial + static_cast<size_t>(dy + R) * (R + 1);
-                int g[2 * R + 1], d[2 * R + 1];
-#pragma unroll
-                for (int j = 0; j <= 2 * R; ++j) {
-                    g[j] = __ldg(grow + j - R);
-                    d[j] = __ldg(drow + j - R);
-                }
-                const double wc = __dmul_rn(__ldg(srow), __ldg(range_g + __usad(gp, g[R], 0)));
-                ws = __dadd_rn(ws, wc);
-                vs = __dadd_rn(vs, __dmul_rn(wc, static_cast<double>(d[R])));
-#pragma unroll
-                for (int dx = 1; dx <= R; ++dx) {
+        const int dy0 = y - R < 0 ? -y : -R;
+        const int dy1 = y + R >= h ? h - 1 - y : R;
+        for (int e = lane; e < S * S; e += 32) {
+            const int r = e / S, c = e - r * S;
+            const int gy = y - R + r, gx = x - R + c;
+            uint8_t gv = 0, dv = 0;
+            if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
+                gv = __ldg(guide + static_cast<size_t>(gy) * pitch + gx);
+                dv = __ldg(depth + static_cast<size_t>(gy) * pitch + gx);
+            }
+            s_g[wib][e] = gv;
+            s_d[wib][e] = dv;
+        }
+        __syncwarp();
+        const int gp = s_g[wib][R * S + R];
+        double ws = 0.0, vs = 0.0;
+        for (int dy = dy0; dy <= dy1; ++dy) {
+            const int r = dy + R;
+            if (lane <= R) {
+                const double* srow = spatial + static_cast<size_t>(r) * (R + 1);
+                const uint8_t* gr = s_g[wib] + r * S + R;
+                const uint8_t* dr = s_d[wib] + r * S + R;
+                double t = 0.0, u = 0.0;
+                if (lane == 0) {
+                    const double wc = __dmul_rn(__ldg(srow), __ldg(range_g + __usad(gp, gr[0], 0)));
+                    t = wc;
+                    u = __dmul_rn(wc, static_cast<double>(dr[0]));
+                } else {
+                    const int dx = lane;
+                    const bool lin = x - dx >= 0, rin = x + dx < w;
                     const double sdx = __ldg(srow + dx);
-                    const double wl = __dmul_rn(sdx, __ldg(range_g + __usad(gp, g[R - dx], 0)));
-                    const double wr = __dmul_rn(sdx, __ldg(range_g + __usad(gp, g[R + dx], 0)));
-                    ws = __dadd_rn(ws, __dadd_rn(wl, wr));
-                    vs = __dadd_rn(vs, __dadd_rn(__dmul_rn(wl, static_cast<double>(d[R - dx])),
-                                                 __dmul_rn(wr, static_cast<double>(d[R + dx]))));
+                    if (lin && rin) {
+                        const double wl = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[-dx], 0)));
+                        const double wr = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[dx], 0)));
+                        t = __dadd_rn(wl, wr);
+                        u = __dadd_rn(__dmul_rn(wl, static_cast<double>(dr[-dx])),
+                                      __dmul_rn(wr, static_cast<double>(dr[dx])));
+                    } else if (lin) {
+                        const double wl = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[-dx], 0)));
+                        t = wl;
+                        u = __dmul_rn(wl, static_cast<double>(dr[-dx]));
+                    } else if (rin) {
+                        const double wr = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[dx], 0)));
+                        t = wr;
+                        u = __dmul_rn(wr, static_cast<double>(dr[dx]));
+                    }
+                }
+                s_t[wib][lane] = t;
+                s_u[wib][lane] = u;
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 0; j <= R; ++j) {
+                    ws = __dadd_rn(ws, s_t[wib][j]);
+                    vs = __dadd_rn(vs, s_u[wib][j]);
                 }
             }
-            v = __ddiv_rn(vs, ws);
+            __syncwarp();
         }
-        out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(v);
+        if (lane == 0) out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(__ddiv_rn(vs, ws));
+        __syncwarp();
     }
 }
 
@@ -712,10 +758,9 @@ template <int R, int P, int NW, int MINB>
 cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
                      const double* spatial_host, const double* range, uint8_t* out, double* raw,
                      cudaStream_t st) {
-    constexpr int N = (2 * R + 2 * P - 1) * (R + 1);  // zero-padded by P-1 rows each side
+    constexpr int N = (2 * R + 1) * (R + 1);
     SpatialParam<N> sp;
-    for (int i = 0; i < N; ++i) sp.s[i] = 0.0;
-    for (int i = 0; i < (2 * R + 1) * (R + 1); ++i) sp.s[i + (P - 1) * (R + 1)] = spatial_host[i];
+    for (int i = 0; i < N; ++i) sp.s[i] = spatial_host[i];
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
     const size_t smem = kSignedEntries * kRangeCopies * 8 + static_cast<size_t>(SW) * SH * 4;
@@ -744,14 +789,13 @@ template <int R, int P, int NW, int MINB>
 cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
                        const double* spatial_host, const double* spatial_dev, const double* range,
                        uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
-    constexpr int N = (2 * R + 2 * P - 1) * (R + 1);  // zero-padded by P-1 rows each side
+    constexpr int N = (2 * R + 1) * (R + 1);
     Spatial2Param<N> sp;
-    for (int i = 0; i < N; ++i) sp.s2[i] = 0ull;
-    for (int i = 0; i < (2 * R + 1) * (R + 1); ++i) {
+    for (int i = 0; i < N; ++i) {
         const float f = static_cast<float>(spatial_host[i]);
         unsigned u;
         memcpy(&u, &f, 4);
-        sp.s2[i + (P - 1) * (R + 1)] = (static_cast<unsigned long long>(u) << 32) | u;
+        sp.s2[i] = (static_cast<unsigned long long>(u) << 32) | u;
     }
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
@@ -778,8 +822,8 @@ cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_bilateral_fixup_r<R><<<sm_count() * 4, 128, 0, st>>>(depth, guide, gm.pitch, gm.w, gm.h,
-                                                           spatial_dev, range, out, list, count);
+    k_bilateral_fixup_warp<R><<<sm_count() * 8, 128, 0, st>>>(
+        depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
 }
 
