@@ -154,11 +154,12 @@ struct Pipeline::Impl {
     double *range = nullptr, *spatial = nullptr, *shift = nullptr;
     uint8_t *ana = nullptr, *hsbs = nullptr, *fsbs = nullptr, *eyes = nullptr;
     uint32_t* mbits = nullptr;
-    uint32_t* lists = nullptr;  // [eye][list|list2|repair][N]
+    uint32_t* lists = nullptr;  // [eye][N] damaged pixel lists
+    unsigned char* ipa = nullptr;  // inpaint arena (state words + tile flags)
     uint32_t* counts = nullptr;  // 2
     uint32_t* bil_list = nullptr;   // bilateral fast path: uncertified pixels (N)
     uint32_t* bil_count = nullptr;  // 1
-    uint32_t* ctl = nullptr;     // 64
+    uint32_t* ctl = nullptr;     // 128
     long long* stats = nullptr;  // 6
     // stage-API extras (allocated on first use)
     unsigned char* stage_arena = nullptr;
@@ -224,10 +225,11 @@ struct Pipeline::Impl {
             (formats & kFormatFsbs) ? a.take<uint8_t>(3 * static_cast<std::size_t>(fpitch) * h) : 0;
         const std::size_t o_eyes = a.take<uint8_t>(route == kEyes ? 6 * P : 0);
         const std::size_t o_mbits = a.take<uint32_t>(2 * static_cast<std::size_t>(mwords) * h);
-        const std::size_t o_lists = a.take<uint32_t>(backward ? 0 : 6 * N);
+        const std::size_t o_lists = a.take<uint32_t>(backward ? 0 : 2 * N);
+        const std::size_t o_ipa = a.take<unsigned char>(backward ? 0 : cu::inpaint_scratch_bytes(w, h));
         const std::size_t o_cnt = a.take<uint32_t>(2);
         const std::size_t o_bil = a.take<uint32_t>(N + 1);
-        const std::size_t o_ctl = a.take<uint32_t>(64);
+        const std::size_t o_ctl = a.take<uint32_t>(128);
         const std::size_t o_stats = a.take<long long>(6);
         arena_bytes = a.off;
         CK(cudaSetDevice(dev));
@@ -246,7 +248,10 @@ struct Pipeline::Impl {
         if (formats & kFormatFsbs) fsbs = arena + o_fsbs;
         if (route == kEyes) eyes = arena + o_eyes;
         mbits = reinterpret_cast<uint32_t*>(arena + o_mbits);
-        if (!backward) lists = reinterpret_cast<uint32_t*>(arena + o_lists);
+        if (!backward) {
+            lists = reinterpret_cast<uint32_t*>(arena + o_lists);
+            ipa = arena + o_ipa;
+        }
         counts = reinterpret_cast<uint32_t*>(arena + o_cnt);
         bil_count = reinterpret_cast<uint32_t*>(arena + o_bil);
         bil_list = bil_count + 1;
@@ -296,7 +301,10 @@ struct Pipeline::Impl {
     }
 
     uint8_t* src_plane(const uint8_t* s, int c) const { return const_cast<uint8_t*>(s) + c * plane(); }
-    uint32_t* list_ptr(int eye, int which) const { return lists + (3 * eye + which) * npix(); }
+    uint32_t* list_ptr(int eye, int which) const {
+        (void)which;
+        return lists + eye * npix();
+    }
 
     void ensure_stage() {
         if (stage_arena) return;
@@ -377,8 +385,8 @@ struct Pipeline::Impl {
                 ie[e].mask_pitch = mwords;
                 ie[e].list = list_ptr(e, 0);
                 ie[e].count = counts + e;
-                ie[e].list2 = list_ptr(e, 1);
-                ie[e].repair = list_ptr(e, 2);
+                ie[e].list2 = nullptr;
+                ie[e].repair = reinterpret_cast<uint32_t*>(ipa);
             }
             CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st));
         }
@@ -826,8 +834,8 @@ ImageRGB8 inpaint(const ImageRGB8& frame, const DamageMask& mask, const Conversi
         ie[e].mask_pitch = p->pitch;
         ie[e].list = p->list_ptr(e, 0);
         ie[e].count = p->counts + e;
-        ie[e].list2 = p->list_ptr(e, 1);
-        ie[e].repair = p->list_ptr(e, 2);
+        ie[e].list2 = nullptr;
+        ie[e].repair = reinterpret_cast<uint32_t*>(p->ipa);
     }
     CK(cu::inpaint(ie[0], ie[1], p->gm, static_cast<uint32_t>(p->npix()), p->ctl, p->stats, st));
     ImageRGB8 out(frame.width, frame.height, false);

@@ -57,10 +57,27 @@ __device__ __forceinline__ void append_list(uint32_t* list, uint32_t* count, uns
     }
 }
 
-// Shared-memory phases use a lane-interleaved mapping (lane l of a warp handles pixel
-// base + l), so row-buffer accesses are consecutive bytes / words across a warp and
-// conflict-free; the damage mask of 32 consecutive pixels is one __ballot_sync word.
-// HBM traffic stays 16-byte vectorised through the staging buffers.
+// Exact integer <-> double helpers on the FP64 pipe (no XU conversions):
+//   xd(x)      = (2^52 + x) - 2^52, exact for 0 <= x < 2^31;
+//   col(v)     = trunc(v) for v in (-1, w): (-1, 0) -> 0 as the reference's (int) cast,
+//                else floor(v) = low word of (v + 2^52) rounded toward zero.
+__device__ __forceinline__ double exact_xd(int x) {
+    return __dsub_rn(__hiloint2double(0x43300000, x), 4503599627370496.0);
+}
+// Returns the truncated column if it lies in [0, w), else -1.
+__device__ __forceinline__ int trunc_col(double v, int w) {
+    if (!(v > -1.0) || !(v < static_cast<double>(w))) return -1;
+    if (v < 0.0) return 0;
+    return __double2loint(__dadd_rz(v, 4503599627370496.0));
+}
+
+// ROUTE 0: anaglyph fused (left R, right G/B only, bit masks + lists).
+// ROUTE 1: general (any planes of either eye, byte or bit masks, optional lists).
+// Shared memory: the source row (R, G, B, depth) and two key rows, 12 bytes per pixel.
+// Phases use a lane-interleaved mapping (lane l handles pixel base + l): shared-memory
+// accesses are consecutive across the warp, a warp's 32 output bytes per plane are one
+// 32-byte sector store, and 32 pixels' damage flags are one __ballot_sync word.
+template <int ROUTE>
 __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
                                               const uint8_t* __restrict__ G,
                                               const uint8_t* __restrict__ B,
@@ -72,22 +89,19 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
     const int y = blockIdx.x;
     const int wpad = (w + 15) & ~15;
     const int nvec = wpad >> 4;
-    uint8_t* s_src = smem;                  // [4][wpad]: R, G, B, depth
-    uint8_t* s_out = smem + 4 * wpad;       // [6][wpad]: left R,G,B, right R,G,B
-    uint8_t* s_msk = smem + 10 * wpad;      // [2][wpad]: byte masks (stage API only)
-    uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 12 * wpad);
+    uint8_t* s_src = smem;  // [4][wpad]: R, G, B, depth
+    uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 4 * wpad);
     uint32_t* keyR = keyL + wpad;
     const int tid = threadIdx.x, lane = tid & 31;
-    const bool bytes_mask = L.mask_bytes || Rt.mask_bytes;
 
     for (int i = tid; i < 256; i += blockDim.x) s_shift[i] = shift_g[i];
     const size_t row = static_cast<size_t>(y) * pitch;
     const uint8_t* planes_in[4] = {R + row, G + row, B + row, D + row};
-    for (int c = tid; c < 4 * nvec; c += blockDim.x) {
-        const int pl = c / nvec, v = c - pl * nvec;
-        reinterpret_cast<uint4*>(s_src + pl * wpad)[v] =
-            __ldg(reinterpret_cast<const uint4*>(planes_in[pl]) + v);
-    }
+#pragma unroll
+    for (int pl = 0; pl < 4; ++pl)
+        for (int v = tid; v < nvec; v += blockDim.x)
+            reinterpret_cast<uint4*>(s_src + pl * wpad)[v] =
+                __ldg(reinterpret_cast<const uint4*>(planes_in[pl]) + v);
     if (!backward) {
         const uint4 z = make_uint4(0, 0, 0, 0);
         for (int c = tid; c < 2 * wpad / 4; c += blockDim.x) reinterpret_cast<uint4*>(keyL)[c] = z;
@@ -99,39 +113,36 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
     const uint8_t* s_d = s_src + 3 * wpad;
 
     if (!backward) {
-        // Splat in two phases. (1) Every source stores its key with a plain store; where
-        // several sources hit one destination an arbitrary one survives. (2) Every source
-        // whose key did not survive (only at depth discontinuities) re-applies it with
-        // atomicMax, so each slot ends at the maximum key — the same winner as a full
-        // atomicMax splat — at a fraction of the shared-memory atomics.
+        // Splat: a plain store per source, then atomicMax only for the sources whose key did
+        // not survive (depth discontinuities). Every slot ends at max over its sources of
+        // (d+1) << 22 | (0x3FFFFF - x): largest depth, then smallest column (dibr.cpp:88-99).
         for (int x = tid; x < w; x += blockDim.x) {
             const int d = s_d[x];
             const double sigma = s_shift[d];
-            const double xd = static_cast<double>(x);
-            const int a = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
-            const int b = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
+            const double xd = exact_xd(x);
+            const int a = trunc_col(__dadd_rn(xd, sigma), w);  // left eye: trunc(p.right)
+            const int b = trunc_col(__dsub_rn(xd, sigma), w);  // right eye: trunc(p.left)
             const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
-            if (static_cast<unsigned>(a) < static_cast<unsigned>(w)) keyL[a] = key;
-            if (static_cast<unsigned>(b) < static_cast<unsigned>(w)) keyR[b] = key;
+            if (a >= 0) keyL[a] = key;
+            if (b >= 0) keyR[b] = key;
         }
         __syncthreads();
         for (int x = tid; x < w; x += blockDim.x) {
             const int d = s_d[x];
             const double sigma = s_shift[d];
-            const double xd = static_cast<double>(x);
-            const int a = __double2int_rz(__dadd_rn(xd, sigma));
-            const int b = __double2int_rz(__dsub_rn(xd, sigma));
+            const double xd = exact_xd(x);
+            const int a = trunc_col(__dadd_rn(xd, sigma), w);
+            const int b = trunc_col(__dsub_rn(xd, sigma), w);
             const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
-            if (static_cast<unsigned>(a) < static_cast<unsigned>(w) && keyL[a] != key)
-                atomicMax(&keyL[a], key);
-            if (static_cast<unsigned>(b) < static_cast<unsigned>(w) && keyR[b] != key)
-                atomicMax(&keyR[b], key);
+            if (a >= 0 && keyL[a] != key) atomicMax(&keyL[a], key);
+            if (b >= 0 && keyR[b] != key) atomicMax(&keyR[b], key);
         }
         __syncthreads();
     }
 
-    // resolve: lane-interleaved, whole warps iterate together (ballots need all lanes)
     const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
+    const size_t lrow = static_cast<size_t>(y) * L.pitch;
+    const size_t rrow = static_cast<size_t>(y) * Rt.pitch;
     for (int xb = tid - lane; xb < w; xb += blockDim.x) {
         const int x = xb + lane;
         const bool act = x < w;
@@ -139,27 +150,32 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
         if (act) {
             if (backward) {
                 const double sigma = s_shift[s_d[x]];
-                const double xd = static_cast<double>(x);
-                const int xl = __double2int_rz(__dsub_rn(xd, sigma));  // trunc(p.left)
-                const int xr = __double2int_rz(__dadd_rn(xd, sigma));  // trunc(p.right)
-                sl = static_cast<unsigned>(xl) < static_cast<unsigned>(w) ? xl : x;
-                sr = static_cast<unsigned>(xr) < static_cast<unsigned>(w) ? xr : x;
+                const double xd = exact_xd(x);
+                const int xl = trunc_col(__dsub_rn(xd, sigma), w);  // trunc(p.left)
+                const int xr = trunc_col(__dadd_rn(xd, sigma), w);  // trunc(p.right)
+                sl = xl >= 0 ? xl : x;
+                sr = xr >= 0 ? xr : x;
             } else {
                 const unsigned kl = keyL[x], kr = keyR[x];
                 sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
                 sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
             }
-            s_out[x] = sl >= 0 ? s_r[sl] : 0;
-            s_out[wpad + x] = sl >= 0 ? s_g[sl] : 0;
-            s_out[2 * wpad + x] = sl >= 0 ? s_b[sl] : 0;
-            s_out[3 * wpad + x] = sr >= 0 ? s_r[sr] : 0;
-            s_out[4 * wpad + x] = sr >= 0 ? s_g[sr] : 0;
-            s_out[5 * wpad + x] = sr >= 0 ? s_b[sr] : 0;
-            if (bytes_mask) {
-                s_msk[x] = sl < 0;
-                s_msk[wpad + x] = sr < 0;
+            if (ROUTE == 0) {
+                L.plane[0][lrow + x] = sl >= 0 ? s_r[sl] : 0;
+                Rt.plane[1][rrow + x] = sr >= 0 ? s_g[sr] : 0;
+                Rt.plane[2][rrow + x] = sr >= 0 ? s_b[sr] : 0;
+            } else {
+                if (L.plane[0]) L.plane[0][lrow + x] = sl >= 0 ? s_r[sl] : 0;
+                if (L.plane[1]) L.plane[1][lrow + x] = sl >= 0 ? s_g[sl] : 0;
+                if (L.plane[2]) L.plane[2][lrow + x] = sl >= 0 ? s_b[sl] : 0;
+                if (Rt.plane[0]) Rt.plane[0][rrow + x] = sr >= 0 ? s_r[sr] : 0;
+                if (Rt.plane[1]) Rt.plane[1][rrow + x] = sr >= 0 ? s_g[sr] : 0;
+                if (Rt.plane[2]) Rt.plane[2][rrow + x] = sr >= 0 ? s_b[sr] : 0;
+                if (L.mask_bytes) L.mask_bytes[static_cast<size_t>(y) * L.mask_pitch + x] = sl < 0;
+                if (Rt.mask_bytes) Rt.mask_bytes[static_cast<size_t>(y) * Rt.mask_pitch + x] = sr < 0;
             }
         }
+        if (backward) continue;  // uniform: no damage, no masks or lists to write
         const unsigned mL = __ballot_sync(0xFFFFFFFFu, act && sl < 0);
         const unsigned mR = __ballot_sync(0xFFFFFFFFu, act && sr < 0);
         if (lane == 0) {
@@ -177,26 +193,6 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
             if (lane == 0) start = atomicAdd(Rt.count, static_cast<uint32_t>(__popc(mR)));
             start = __shfl_sync(0xFFFFFFFFu, start, 0);
             if ((mR >> lane) & 1u) Rt.list[start + __popc(mR & ((1u << lane) - 1u))] = row_base + x;
-        }
-    }
-    __syncthreads();
-
-    // vectorised stores of the staged rows (only the planes this route needs)
-#pragma unroll
-    for (int pl = 0; pl < 8; ++pl) {
-        uint8_t* base = pl < 3 ? L.plane[pl] : pl < 6 ? Rt.plane[pl - 3] : pl == 6 ? L.mask_bytes : Rt.mask_bytes;
-        if (!base) continue;
-        const int dp = pl < 3 ? L.pitch : pl < 6 ? Rt.pitch : pl == 6 ? L.mask_pitch : Rt.mask_pitch;
-        const uint8_t* srcrow = pl < 6 ? s_out + pl * wpad : s_msk + (pl - 6) * wpad;
-        uint8_t* orow = base + static_cast<size_t>(y) * dp;
-        for (int v = tid; v < nvec; v += blockDim.x) {
-            const int x0 = 16 * v;
-            uint8_t* o = orow + x0;
-            if (x0 + 16 <= w && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
-                *reinterpret_cast<uint4*>(o) = reinterpret_cast<const uint4*>(srcrow)[v];
-            } else {
-                for (int k = 0; k < 16 && x0 + k < w; ++k) o[k] = srcrow[x0 + k];
-            }
         }
     }
 }
@@ -246,17 +242,25 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                  Geom gm, const double* shift, bool backward, EyeOut left, EyeOut right,
                  cudaStream_t st) {
     const int wpad = (gm.w + 15) & ~15;
-    const size_t smem = static_cast<size_t>(wpad) * (backward ? 12 : 20);
+    const size_t smem = static_cast<size_t>(wpad) * (backward ? 4 : 12);
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
-        cudaFuncSetAttribute(k_dibr, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_dibr<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_dibr<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         configured[dev] = true;
     }
     if (smem > 220 * 1024) return cudaErrorInvalidValue;
-    k_dibr<<<gm.h, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, shift, backward ? 1 : 0,
-                                    left, right);
+    // the fused anaglyph route: left R and right G/B only, bit masks, lists
+    const bool ana = left.plane[0] && !left.plane[1] && !left.plane[2] && !right.plane[0] &&
+                     right.plane[1] && right.plane[2] && !left.mask_bytes && !right.mask_bytes;
+    if (ana)
+        k_dibr<0><<<gm.h, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, shift, backward ? 1 : 0,
+                                           left, right);
+    else
+        k_dibr<1><<<gm.h, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, shift, backward ? 1 : 0,
+                                           left, right);
     return cudaGetLastError();
 }
 

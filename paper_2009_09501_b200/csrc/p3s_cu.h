@@ -92,6 +92,8 @@ cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* lis
 
 // Inpaint (inpaint.cpp:29-130) on both eyes at once, in place on the EyeOut planes.
 // Work lists come from dibr(). stats (device, 6 x i64): passes/repaired/fallback per eye.
+// The masks are the INITIAL damage (read-only). `repair` of the left eye points at a
+// device arena of inpaint_scratch_bytes(w, h) (per-pixel state words + tile flags).
 struct InpaintEye {
     uint8_t* plane[3];
     int pitch;
@@ -100,11 +102,12 @@ struct InpaintEye {
     int mask_pitch;
     uint32_t* list;        // in: damaged indices (length *count)
     uint32_t* count;
-    uint32_t* list2;       // scratch, same capacity
-    uint32_t* repair;      // scratch, same capacity
+    uint32_t* list2;       // unused (kept for layout compatibility)
+    uint32_t* repair;      // left eye: inpaint arena
 };
+size_t inpaint_scratch_bytes(int w, int h);
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
-                    uint32_t* scratch /* 64 words, zeroed by the call */, long long* stats,
+                    uint32_t* scratch /* >= 128 words, zeroed by the call */, long long* stats,
                     cudaStream_t st);
 
 // Formats from materialised eyes (stereo_format.cpp:8-73).
