@@ -7,7 +7,10 @@
 // (pipeline.cpp:56-65) and run in the same launch.
 //
 // Temporal blocking. The frame is cut into 32x32 tiles; a round runs kPasses Jacobi passes
-// of one tile inside shared memory over the tile plus a kPasses-pixel halo. Information
+// of one tile inside shared memory (one warp per tile, 8 tiles per CTA) over the tile plus
+// a kPasses-pixel halo. Only damage-mask words and the colours of intact pixels that touch
+// damage are read from HBM; a pass with no local repair and no pending neighbour
+// repair ends the simulation early (fixed point). Information
 // moves one pixel per pass, so after kPasses passes the tile interior equals the global
 // Jacobi state (pixels near the halo edge may be wrong, they are discarded). Only tiles
 // whose interior still holds damage are processed.
@@ -32,9 +35,10 @@ namespace {
 
 constexpr int kT = 32;                 // tile side (interior)
 constexpr int kPasses = 16;            // passes per round = halo width
-constexpr int kE = kT + 2 * kPasses;   // extended side
+constexpr int kE = kT + 2 * kPasses;   // extended side (64: one u64 mask per row)
 constexpr int kEN = kE * kE;
-constexpr int kThreads = 256;
+constexpr int kWarps = 8;              // one tile per warp
+constexpr int kThreads = 32 * kWarps;
 constexpr unsigned long long kRepaired = 1ull << 63;
 
 struct Eye {
@@ -43,65 +47,119 @@ struct Eye {
     uint8_t* flags;             // [2][tiles] round flags
 };
 
-__device__ __forceinline__ bool damaged0(const InpaintEye& e, int x, int y) {
-    if (e.mask_bits) return (__ldg(e.mask_bits + static_cast<size_t>(y) * e.mask_pitch + (x >> 5)) >> (x & 31)) & 1u;
-    return __ldg(e.mask_bytes + static_cast<size_t>(y) * e.mask_pitch + x) != 0;
-}
+struct WarpSmem {
+    uint8_t st[kEN];            // 0 intact, 1 damaged, k+1 repaired at local pass k (valid only
+                                // on damaged pixels and their in-image neighbours)
+    uint8_t col[3][kEN];
+    uint16_t lst[kEN];          // damaged pixels of the extended region
+    unsigned long long dmg[kE]; // initial damage bits per extended row
+    unsigned long long img[kE]; // in-image bits per extended row
+    int rep[kPasses + 1];
+};
 
-// st: 0 intact, 1 damaged, k+1 repaired at local pass k (intact for passes > k), 255 outside image
-__device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int round, int tiles_x,
-                             uint8_t* st, uint8_t* col, uint16_t* lst, int* s_n, int* s_rep,
-                             int* s_left, uint32_t* counts_slot, uint8_t* next_flags) {
-    const InpaintEye& io = E.io;
-    const int x0 = tx * kT - kPasses, y0 = ty * kT - kPasses;
-    const long long pass0 = static_cast<long long>(round) * kPasses;  // passes before this round
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        *s_n = 0;
-        *s_left = 0;
-    }
-    if (tid < kPasses + 1) s_rep[tid] = 0;
-    __syncthreads();
-    // load the extended region
-    for (int e = tid; e < kEN; e += kThreads) {
-        const int ly = e / kE, lx = e - ly * kE;
-        const int gx = x0 + lx, gy = y0 + ly;
-        uint8_t s = 255;
-        uint8_t c0 = 0, c1 = 0, c2 = 0;
-        if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
-            const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
-            if (!damaged0(io, gx, gy)) {
-                s = 0;
-                if (io.plane[0]) c0 = io.plane[0][o];
-                if (io.plane[1]) c1 = io.plane[1][o];
-                if (io.plane[2]) c2 = io.plane[2][o];
-            } else {
-                const unsigned long long v =
-                    __ldcg(E.state + static_cast<size_t>(gy) * w + gx);
-                if (v & kRepaired) {
-                    const long long g = static_cast<long long>((v >> 24) & 0xFFFFFFFFull);
-                    s = g <= pass0 ? 0 : static_cast<uint8_t>(g - pass0 + 1);
-                    c0 = static_cast<uint8_t>(v);
-                    c1 = static_cast<uint8_t>(v >> 8);
-                    c2 = static_cast<uint8_t>(v >> 16);
-                } else {
-                    s = 1;
-                    const int at = atomicAdd(s_n, 1);
-                    lst[at] = static_cast<uint16_t>(e);
-                }
+// 64 damage bits of row gy starting at column gx0 (may be negative / past the width).
+__device__ __forceinline__ unsigned long long row_bits(const InpaintEye& e, int gx0, int gy, int w,
+                                                       unsigned long long& inimg) {
+    unsigned long long inb = 0, m = 0;
+    for (int j = 0; j < 64; j += 32) {
+        // bits for columns gx0+j .. gx0+j+31
+        unsigned lo = 0, in32 = 0;
+        const int c0 = gx0 + j;
+        if (e.mask_bits) {
+            const int wi = c0 >> 5;  // floor division (c0 may be negative)
+            const int sh = c0 & 31;
+            const int words = (w + 31) >> 5;
+            const uint32_t* rowp = e.mask_bits + static_cast<size_t>(gy) * e.mask_pitch;
+            const unsigned a = (wi >= 0 && wi < words) ? __ldg(rowp + wi) : 0u;
+            const unsigned b = (wi + 1 >= 0 && wi + 1 < words) ? __ldg(rowp + wi + 1) : 0u;
+            lo = sh ? ((a >> sh) | (b << (32 - sh))) : a;
+        } else {
+            for (int k = 0; k < 32; ++k) {
+                const int c = c0 + k;
+                if (c >= 0 && c < w && __ldg(e.mask_bytes + static_cast<size_t>(gy) * e.mask_pitch + c))
+                    lo |= 1u << k;
             }
         }
-        st[e] = s;
-        col[e] = c0;
-        col[kEN + e] = c1;
-        col[2 * kEN + e] = c2;
+        for (int k = 0; k < 32; ++k) {
+            const int c = c0 + k;
+            if (c >= 0 && c < w) in32 |= 1u << k;
+        }
+        lo &= in32;
+        m |= static_cast<unsigned long long>(lo) << j;
+        inb |= static_cast<unsigned long long>(in32) << j;
     }
-    __syncthreads();
-    const int n = *s_n;
+    inimg = inb;
+    return m;
+}
+
+// One warp simulates kPasses Jacobi passes of one tile (+ halo) in its shared memory.
+__device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int round, int tiles_x,
+                             WarpSmem& S, uint32_t* counts_slot, uint8_t* next_flags) {
+    const InpaintEye& io = E.io;
+    const int lane = threadIdx.x & 31;
+    const int x0 = tx * kT - kPasses, y0 = ty * kT - kPasses;
+    const long long pass0 = static_cast<long long>(round) * kPasses;
+
+    // 1. damage / in-image bits per extended row
+    for (int r = lane; r < kE; r += 32) {
+        const int gy = y0 + r;
+        unsigned long long inimg = 0, m = 0;
+        if (gy >= 0 && gy < h) m = row_bits(io, x0, gy, w, inimg);
+        S.dmg[r] = m;
+        S.img[r] = inimg;
+    }
+    if (lane <= kPasses) S.rep[lane] = 0;
+    __syncwarp();
+    // 2. states and colours, only where a damaged pixel can read them: the initially damaged
+    //    pixels and the in-image pixels of their 8-neighbourhood (a one-pixel dilation of the
+    //    damage bits). Nothing else in the region is ever read.
+    int n = 0;
+    int max_future = 0;
+    for (int r = 0; r < kE; ++r) {
+        const unsigned long long m = S.dmg[r];
+        const unsigned long long up = r > 0 ? S.dmg[r - 1] : 0, dn = r + 1 < kE ? S.dmg[r + 1] : 0;
+        const unsigned long long near = m | up | dn;
+        const unsigned long long need = (near | (near << 1) | (near >> 1)) & S.img[r] & ~m;
+        if ((m | need) == 0) continue;  // warp-uniform
+        const int gy = y0 + r;
+        for (int c = lane; c < kE; c += 32) {
+            const int e = r * kE + c;
+            const unsigned long long bit = 1ull << c;
+            bool is_dmg = false;
+            if (need & bit) {
+                const size_t o = static_cast<size_t>(gy) * io.pitch + (x0 + c);
+                S.st[e] = 0;
+                S.col[0][e] = io.plane[0] ? io.plane[0][o] : 0;
+                S.col[1][e] = io.plane[1] ? io.plane[1][o] : 0;
+                S.col[2][e] = io.plane[2] ? io.plane[2][o] : 0;
+            } else if (m & bit) {
+                const unsigned long long v = __ldcg(E.state + static_cast<size_t>(gy) * w + (x0 + c));
+                if (v & kRepaired) {
+                    const long long g = static_cast<long long>((v >> 24) & 0xFFFFFFFFull);
+                    const int sv = g <= pass0 ? 0 : static_cast<int>(g - pass0 + 1);
+                    if (sv > max_future) max_future = sv;
+                    S.st[e] = static_cast<uint8_t>(sv);
+                    S.col[0][e] = static_cast<uint8_t>(v);
+                    S.col[1][e] = static_cast<uint8_t>(v >> 8);
+                    S.col[2][e] = static_cast<uint8_t>(v >> 16);
+                } else {
+                    S.st[e] = 1;
+                    is_dmg = true;
+                }
+            }
+            const unsigned dm = __ballot_sync(0xFFFFFFFFu, is_dmg);
+            if (is_dmg) S.lst[n + __popc(dm & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
+            n += __popc(dm);
+        }
+    }
+    for (int o = 16; o; o >>= 1) max_future = max(max_future, __shfl_xor_sync(0xFFFFFFFFu, max_future, o));
+    __syncwarp();
+    // 3. passes
     for (int k = 1; k <= kPasses; ++k) {
-        for (int i = tid; i < n; i += kThreads) {
-            const int e = lst[i];
-            if (st[e] != 1) continue;
+        int local = 0;
+        for (int i = lane; i < n; i += 32) {
+            const int e = S.lst[i];
+            if (S.st[e] != 1) continue;
             const int ly = e / kE, lx = e - ly * kE;
             unsigned cnt = 0, a0 = 0, a1 = 0, a2 = 0;
 #pragma unroll
@@ -111,65 +169,74 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
                     if (!dx && !dy) continue;
                     const int nx = lx + dx, ny = ly + dy;
                     if (nx < 0 || nx >= kE || ny < 0 || ny >= kE) continue;  // unknown: not intact
+                    const int gx = x0 + nx, gy = y0 + ny;
+                    if (gx < 0 || gx >= w || gy < 0 || gy >= h) continue;  // outside the image
                     const int ne = ny * kE + nx;
-                    const int s = st[ne];
-                    if (s == 0 || (s >= 2 && s != 255 && s <= k)) {  // intact at pass start
+                    const int s = S.st[ne];
+                    if (s == 0 || (s >= 2 && s <= k)) {
                         ++cnt;
-                        a0 += col[ne];
-                        a1 += col[kEN + ne];
-                        a2 += col[2 * kEN + ne];
+                        a0 += S.col[0][ne];
+                        a1 += S.col[1][ne];
+                        a2 += S.col[2][ne];
                     }
                 }
             }
             if (cnt >= 2) {
-                col[e] = static_cast<uint8_t>((2 * a0 + cnt) / (2 * cnt));
-                col[kEN + e] = static_cast<uint8_t>((2 * a1 + cnt) / (2 * cnt));
-                col[2 * kEN + e] = static_cast<uint8_t>((2 * a2 + cnt) / (2 * cnt));
-                st[e] = static_cast<uint8_t>(k + 1);
+                S.col[0][e] = static_cast<uint8_t>((2 * a0 + cnt) / (2 * cnt));
+                S.col[1][e] = static_cast<uint8_t>((2 * a1 + cnt) / (2 * cnt));
+                S.col[2][e] = static_cast<uint8_t>((2 * a2 + cnt) / (2 * cnt));
+                S.st[e] = static_cast<uint8_t>(k + 1);
+                ++local;
                 if (lx >= kPasses && lx < kPasses + kT && ly >= kPasses && ly < kPasses + kT)
-                    atomicAdd(&s_rep[k], 1);
+                    atomicAdd(&S.rep[k], 1);
             }
         }
-        __syncthreads();
+        __syncwarp();
+        const int any = __reduce_add_sync(0xFFFFFFFFu, local);
+        // no repair anywhere in the region and no neighbour-published repair still to come:
+        // the simulated state is a fixed point, later passes cannot change it
+        if (any == 0 && max_future <= k) break;
     }
-    // publish the interior
-    for (int i = tid; i < n; i += kThreads) {
-        const int e = lst[i];
+    __syncwarp();
+    // 4. publish the interior
+    int left = 0;
+    for (int i = lane; i < n; i += 32) {
+        const int e = S.lst[i];
         const int ly = e / kE, lx = e - ly * kE;
         if (lx < kPasses || lx >= kPasses + kT || ly < kPasses || ly >= kPasses + kT) continue;
-        const int gx = x0 + lx, gy = y0 + ly;
-        const int s = st[e];
+        const int s = S.st[e];
         if (s == 1) {
-            atomicAdd(s_left, 1);
+            ++left;
             continue;
         }
+        const int gx = x0 + lx, gy = y0 + ly;
         const unsigned long long g = static_cast<unsigned long long>(pass0 + s - 1);
         const unsigned long long v = kRepaired | (g << 24) |
-                                     (static_cast<unsigned long long>(col[2 * kEN + e]) << 16) |
-                                     (static_cast<unsigned long long>(col[kEN + e]) << 8) | col[e];
+                                     (static_cast<unsigned long long>(S.col[2][e]) << 16) |
+                                     (static_cast<unsigned long long>(S.col[1][e]) << 8) | S.col[0][e];
         E.state[static_cast<size_t>(gy) * w + gx] = v;
         const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
-        if (io.plane[0]) io.plane[0][o] = col[e];
-        if (io.plane[1]) io.plane[1][o] = col[kEN + e];
-        if (io.plane[2]) io.plane[2][o] = col[2 * kEN + e];
+        if (io.plane[0]) io.plane[0][o] = S.col[0][e];
+        if (io.plane[1]) io.plane[1][o] = S.col[1][e];
+        if (io.plane[2]) io.plane[2][o] = S.col[2][e];
     }
-    __syncthreads();
-    if (tid >= 1 && tid <= kPasses && s_rep[tid]) atomicAdd(&counts_slot[tid], static_cast<uint32_t>(s_rep[tid]));
-    if (tid == 0 && *s_left) next_flags[ty * tiles_x + tx] = 1;
-    __syncthreads();
+    left = __reduce_add_sync(0xFFFFFFFFu, left);
+    if (lane >= 1 && lane <= kPasses && S.rep[lane]) atomicAdd(&counts_slot[lane], static_cast<uint32_t>(S.rep[lane]));
+    if (lane == 0 && left) next_flags[ty * tiles_x + tx] = 1;
+    __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads) k_inpaint_tiles(Eye L, Eye R, int w, int h,
-                                                            int tiles_x, int tiles_y,
-                                                            uint32_t* ctl, long long* stats) {
+__global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, int w, int h,
+                                                               int tiles_x, int tiles_y,
+                                                               uint32_t* ctl, long long* stats) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint8_t st[kEN];
-    __shared__ uint8_t col[3 * kEN];
-    __shared__ uint16_t lst[kEN];
-    __shared__ int s_n, s_left, s_rep[kPasses + 1];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
     const int ntiles = tiles_x * tiles_y;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gsize = gridDim.x * blockDim.x;
+    const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * kWarps;
     Eye eyes[2] = {L, R};
 
     // init: state words of damaged pixels = 0, round-0 flags of tiles holding damage
@@ -196,15 +263,15 @@ __global__ void __launch_bounds__(kThreads) k_inpaint_tiles(Eye L, Eye R, int w,
             const int e = gtid / (kPasses + 1), k = gtid % (kPasses + 1);
             ctl[(e * 3 + nslot) * (kPasses + 1) + k] = 0;
         }
-        for (int item = blockIdx.x; item < 2 * ntiles; item += gridDim.x) {
+        for (int item = gwarp; item < 2 * ntiles; item += nwarps) {
             const int e = item / ntiles, t = item - e * ntiles;
             if (done[e]) continue;
             uint8_t* cur = eyes[e].flags + (round & 1) * ntiles;
             uint8_t* nxt = eyes[e].flags + ((round + 1) & 1) * ntiles;
             if (!cur[t]) continue;
-            process_tile(eyes[e], t % tiles_x, t / tiles_x, w, h, round, tiles_x, st, col, lst,
-                         &s_n, s_rep, &s_left, ctl + (e * 3 + slot) * (kPasses + 1), nxt);
-            if (threadIdx.x == 0) cur[t] = 0;
+            process_tile(eyes[e], t % tiles_x, t / tiles_x, w, h, round, tiles_x, S,
+                         ctl + (e * 3 + slot) * (kPasses + 1), nxt);
+            if ((threadIdx.x & 31) == 0) cur[t] = 0;
         }
         grid.sync();
         for (int e = 0; e < 2; ++e) {
@@ -278,21 +345,23 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(arena + 2 * n * 8, 0, 4 * tiles, st);
     if (e != cudaSuccess) return e;
-    static int per_sm_cache[64] = {0};
+    const size_t smem = kWarps * sizeof(WarpSmem);
+    static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
-    int per_sm = dev < 64 ? per_sm_cache[dev] : 0;
-    if (per_sm == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inpaint_tiles, kThreads, 0);
-        if (per_sm < 1) per_sm = 1;
-        if (per_sm > 4) per_sm = 4;
-        if (dev < 64) per_sm_cache[dev] = per_sm;
+    if (dev < 64 && !configured[dev]) {
+        cudaFuncSetAttribute(k_inpaint_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured[dev] = true;
     }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inpaint_tiles, kThreads, smem);
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     const int blocks = per_sm * sm_count();
     int w = gm.w, h = gm.h, tx = tiles_x, ty = tiles_y;
     void* args[] = {&L, &R, &w, &h, &tx, &ty, &scratch, &stats};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_inpaint_tiles), dim3(blocks),
-                                       dim3(kThreads), args, 0, st);
+                                       dim3(kThreads), args, smem, st);
 }
 
 }  // namespace cu
