@@ -110,46 +110,94 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
     }
     if (lane <= kPasses) S.rep[lane] = 0;
     __syncwarp();
-    // 2. states and colours, only where a damaged pixel can read them: the initially damaged
-    //    pixels and the in-image pixels of their 8-neighbourhood (a one-pixel dilation of the
-    //    damage bits). Nothing else in the region is ever read.
-    int n = 0;
+    // 2. Lists built from the bits alone (no memory round trip): lst[0, n) = the initially
+    //    damaged pixels, lst[n, n + nn) = the in-image pixels of their 8-neighbourhood (a
+    //    one-pixel dilation of the damage bits). Nothing else in the region is ever read.
+    int n = 0, nn = 0;
+    {
+        // each lane owns rows lane and lane + 32
+        unsigned long long md[2], mn[2];
+        int cd = 0, cn = 0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int r = lane + 32 * j;
+            const unsigned long long m = S.dmg[r];
+            const unsigned long long up = r > 0 ? S.dmg[r - 1] : 0, dn = r + 1 < kE ? S.dmg[r + 1] : 0;
+            const unsigned long long near = m | up | dn;
+            md[j] = m;
+            mn[j] = (near | (near << 1) | (near >> 1)) & S.img[r] & ~m;
+            cd += __popcll(md[j]);
+            cn += __popcll(mn[j]);
+        }
+        int id = cd, in_ = cn;  // inclusive warp scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a1 = __shfl_up_sync(0xFFFFFFFFu, id, o);
+            const int a2 = __shfl_up_sync(0xFFFFFFFFu, in_, o);
+            if (lane >= o) {
+                id += a1;
+                in_ += a2;
+            }
+        }
+        n = __shfl_sync(0xFFFFFFFFu, id, 31);
+        nn = __shfl_sync(0xFFFFFFFFu, in_, 31);
+        int pd = id - cd, pn = n + in_ - cn;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int r = lane + 32 * j;
+            for (unsigned long long m = md[j]; m; m &= m - 1) S.lst[pd++] = static_cast<uint16_t>(r * kE + __ffsll(m) - 1);
+            for (unsigned long long m = mn[j]; m; m &= m - 1) S.lst[pn++] = static_cast<uint16_t>(r * kE + __ffsll(m) - 1);
+        }
+    }
+    __syncwarp();
+    // 3. loads, batched so each lane has several independent requests in flight
     int max_future = 0;
-    for (int r = 0; r < kE; ++r) {
-        const unsigned long long m = S.dmg[r];
-        const unsigned long long up = r > 0 ? S.dmg[r - 1] : 0, dn = r + 1 < kE ? S.dmg[r + 1] : 0;
-        const unsigned long long near = m | up | dn;
-        const unsigned long long need = (near | (near << 1) | (near >> 1)) & S.img[r] & ~m;
-        if ((m | need) == 0) continue;  // warp-uniform
-        const int gy = y0 + r;
-        for (int c = lane; c < kE; c += 32) {
-            const int e = r * kE + c;
-            const unsigned long long bit = 1ull << c;
-            bool is_dmg = false;
-            if (need & bit) {
-                const size_t o = static_cast<size_t>(gy) * io.pitch + (x0 + c);
-                S.st[e] = 0;
-                S.col[0][e] = io.plane[0] ? io.plane[0][o] : 0;
-                S.col[1][e] = io.plane[1] ? io.plane[1][o] : 0;
-                S.col[2][e] = io.plane[2] ? io.plane[2][o] : 0;
-            } else if (m & bit) {
-                const unsigned long long v = __ldcg(E.state + static_cast<size_t>(gy) * w + (x0 + c));
-                if (v & kRepaired) {
-                    const long long g = static_cast<long long>((v >> 24) & 0xFFFFFFFFull);
+    constexpr int kB = 8;
+    for (int base = 0; base < n + nn; base += 32 * kB) {
+        unsigned long long v[kB];
+        uint8_t c0[kB], c1[kB], c2[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const int i = base + lane + 32 * j;
+            v[j] = 0;
+            c0[j] = c1[j] = c2[j] = 0;
+            if (i < n + nn) {
+                const int e = S.lst[i];
+                const int ly = e / kE, lx = e - ly * kE;
+                const int gx = x0 + lx, gy = y0 + ly;
+                if (i < n) {
+                    v[j] = __ldcg(E.state + static_cast<size_t>(gy) * w + gx);
+                } else {
+                    const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
+                    if (io.plane[0]) c0[j] = io.plane[0][o];
+                    if (io.plane[1]) c1[j] = io.plane[1][o];
+                    if (io.plane[2]) c2[j] = io.plane[2][o];
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const int i = base + lane + 32 * j;
+            if (i >= n + nn) continue;
+            const int e = S.lst[i];
+            if (i < n) {
+                if (v[j] & kRepaired) {
+                    const long long g = static_cast<long long>((v[j] >> 24) & 0xFFFFFFFFull);
                     const int sv = g <= pass0 ? 0 : static_cast<int>(g - pass0 + 1);
                     if (sv > max_future) max_future = sv;
                     S.st[e] = static_cast<uint8_t>(sv);
-                    S.col[0][e] = static_cast<uint8_t>(v);
-                    S.col[1][e] = static_cast<uint8_t>(v >> 8);
-                    S.col[2][e] = static_cast<uint8_t>(v >> 16);
+                    S.col[0][e] = static_cast<uint8_t>(v[j]);
+                    S.col[1][e] = static_cast<uint8_t>(v[j] >> 8);
+                    S.col[2][e] = static_cast<uint8_t>(v[j] >> 16);
                 } else {
                     S.st[e] = 1;
-                    is_dmg = true;
                 }
+            } else {
+                S.st[e] = 0;
+                S.col[0][e] = c0[j];
+                S.col[1][e] = c1[j];
+                S.col[2][e] = c2[j];
             }
-            const unsigned dm = __ballot_sync(0xFFFFFFFFu, is_dmg);
-            if (is_dmg) S.lst[n + __popc(dm & ((1u << lane) - 1u))] = static_cast<uint16_t>(e);
-            n += __popc(dm);
         }
     }
     for (int o = 16; o; o >>= 1) max_future = max(max_future, __shfl_xor_sync(0xFFFFFFFFu, max_future, o));
