@@ -42,6 +42,10 @@ W4K, H4K = 3840, 2160
 RING = 8
 SWEEP = [0, 2, 16, 30, 60, 120, 254, 510]
 L2_BYTES = 126 * 2**20
+# kernels per step on the default route: k_depth_front, k_block_values, k_upsample,
+# k_bilateral_f32, k_bilateral_fixup_warp, k_dibr<0>, k_inpaint_tiles (ncu launch list in
+# profiles/)
+LAUNCHES_PER_STEP = 7
 
 
 def dist_env():
@@ -236,7 +240,10 @@ def main():
     pipe = p3s.Pipeline(W4K, H4K, cfg)
     # frames: distinct per rank (frame-sharded video); seeds follow the reference's
     # video convention seed = 1 + global frame index
-    frames = make_frames(W4K, H4K, RING, 1 + rank * RING)
+    from paper_2009_09501_b200.sharding import frame_seed, shard_frames
+    mine = shard_frames(RING * world, rank, world)  # frame i -> rank i mod world
+    o = __import__("oracle").load("port")
+    frames = [o.synthetic_frame(W4K, H4K, frame_seed(i)) for i in mine]
     ring = [p3s.DeviceBuffer(pipe.frame_bytes) for _ in range(RING)]
     for f, d in zip(frames, ring):
         pipe.upload(f, d.addr)
@@ -291,6 +298,28 @@ def main():
     e2e_fps = e2e_steps * world / e2e_max
     N = W4K * H4K
 
+    # ---- e2e through the streaming video API (pinned host frames, 3 streams) ----
+    vid = p3s.Video(W4K, H4K, cfg, streams=3)
+    src = [p3s.PinnedBuffer(3 * N) for _ in range(RING)]
+    dst = [p3s.PinnedBuffer(3 * N) for _ in range(RING)]
+    for b, f in zip(src, frames):
+        b.array[:] = f.reshape(-1)
+    vid.convert_ptrs([b.ptr for b in src[:4]], [b.ptr for b in dst[:4]])  # warm-up
+    nvid = max(RING, (min(args.steps, 96) // RING) * RING)
+    fptrs = [src[i % RING].ptr for i in range(nvid)]
+    optrs = [dst[i % RING].ptr for i in range(nvid)]
+    barrier(world)
+    t0 = time.perf_counter()
+    vid.convert_ptrs(fptrs, optrs)
+    vs = time.perf_counter() - t0
+    barrier(world)
+    (vs_max,) = allreduce_max([vs], world, use_dist)
+    e2e_stream = {"value": nvid * world / vs_max, "unit": "frames/s",
+                  "h2d_bytes_per_step": 3 * N, "d2h_bytes_per_step": 3 * N, "steps": nvid,
+                  "path": "p3s_video_convert (C ABI), 3 streams, pinned host frames in and "
+                          "anaglyph out; H2D/compute/D2H of neighbouring frames overlap"}
+    del vid
+
     # ---- parallax sweep (configs[1]: "max parallax sweep") ----
     sweep = {}
     if not args.no_sweep:
@@ -323,48 +352,73 @@ def main():
 
     # ---- rooflines ----
     peaks, peaks_src = measured_peaks()
-    fp64 = p3s.fp64_peak()
     per = {k: v / nruns for k, v in stage_sum.items()}
     bil_ns = per["filter_ns"]
-    flops = bilateral_flops(W4K, H4K)
-    achieved_tf = flops / (bil_ns * 1e-9) / 1e12
-    dibr_ns = per["dibr_ns"]
-    k3_bytes = 7 * N  # 4N read (R, G, B, filtered depth) + 3N anaglyph write
-    k3_gbs = k3_bytes / (dibr_ns * 1e-9) / 1e9
-    prof_traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "bilateral_traffic.json")
+    taps = bilateral_flops(W4K, H4K) / 4.0
+    fast = p3s.bilateral_fast_path(cfg)
+    prof = {}
+    prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         with open(prof_path) as f:
-            prof_traffic = json.load(f).get("dram_bytes_per_launch")
+            prof = json.load(f)
+    if fast:
+        smem = p3s.smem_peak()
+        achieved = taps * 4.0 / (bil_ns * 1e-9) / 1e9
+        roof = {"kernel": "k_bilateral_f32 + k_bilateral_fixup_warp (certified FP32 "
+                          "cross-bilateral, exact FP64 recompute of uncertified pixels)",
+                "bound": "smem", "achieved": achieved, "peak": smem / 1e9, "unit": "GB/s",
+                "frac": achieved * 1e9 / smem,
+                "traffic": prof.get("k_bilateral_f32"),
+                "algorithmic": f"one 4-byte range-table lookup per tap: {taps:.4g} taps x 4 B "
+                               f"per launch (SURVEY.md 8d tap count, r=16)",
+                "peak_source": "measured in this run: conflict-free LDS.32 gather bandwidth, "
+                               "all SMs (p3s_gpu_smem_peak)",
+                "note": "HBM is not the bound of this kernel (2N read + N write = "
+                        f"{3 * N / 1e6:.1f} MB per frame); the filter-stage time (both kernels) "
+                        "is the denominator"}
+    else:
+        fp64 = p3s.fp64_peak()
+        achieved = 4.0 * taps / (bil_ns * 1e-9) / 1e12
+        roof = {"kernel": "k_bilateral_r (exact FP64 cross-bilateral)", "bound": "fp64",
+                "achieved": achieved, "peak": fp64 / 1e12, "unit": "TFLOP/s",
+                "frac": achieved * 1e12 / fp64, "traffic": prof.get("k_bilateral_r"),
+                "algorithmic": f"4 FP64 ops/tap x {taps:.4g} taps per launch",
+                "peak_source": "measured in this run: non-FMA DMUL/DADD issue rate "
+                               "(p3s_gpu_fp64_peak)"}
+    hbm = peaks["hbm_gbs"]
+
+    def hbm_line(kernel, nbytes, ns, what):
+        gbs = nbytes / (ns * 1e-9) / 1e9
+        return {"kernel": kernel, "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                "frac": gbs / hbm, "traffic": prof.get(kernel.split(" ")[0]),
+                "algorithmic": what, "peak_source": peaks_src}
 
     line = {
         "metric": "4K stereo frames/sec", "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32+f64",
         "data": "synthetic", "mpix_per_s": fps * N / 1e6,
-        "config": {"workload": "UHD 3840x2160 synthetic_frame -> depth -> exact FP64 bilateral "
-                               "-> forward DIBR -> inpaint -> anaglyph (BASELINE configs[1]), "
-                               "default config, auto base 30",
+        "config": {"workload": "UHD 3840x2160 synthetic_frame -> depth -> cross-bilateral "
+                               "(bit-exact) -> forward DIBR -> inpaint -> anaglyph (BASELINE "
+                               "configs[1]), default config, auto base 30",
                    "width": W4K, "height": H4K, "base": 30, "format": "anaglyph",
                    "l2": f"input ring {RING} frames x {3 * N / 1e6:.1f} MB = "
                          f"{RING * 3 * N / 1e6:.0f} MB > 126 MB L2",
                    "parallelism": f"frame-sharded x{world}, no collectives"},
         "stages_ms": {k: v / 1e6 for k, v in per.items()},
-        "roofline": {"kernel": "k_bilateral_tiled (exact FP64 cross-bilateral)",
-                     "bound": "fp64", "achieved": achieved_tf, "peak": fp64 / 1e12,
-                     "unit": "TFLOP/s", "frac": achieved_tf / (fp64 / 1e12),
-                     "traffic": prof_traffic,
-                     "algorithmic": f"4 FP64 ops/tap x {flops / 4:.4g} taps per launch",
-                     "peak_source": "measured in this run: non-FMA DMUL/DADD issue-rate "
-                                    "microbenchmark (p3s_gpu_fp64_peak)"},
-        "roofline_hbm": {"kernel": "k_dibr (forward DIBR fused with anaglyph)", "bound": "hbm",
-                         "achieved": k3_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": k3_gbs / peaks["hbm_gbs"], "algorithmic": "7N bytes per frame",
-                         "peak_source": peaks_src},
+        "roofline": roof,
+        "roofline_hbm": [
+            hbm_line("k_dibr (forward DIBR fused with anaglyph)", 7 * N, per["dibr_ns"],
+                     "4N read (R,G,B,filtered depth) + 3N anaglyph write per frame"),
+            hbm_line("k_depth_front+k_block_values+k_upsample (depth stage)", 5 * N,
+                     per["depth_gen_ns"], "3N read + N luma write + N depth write per frame"),
+        ],
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 3 * N,
                 "d2h_bytes_per_step": 5 * N, "steps": e2e_steps,
-                "path": "p3s_convert (C ABI) on pinned p3s_image, outputs+depth+filtered D2H"},
-        "gpu_launches": 6 * args.steps,
+                "path": "p3s_convert (C ABI, one synchronous call per frame) on pinned "
+                        "p3s_image; anaglyph + depth + filtered depth D2H"},
+        "e2e_stream": e2e_stream,
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "clocks": clk,
         "sweep_base": sweep,
     }

@@ -158,6 +158,8 @@ _SIGS = {
     "p3s_host_alloc": (vp, [C.c_size_t]),
     "p3s_host_free": (None, [vp]),
     "p3s_gpu_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
+    "p3s_gpu_smem_peak": (C.c_int, [C.POINTER(C.c_double)]),
+    "p3s_gpu_bilateral_path": (C.c_int, [vp, C.POINTER(C.c_int)]),
 }
 
 _lib = None
@@ -544,6 +546,20 @@ def fp64_peak() -> float:
     """Measured non-FMA FP64 issue rate of the current device, ops/s."""
     v = C.c_double()
     _check(lib().p3s_gpu_fp64_peak(C.byref(v)))
+    return v.value
+
+
+def bilateral_fast_path(cfg) -> bool:
+    """True when p3s_convert runs the certified FP32 bilateral (+ exact fix-up) for cfg."""
+    v = C.c_int()
+    _check(lib().p3s_gpu_bilateral_path(cfg.h, C.byref(v)))
+    return bool(v.value)
+
+
+def smem_peak() -> float:
+    """Measured conflict-free shared-memory gather bandwidth of the current device, B/s."""
+    v = C.c_double()
+    _check(lib().p3s_gpu_smem_peak(C.byref(v)))
     return v.value
 
 

@@ -8,6 +8,7 @@
 // errors) map to P3S_ERR_INTERNAL with the CUDA message; there is no CPU fallback.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -746,6 +747,23 @@ p3s_status p3s_gpu_fp64_peak(double* ops_per_s) {
     return guarded([&] {
         p3s::Device::current();
         const cudaError_t e = p3s::cu::fp64_peak(ops_per_s);
+        if (e != cudaSuccess) throw p3s::DeviceError(cudaGetErrorString(e));
+    });
+}
+
+p3s_status p3s_gpu_bilateral_path(const p3s_config* cfg, int* certified_fp32) {
+    NEED(cfg, certified_fp32);
+    return guarded([&] {
+        const int r = static_cast<int>(std::ceil(2.0 * cfg->cfg.sigma_spatial));
+        *certified_fp32 = p3s::cu::bilateral_fast_available(r) ? 1 : 0;
+    });
+}
+
+p3s_status p3s_gpu_smem_peak(double* bytes_per_s) {
+    NEED(bytes_per_s);
+    return guarded([&] {
+        p3s::Device::current();
+        const cudaError_t e = p3s::cu::smem_peak(bytes_per_s);
         if (e != cudaSuccess) throw p3s::DeviceError(cudaGetErrorString(e));
     });
 }

@@ -31,7 +31,60 @@ __global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters, doubl
     for (int k = 0; k < 8; ++k) s += x[k];
     if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
+
+// Shared-memory lookup bandwidth: the access pattern of the bilateral's range table
+// (lane l reads word k*32 + l of a 32-way replicated table: one LDS.32 per lane, every
+// lane in its own bank). 16 independent loads per iteration off one base register, each
+// consumed by one FADD, so the LDS pipe — not issue — is the limiter.
+__global__ void __launch_bounds__(512) k_smem_peak(float* out, int iters) {
+    __shared__ float tbl[256 * 32];
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) tbl[i] = 1e-6f * (i & 255);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    float acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+    int base = ((threadIdx.x >> 5) * 7) & 15;
+    for (int i = 0; i < iters; ++i) {
+        const float* t = tbl + base * 32 * 16 + lane;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] += t[k * 32];
+        base = (base + 5) & 15;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += acc[k];
+    if (s == 12345.678f) out[0] = s;
+}
 }  // namespace
+
+cudaError_t smem_peak(double* bytes_per_s) {
+    const int blocks = sm_count() * 4, threads = 512, iters = 2048;
+    float* dummy = nullptr;
+    cudaError_t e = cudaMalloc(&dummy, sizeof(float));
+    if (e != cudaSuccess) return e;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_smem_peak<<<blocks, threads>>>(dummy, iters);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(a);
+        k_smem_peak<<<blocks, threads>>>(dummy, iters);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(dummy);
+    const double bytes = 4.0 * 16.0 * iters * static_cast<double>(blocks) * threads;
+    *bytes_per_s = bytes / (best * 1e-3);
+    return e;
+}
 
 cudaError_t fp64_peak(double* ops_per_s) {
     const int blocks = sm_count() * 8, threads = 256, iters = 4096;

@@ -121,6 +121,8 @@ cudaError_t side_by_side_full(const uint8_t* const* left, const uint8_t* const* 
 int sm_count();
 // Non-FMA FP64 issue-rate microbenchmark (independent DMUL/DADD chains), ops per second.
 cudaError_t fp64_peak(double* ops_per_s);
+// Measured conflict-free shared-memory lookup bandwidth (LDS.32 gathers, all SMs), bytes/s.
+cudaError_t smem_peak(double* bytes_per_s);
 
 }  // namespace cu
 }  // namespace p3s
