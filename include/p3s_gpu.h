@@ -132,10 +132,10 @@ P3S_API void* p3s_host_alloc(size_t bytes); /* pinned pool */
 /* Measured non-FMA FP64 issue rate of the current device (DADD/DMUL ops per second), the
  * roofline denominator of the exact bilateral kernel. */
 P3S_API p3s_status p3s_gpu_fp64_peak(double* ops_per_s);
-/* Measured conflict-free shared-memory lookup bandwidth (bytes/s, all SMs): the roofline
- * denominator of the certified FP32 bilateral, whose per-tap range-table gather is its
- * limiting stream. */
-P3S_API p3s_status p3s_gpu_smem_peak(double* bytes_per_s);
+/* Measured conflict-free shared-memory load bandwidth (bytes/s, all SMs): gather = 0 for
+ * lane-contiguous LDS.32, 1 for data-dependent per-lane gathers from a 32-way replicated
+ * table (the certified FP32 bilateral's range lookups, its limiting stream). */
+P3S_API p3s_status p3s_gpu_smem_peak(double* bytes_per_s, int gather);
 /* Which bilateral kernel p3s_convert uses for this config (no GPU needed): 1 = certified
  * FP32 + exact FP64 fix-up (radius 16), 0 = exact FP64 kernels. */
 P3S_API p3s_status p3s_gpu_bilateral_path(const p3s_config* cfg, int* certified_fp32);

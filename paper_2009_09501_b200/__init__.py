@@ -158,7 +158,7 @@ _SIGS = {
     "p3s_host_alloc": (vp, [C.c_size_t]),
     "p3s_host_free": (None, [vp]),
     "p3s_gpu_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
-    "p3s_gpu_smem_peak": (C.c_int, [C.POINTER(C.c_double)]),
+    "p3s_gpu_smem_peak": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
     "p3s_gpu_bilateral_path": (C.c_int, [vp, C.POINTER(C.c_int)]),
 }
 
@@ -556,10 +556,11 @@ def bilateral_fast_path(cfg) -> bool:
     return bool(v.value)
 
 
-def smem_peak() -> float:
-    """Measured conflict-free shared-memory gather bandwidth of the current device, B/s."""
+def smem_peak(gather: bool = False) -> float:
+    """Measured conflict-free shared-memory load bandwidth of the current device, B/s
+    (gather=True: data-dependent per-lane gathers, the bilateral's lookup pattern)."""
     v = C.c_double()
-    _check(lib().p3s_gpu_smem_peak(C.byref(v)))
+    _check(lib().p3s_gpu_smem_peak(C.byref(v), 1 if gather else 0))
     return v.value
 
 

@@ -759,11 +759,12 @@ p3s_status p3s_gpu_bilateral_path(const p3s_config* cfg, int* certified_fp32) {
     });
 }
 
-p3s_status p3s_gpu_smem_peak(double* bytes_per_s) {
+p3s_status p3s_gpu_smem_peak(double* bytes_per_s, int gather) {
     NEED(bytes_per_s);
     return guarded([&] {
         p3s::Device::current();
-        const cudaError_t e = p3s::cu::smem_peak(bytes_per_s);
+        const cudaError_t e =
+            gather ? p3s::cu::smem_gather_peak(bytes_per_s) : p3s::cu::smem_peak(bytes_per_s);
         if (e != cudaSuccess) throw p3s::DeviceError(cudaGetErrorString(e));
     });
 }

@@ -56,7 +56,65 @@ __global__ void __launch_bounds__(512) k_smem_peak(float* out, int iters) {
     for (int k = 0; k < 16; ++k) s += acc[k];
     if (s == 12345.678f) out[0] = s;
 }
+
+// Same, but the bilateral's exact pattern: each lane gathers a data-dependent entry k of a
+// 32-way replicated 512-entry table (word k*32 + lane: own bank, non-contiguous), with the
+// address formed by one add from the previous value (16 independent chains per thread).
+__global__ void __launch_bounds__(512) k_smem_gather(unsigned* out, int iters) {
+    extern __shared__ unsigned gt[];  // [512][32]
+    for (int i = threadIdx.x; i < 512 * 32; i += blockDim.x) {
+        const int k = i >> 5;
+        gt[i] = static_cast<unsigned>(((k * 37 + 11) & 511) * 128);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(gt)) + lane * 4u;
+    unsigned v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = ((threadIdx.x * 7 + k * 29) & 511) * 128u;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            unsigned r;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(base + v[k]));
+            v[k] = r;
+        }
+    }
+    unsigned s = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s ^= v[k];
+    if (s == 0x12345u) out[0] = s;
+}
 }  // namespace
+
+cudaError_t smem_gather_peak(double* bytes_per_s) {
+    const int blocks = sm_count() * 2, threads = 512, iters = 1024;
+    const size_t smem = 512 * 32 * 4;
+    unsigned* dummy = nullptr;
+    cudaError_t e = cudaMalloc(&dummy, sizeof(unsigned));
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(k_smem_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_smem_gather<<<blocks, threads, smem>>>(dummy, iters);
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(a);
+        k_smem_gather<<<blocks, threads, smem>>>(dummy, iters);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(dummy);
+    *bytes_per_s = 4.0 * 16.0 * iters * static_cast<double>(blocks) * threads / (best * 1e-3);
+    return e;
+}
 
 cudaError_t smem_peak(double* bytes_per_s) {
     const int blocks = sm_count() * 4, threads = 512, iters = 2048;

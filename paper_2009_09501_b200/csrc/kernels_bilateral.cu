@@ -530,6 +530,361 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_f32(
     }
 }
 
+// ---- certified FP32, separable spatial factor (radius 16) ---------------------------------
+// Same certificate idea as k_bilateral_f32, cheaper per tap. The spatial weight factors as
+// s(dx,dy) = sx(dx) * sy(dy) (exp of a sum; host tables, each rounded to float), so inside a
+// window row a tap contributes sx(dx)*R(|gi-gq|) to the weight sum and (sx(dx)*d_q)*R to the
+// value sum: sx(dx) and sx(dx)*d_q depend only on the tap and are shared by the thread's P
+// outputs (one FMUL2 per tap pair), leaving per tap pair and output 2 address adds
+// (LEA.HI), 2 conflict-free LDS.32 range lookups and 2 FFMA2. The row's FP32 sums are
+// scaled by sy(dy) when they are folded into the FP64 totals (float x float is exact in
+// double; the fold is one DFMA).
+//  * tile element (u32): (goff << 16) | depth, goff = guide * 128 (byte offset of the range
+//    row), or 511 * 128 for pixels outside the image: base_i + goff then lands in the zero
+//    tail of the table for every centre guide, so image borders need no clipping code;
+//  * table: entries k = gq - gi + 255 in [0, 510] hold R(|k - 255|) as float, 511..766 are
+//    0; 32 copies, lane l reads copy l (bank l);
+//  * depth u8 -> float without the XU pipe: PRMT builds 0x4B0000dd = 2^23 + d, FADD2 -2^23.
+// Error bound (u = 2^-24, every term >= 0, d exact in float). Weight-sum terms: sx (1
+// rounding), R (1), the product is exact inside the FFMA; value-sum terms: sx (1), R (1),
+// sx*d (1). Accumulation adds <= 16 roundings (FFMA chain), the half-row combine 1, sy 1.
+// So every term of N and D is within gamma_21 (+2^-46 for the double-level table, fold and
+// division roundings) of its exact value, |v~ - v| <= v * 42.0001u, and the reference's own
+// FP64 result is within v * 2200 * 2^-53 of v; underflowed float weights add < 1e-35
+// absolute against D >= 1 (the centre tap's weight is exactly 1). A byte is accepted only
+// when v~ + 0.5 is farther than 44u * v~ + 1e-9 from every integer.
+constexpr int kSepEntries = 767;  // 511 real + 256 zero
+constexpr int kSepOob = 511 * 128;
+
+__device__ __forceinline__ unsigned long long depth_pair(uint32_t a, uint32_t b) {
+    // (2^23 + da, 2^23 + db) as f32x2 bit patterns
+    const uint32_t lo = __byte_perm(a, 0x4B000000u, 0x7650);
+    const uint32_t hi = __byte_perm(b, 0x4B000000u, 0x7650);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+template <int R, int P>
+struct SepParam {
+    unsigned long long sx2[R + 1];  // (float(sx), float(sx)), dx = 0..R
+    double sy[2 * R + 1];            // double(float(sy(dy))), dy + R
+};
+
+// One LDS.32 at a shared-window byte address (base already includes the table's address,
+// so address = base + goff is a single LEA.HI).
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+template <int R, int P, bool ALL>
+__device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t* __restrict__ row,
+                                        int t, const uint32_t (&base)[P], double (&ws)[P],
+                                        double (&vs)[P]) {
+    unsigned long long SW[P], SV[P];
+    {
+        const uint32_t c = row[0];
+        const uint32_t goff = c >> 16;
+        float dc, dummy;
+        unpack2(depth_pair(c, c), dc, dummy);
+        dc -= 8388608.0f;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            SW[i] = 0ull;
+            SV[i] = 0ull;
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const float wc = lds_f32(base[i] + goff);
+            SW[i] = pack2(wc, 0.0f);
+            SV[i] = pack2(__fmul_rn(wc, dc), 0.0f);
+        }
+    }
+    const unsigned long long kBias = pack2(-8388608.0f, -8388608.0f);
+#pragma unroll 4
+    for (int dx = 1; dx <= R; ++dx) {
+        const uint32_t a = row[-dx], b = row[dx];
+        const uint32_t ga = a >> 16, gb = b >> 16;
+        const unsigned long long D2 = fadd2(depth_pair(a, b), kBias);
+        const unsigned long long S2 = sp.sx2[dx];
+        const unsigned long long SD2 = fmul2(S2, D2);  // sx(dx) * d, shared by the P outputs
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const unsigned long long R2 = pack2(lds_f32(base[i] + ga), lds_f32(base[i] + gb));
+            SW[i] = ffma2(S2, R2, SW[i]);
+            SV[i] = ffma2(SD2, R2, SV[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+        float a0, a1, b0, b1;
+        unpack2(SW[i], a0, a1);
+        unpack2(SV[i], b0, b1);
+        const double sy = sp.sy[t - i];
+        ws[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(a0, a1)), ws[i]);
+        vs[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(b0, b1)), vs[i]);
+    }
+}
+
+template <int R, int P, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
+    const __grid_constant__ SepParam<R, P> sp, const uint8_t* __restrict__ depth,
+    const uint8_t* __restrict__ guide, int pitch, int w, int h,
+    const double* __restrict__ range_g, uint8_t* __restrict__ out, uint32_t* __restrict__ list,
+    uint32_t* __restrict__ count, int tiles_x, int ntiles) {
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R;
+    constexpr int SH = TY + 2 * R;
+    extern __shared__ __align__(16) unsigned char smem[];
+    char* tbl = reinterpret_cast<char*>(smem);  // [767][32] floats
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + kSepEntries * kF32Copies * 4);
+
+    for (int i = threadIdx.x; i < kSepEntries * kF32Copies; i += blockDim.x) {
+        const int k = i / kF32Copies;
+        reinterpret_cast<float*>(tbl)[i] = k < 511 ? static_cast<float>(range_g[abs(k - 255)]) : 0.0f;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr double kRel = 44.0 / 16777216.0;
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tx0 = (tile % tiles_x) * kTX;
+        const int ty0 = (tile / tiles_x) * TY;
+        __syncthreads();
+        for (int sy = warp; sy < SH; sy += NW) {
+            const int gy = ty0 - R + sy;
+            const bool yin = gy >= 0 && gy < h;
+            const uint8_t* grow = guide + static_cast<size_t>(yin ? gy : 0) * pitch;
+            const uint8_t* drow = depth + static_cast<size_t>(yin ? gy : 0) * pitch;
+            for (int sx = lane; sx < SW; sx += 32) {
+                const int gx = tx0 - R + sx;
+                uint32_t v = static_cast<uint32_t>(kSepOob) << 16;
+                if (yin && gx >= 0 && gx < w)
+                    v = (static_cast<uint32_t>(grow[gx]) << 23) | drow[gx];
+                s_tile[sy * SW + sx] = v;
+            }
+        }
+        __syncthreads();
+
+        const int x = tx0 + lane;
+        const int yb = ty0 + warp * P;
+        if (yb >= h) continue;
+        const uint32_t* tile_col = s_tile + (warp * P) * SW + lane + R;
+        const uint32_t tbl_s = static_cast<uint32_t>(__cvta_generic_to_shared(tbl));
+        uint32_t base[P];
+        double ws[P], vs[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int gi = static_cast<int>(tile_col[(i + R) * SW] >> 23) & 0xFF;
+            base[i] = tbl_s + static_cast<uint32_t>((255 - gi) * 128 + lane * 4);
+            ws[i] = 0.0;
+            vs[i] = 0.0;
+        }
+        // Every window row of the band is processed: rows outside the image hold the OOB
+        // guide offset (zero weight, exact zeros), so there is no clipping logic. The ramp
+        // rows (only some outputs inside their window) are unrolled with compile-time t, so
+        // their per-output predicates fold away; the bulk rows run all P outputs.
+#pragma unroll
+        for (int t = 0; t < P - 1; ++t) sep_row<R, P, false>(sp, tile_col + t * SW, t, base, ws, vs);
+        for (int t = P - 1; t <= 2 * R; ++t) sep_row<R, P, true>(sp, tile_col + t * SW, t, base, ws, vs);
+#pragma unroll
+        for (int t = 2 * R + 1; t < 2 * R + P; ++t) sep_row<R, P, false>(sp, tile_col + t * SW, t, base, ws, vs);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int y = yb + i;
+            const bool valid = x < w && y < h;
+            bool uncertain = false;
+            if (valid) {
+                const double v = __ddiv_rn(vs[i], ws[i]);
+                const double f = __dadd_rn(v, 0.5);
+                const double r = floor(f);
+                const double dist = fmin(f - r, r + 1.0 - f);
+                const double bound = v * kRel + 1e-9;
+                uncertain = !(dist > bound);
+                out[static_cast<size_t>(y) * pitch + x] =
+                    uncertain ? 0 : (r <= 0.0 ? 0 : (r >= 255.0 ? 255 : static_cast<uint8_t>(static_cast<int>(r))));
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, uncertain);
+            if (m) {
+                uint32_t start = 0;
+                if (lane == 0) start = atomicAdd(count, static_cast<uint32_t>(__popc(m)));
+                start = __shfl_sync(0xFFFFFFFFu, start, 0);
+                if (uncertain)
+                    list[start + __popc(m & ((1u << lane) - 1u))] =
+                        static_cast<uint32_t>(y) * static_cast<uint32_t>(w) + static_cast<uint32_t>(x);
+            }
+        }
+    }
+}
+
+// ---- k_bilateral_sep2: the same arithmetic and certificate as k_bilateral_sep, sized for
+// two resident CTAs per SM (more warps to hide the LDS -> FFMA2 latency). The range table
+// drops the 256-entry zero tail (64 KB: 511 entries + one zero sentinel per copy):
+//  * rows outside the image are skipped with a warp-uniform test (no taps issued);
+//  * columns outside the image only occur in the first/last tile column; those tiles run an
+//    EDGE instance that routes out-of-image taps to the zero sentinel with a select.
+constexpr int kSep2Entries = 512;
+
+template <int R, int P, bool ALL, bool EDGE>
+__device__ __forceinline__ void sep2_row(const SepParam<R, P>& sp, const uint32_t* __restrict__ row,
+                                         int t, int x, int w, uint32_t zaddr,
+                                         const uint32_t (&base)[P], double (&ws)[P],
+                                         double (&vs)[P]) {
+    unsigned long long SW[P], SV[P];
+    {
+        const uint32_t c = row[0];
+        const uint32_t goff = c >> 16;
+        float dc, dummy;
+        unpack2(depth_pair(c, c), dc, dummy);
+        dc -= 8388608.0f;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            SW[i] = 0ull;
+            SV[i] = 0ull;
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const float wc = lds_f32(base[i] + goff);
+            SW[i] = pack2(wc, 0.0f);
+            SV[i] = pack2(__fmul_rn(wc, dc), 0.0f);
+        }
+    }
+    const unsigned long long kBias = pack2(-8388608.0f, -8388608.0f);
+#pragma unroll 4
+    for (int dx = 1; dx <= R; ++dx) {
+        const uint32_t a = row[-dx], b = row[dx];
+        const uint32_t ga = a >> 16, gb = b >> 16;
+        const unsigned long long D2 = fadd2(depth_pair(a, b), kBias);
+        const unsigned long long S2 = sp.sx2[dx];
+        const unsigned long long SD2 = fmul2(S2, D2);
+        const bool oob_l = EDGE && (x - dx < 0);
+        const bool oob_r = EDGE && (x + dx >= w);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+            const uint32_t al = oob_l ? zaddr : base[i] + ga;
+            const uint32_t ar = oob_r ? zaddr : base[i] + gb;
+            const unsigned long long R2 = pack2(lds_f32(al), lds_f32(ar));
+            SW[i] = ffma2(S2, R2, SW[i]);
+            SV[i] = ffma2(SD2, R2, SV[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
+        float a0, a1, b0, b1;
+        unpack2(SW[i], a0, a1);
+        unpack2(SV[i], b0, b1);
+        const double sy = sp.sy[t - i];
+        ws[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(a0, a1)), ws[i]);
+        vs[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(b0, b1)), vs[i]);
+    }
+}
+
+template <int R, int P, bool EDGE>
+__device__ __forceinline__ void sep2_band(const SepParam<R, P>& sp, const uint32_t* tile_col,
+                                          int yb, int h, int x, int w, uint32_t zaddr,
+                                          const uint32_t (&base)[P], double (&ws)[P],
+                                          double (&vs)[P]) {
+    constexpr int SW = kTX + 2 * R;
+    // window row t is image row yb - R + t; rows outside the image are skipped (uniform)
+#pragma unroll
+    for (int t = 0; t < P - 1; ++t)
+        if (static_cast<unsigned>(yb - R + t) < static_cast<unsigned>(h))
+            sep2_row<R, P, false, EDGE>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
+    const int t0 = max(P - 1, R - yb), t1 = min(2 * R, h - 1 - yb + R);
+    for (int t = t0; t <= t1; ++t)
+        sep2_row<R, P, true, EDGE>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
+#pragma unroll
+    for (int t = 2 * R + 1; t < 2 * R + P; ++t)
+        if (static_cast<unsigned>(yb - R + t) < static_cast<unsigned>(h))
+            sep2_row<R, P, false, EDGE>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
+}
+
+template <int R, int P, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_sep2(
+    const __grid_constant__ SepParam<R, P> sp, const uint8_t* __restrict__ depth,
+    const uint8_t* __restrict__ guide, int pitch, int w, int h,
+    const double* __restrict__ range_g, uint8_t* __restrict__ out, uint32_t* __restrict__ list,
+    uint32_t* __restrict__ count, int tiles_x, int ntiles) {
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R;
+    constexpr int SH = TY + 2 * R;
+    extern __shared__ __align__(16) unsigned char smem[];
+    char* tbl = reinterpret_cast<char*>(smem);  // [512][32] floats, entry 511 = 0
+    uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + kSep2Entries * kF32Copies * 4);
+
+    for (int i = threadIdx.x; i < kSep2Entries * kF32Copies; i += blockDim.x) {
+        const int k = i / kF32Copies;
+        reinterpret_cast<float*>(tbl)[i] = k < 511 ? static_cast<float>(range_g[abs(k - 255)]) : 0.0f;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tbl_s = static_cast<uint32_t>(__cvta_generic_to_shared(tbl));
+    const uint32_t zaddr = tbl_s + 511u * 128u + static_cast<uint32_t>(lane) * 4u;
+    constexpr double kRel = 44.0 / 16777216.0;
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int txi = tile % tiles_x;
+        const int tx0 = txi * kTX;
+        const int ty0 = (tile / tiles_x) * TY;
+        __syncthreads();
+        for (int sy = warp; sy < SH; sy += NW) {
+            const int gy = ty0 - R + sy;
+            const bool yin = gy >= 0 && gy < h;
+            const uint8_t* grow = guide + static_cast<size_t>(yin ? gy : 0) * pitch;
+            const uint8_t* drow = depth + static_cast<size_t>(yin ? gy : 0) * pitch;
+            for (int sx = lane; sx < SW; sx += 32) {
+                const int gx = tx0 - R + sx;
+                uint32_t v = 0;
+                if (yin && gx >= 0 && gx < w) v = (static_cast<uint32_t>(grow[gx]) << 23) | drow[gx];
+                s_tile[sy * SW + sx] = v;
+            }
+        }
+        __syncthreads();
+
+        const int x = tx0 + lane;
+        const int yb = ty0 + warp * P;
+        if (yb >= h) continue;
+        const uint32_t* tile_col = s_tile + (warp * P) * SW + lane + R;
+        uint32_t base[P];
+        double ws[P], vs[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int gi = static_cast<int>(tile_col[(i + R) * SW] >> 23) & 0xFF;
+            base[i] = tbl_s + static_cast<uint32_t>((255 - gi) * 128 + lane * 4);
+            ws[i] = 0.0;
+            vs[i] = 0.0;
+        }
+        const bool edge = (tx0 - R < 0) || (tx0 + kTX - 1 + R >= w);
+        if (edge)
+            sep2_band<R, P, true>(sp, tile_col, yb, h, x, w, zaddr, base, ws, vs);
+        else
+            sep2_band<R, P, false>(sp, tile_col, yb, h, x, w, zaddr, base, ws, vs);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const int y = yb + i;
+            const bool valid = x < w && y < h;
+            bool uncertain = false;
+            if (valid) {
+                const double v = __ddiv_rn(vs[i], ws[i]);
+                const double f = __dadd_rn(v, 0.5);
+                const double r = floor(f);
+                const double dist = fmin(f - r, r + 1.0 - f);
+                const double bound = v * kRel + 1e-9;
+                uncertain = !(dist > bound);
+                out[static_cast<size_t>(y) * pitch + x] =
+                    uncertain ? 0 : (r <= 0.0 ? 0 : (r >= 255.0 ? 255 : static_cast<uint8_t>(static_cast<int>(r))));
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, uncertain);
+            if (m) {
+                uint32_t start = 0;
+                if (lane == 0) start = atomicAdd(count, static_cast<uint32_t>(__popc(m)));
+                start = __shfl_sync(0xFFFFFFFFu, start, 0);
+                if (uncertain)
+                    list[start + __popc(m & ((1u << lane) - 1u))] =
+                        static_cast<uint32_t>(y) * static_cast<uint32_t>(w) + static_cast<uint32_t>(x);
+            }
+        }
+    }
+}
+
 // Exact recompute of the uncertified pixels, one thread per pixel, the reference's order.
 __device__ __forceinline__ double bilateral_exact_px(const uint8_t* __restrict__ depth,
                                                      const uint8_t* __restrict__ guide, int pitch,
@@ -827,6 +1182,91 @@ cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
     return cudaGetLastError();
 }
 
+template <int R, int P, int NW>
+cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
+                       const double* spatial_host, const double* spatial_dev, const double* range,
+                       uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
+    SepParam<R, P> sp;
+    // sx(d) = exp(-(d*d) * inv_s): the dy = 0 row of the host spatial table (same formula)
+    const double* row0 = spatial_host + static_cast<size_t>(R) * (R + 1);
+    for (int d = 0; d <= R; ++d) {
+        const float f = static_cast<float>(row0[d]);
+        unsigned u;
+        memcpy(&u, &f, 4);
+        sp.sx2[d] = (static_cast<unsigned long long>(u) << 32) | u;
+    }
+    for (int dy = -R; dy <= R; ++dy) sp.sy[dy + R] = static_cast<double>(static_cast<float>(row0[dy < 0 ? -dy : dy]));
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
+    const size_t smem = kSepEntries * kF32Copies * 4 + static_cast<size_t>(SW) * SH * 4;
+    static int configured_dev[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured_dev[dev]) {
+        cudaFuncSetAttribute(k_bilateral_sep<R, P, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured_dev[dev] = 1;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_sep<R, P, NW>, NW * 32, smem);
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    const int tiles_x = (gm.w + kTX - 1) / kTX;
+    const int tiles_y = (gm.h + TY - 1) / TY;
+    const int ntiles = tiles_x * tiles_y;
+    const int grid = min(ntiles, per_sm * sm_count());
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    k_bilateral_sep<R, P, NW><<<grid, NW * 32, smem, st>>>(
+        sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_bilateral_fixup_warp<R><<<sm_count() * 8, 128, 0, st>>>(
+        depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
+    return cudaGetLastError();
+}
+
+template <int R, int P, int NW, int MINB>
+cudaError_t launch_sep2(const uint8_t* depth, const uint8_t* guide, Geom gm,
+                        const double* spatial_host, const double* spatial_dev, const double* range,
+                        uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
+    SepParam<R, P> sp;
+    const double* row0 = spatial_host + static_cast<size_t>(R) * (R + 1);
+    for (int d = 0; d <= R; ++d) {
+        const float f = static_cast<float>(row0[d]);
+        unsigned u;
+        memcpy(&u, &f, 4);
+        sp.sx2[d] = (static_cast<unsigned long long>(u) << 32) | u;
+    }
+    for (int dy = -R; dy <= R; ++dy) sp.sy[dy + R] = static_cast<double>(static_cast<float>(row0[dy < 0 ? -dy : dy]));
+    constexpr int TY = NW * P;
+    constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
+    const size_t smem = kSep2Entries * kF32Copies * 4 + static_cast<size_t>(SW) * SH * 4;
+    auto kern = k_bilateral_sep2<R, P, NW, MINB>;
+    static int configured_dev[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !configured_dev[dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured_dev[dev] = 1;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    const int tiles_x = (gm.w + kTX - 1) / kTX;
+    const int tiles_y = (gm.h + TY - 1) / TY;
+    const int ntiles = tiles_x * tiles_y;
+    const int grid = min(ntiles, per_sm * sm_count());
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, NW * 32, smem, st>>>(sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list,
+                                      count, tiles_x, ntiles);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_bilateral_fixup_warp<R><<<sm_count() * 8, 128, 0, st>>>(
+        depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
@@ -836,6 +1276,21 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
     const char* v = getenv("P3S_BIL_FAST");
     const int var = v ? atoi(v) : 1;
     if (radius == 16 && var == 1)
+        return launch_sep<16, 8, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out, list,
+                                     count, st);
+    if (radius == 16 && var == 5)
+        return launch_sep2<16, 8, 8, 2>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                        list, count, st);
+    if (radius == 16 && var == 6)
+        return launch_sep2<16, 8, 16, 1>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                         list, count, st);
+    if (radius == 16 && var == 7)
+        return launch_sep2<16, 4, 16, 2>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                         list, count, st);
+    if (radius == 16 && var == 4)
+        return launch_sep<16, 4, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out, list,
+                                     count, st);
+    if (radius == 16 && var == 3)
         return launch_f32<16, 4, 16, 2>(depth, guide, gm, spatial_host, spatial_dev, range, out,
                                         list, count, st);
     if (radius == 16 && var == 2)

@@ -123,6 +123,8 @@ int sm_count();
 cudaError_t fp64_peak(double* ops_per_s);
 // Measured conflict-free shared-memory lookup bandwidth (LDS.32 gathers, all SMs), bytes/s.
 cudaError_t smem_peak(double* bytes_per_s);
+// Same for data-dependent per-lane gathers from a 32-way replicated table (the bilateral's pattern).
+cudaError_t smem_gather_peak(double* bytes_per_s);
 
 }  // namespace cu
 }  // namespace p3s
