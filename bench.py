@@ -362,7 +362,7 @@ def main():
         with open(prof_path) as f:
             prof = json.load(f)
     if fast:
-        smem = p3s.smem_peak()
+        smem = p3s.smem_peak(gather=True)
         achieved = taps * 4.0 / (bil_ns * 1e-9) / 1e9
         roof = {"kernel": "k_bilateral_f32 + k_bilateral_fixup_warp (certified FP32 "
                           "cross-bilateral, exact FP64 recompute of uncertified pixels)",
@@ -371,7 +371,7 @@ def main():
                 "traffic": prof.get("k_bilateral_f32"),
                 "algorithmic": f"one 4-byte range-table lookup per tap: {taps:.4g} taps x 4 B "
                                f"per launch (SURVEY.md 8d tap count, r=16)",
-                "peak_source": "measured in this run: conflict-free LDS.32 gather bandwidth, "
+                "peak_source": "measured in this run: conflict-free data-dependent LDS.32 gathers, "
                                "all SMs (p3s_gpu_smem_peak)",
                 "note": "HBM is not the bound of this kernel (2N read + N write = "
                         f"{3 * N / 1e6:.1f} MB per frame); the filter-stage time (both kernels) "

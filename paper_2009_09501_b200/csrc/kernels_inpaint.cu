@@ -7,22 +7,26 @@
 // (pipeline.cpp:56-65) and run in the same launch.
 //
 // Temporal blocking. The frame is cut into 32x32 tiles; a round runs kPasses Jacobi passes
-// of one tile inside shared memory (one warp per tile, 8 tiles per CTA) over the tile plus
-// a kPasses-pixel halo. Only damage-mask words and the colours of intact pixels that touch
-// damage are read from HBM; a pass with no local repair and no pending neighbour
-// repair ends the simulation early (fixed point). Information
-// moves one pixel per pass, so after kPasses passes the tile interior equals the global
-// Jacobi state (pixels near the halo edge may be wrong, they are discarded). Only tiles
-// whose interior still holds damage are processed.
+// of one tile inside shared memory over the tile plus a kPasses-pixel halo (a 64x64 region,
+// one warp per tile, lane l owning region rows l and l + 32). Information moves one pixel
+// per pass, so after kPasses passes the tile interior equals the global Jacobi state;
+// pixels outside the region are treated as not intact, which can only disturb the
+// discarded halo. A pass that repairs nothing in the region is a fixed point of the
+// simulation, so the remaining passes of the round are skipped.
+//
+// Bit-parallel passes. Damage and in-image flags are 64-bit row words, so the "at least two
+// intact 8-neighbours" decision for a whole row is ~20 word operations; colours are only
+// computed for the pixels a pass repairs (each damaged pixel exactly once), from the
+// pass-start colours of its intact neighbours in shared memory.
 //
 // Cross-tile state is one 64-bit word per initially damaged pixel: 0 = damaged, else
-// (1 << 63) | global pass of repair << 24 | colour bytes — the final truth, written once
-// by the owning tile, read atomically by neighbours. A neighbour that reads a word written
-// in the current round simply knows that pixel's future (it becomes intact after that
-// pass), which is what its own simulation would have derived; a word still 0 is simulated.
-// So one state buffer and ONE grid barrier per round suffice (the old kernel needed two
-// barriers per pass). Per-pass global repair counts (interior pixels only) reproduce the
-// reference's global stall rule and pass statistics exactly.
+// (1 << 63) | global pass of repair << 24 | colour bytes, written once by the owning tile.
+// A tile starting round r takes a neighbour pixel as intact only if its word records a
+// repair at a pass <= the round's first pass; words written during the current round are
+// ignored (the region simulation re-derives them), so the racy reads are harmless and ONE
+// grid barrier per round suffices. Per-pass global repair counts (interior pixels only)
+// reproduce the reference's global stall rule and pass statistics exactly. Tiles are taken
+// from a per-round work list with one atomic per claim (dynamic load balance).
 #include <cooperative_groups.h>
 
 #include "p3s_cu.h"
@@ -35,8 +39,7 @@ namespace {
 
 constexpr int kT = 32;                 // tile side (interior)
 constexpr int kPasses = 16;            // passes per round = halo width
-constexpr int kE = kT + 2 * kPasses;   // extended side (64: one u64 mask per row)
-constexpr int kEN = kE * kE;
+constexpr int kE = kT + 2 * kPasses;   // region side (64: one u64 per row)
 constexpr int kWarps = 8;              // one tile per warp
 constexpr int kThreads = 32 * kWarps;
 constexpr unsigned long long kRepaired = 1ull << 63;
@@ -44,17 +47,19 @@ constexpr unsigned long long kRepaired = 1ull << 63;
 struct Eye {
     InpaintEye io;
     unsigned long long* state;  // per pixel (only initially damaged entries used)
-    uint8_t* flags;             // [2][tiles] round flags
+};
+
+struct Work {
+    uint32_t* init_flags;  // [2][tiles] (dedupe of the initial work list)
+    uint32_t* lists;       // [3][2 * tiles] (eye * tiles + tile)
+    uint32_t* counters;    // [3][2]: count, claim
+    int cap;               // 2 * tiles
 };
 
 struct WarpSmem {
-    uint8_t st[kEN];            // 0 intact, 1 damaged, k+1 repaired at local pass k (valid only
-                                // on damaged pixels and their in-image neighbours)
-    uint8_t col[3][kEN];
-    uint16_t lst[kEN];          // damaged pixels of the extended region
-    unsigned long long dmg[kE]; // initial damage bits per extended row
-    unsigned long long img[kE]; // in-image bits per extended row
-    int rep[kPasses + 1];
+    uint8_t col[3][kE][kE];      // colours (valid on intact pixels next to damage)
+    unsigned long long dmg[kE];  // current damage bits per region row
+    unsigned long long img[kE];  // in-image bits per region row
 };
 
 // 64 damage bits of row gy starting at column gx0 (may be negative / past the width).
@@ -62,7 +67,6 @@ __device__ __forceinline__ unsigned long long row_bits(const InpaintEye& e, int 
                                                        unsigned long long& inimg) {
     unsigned long long inb = 0, m = 0;
     for (int j = 0; j < 64; j += 32) {
-        // bits for columns gx0+j .. gx0+j+31
         unsigned lo = 0, in32 = 0;
         const int c0 = gx0 + j;
         if (e.mask_bits) {
@@ -80,10 +84,9 @@ __device__ __forceinline__ unsigned long long row_bits(const InpaintEye& e, int 
                     lo |= 1u << k;
             }
         }
-        for (int k = 0; k < 32; ++k) {
-            const int c = c0 + k;
-            if (c >= 0 && c < w) in32 |= 1u << k;
-        }
+        const int lo_c = max(0, -c0), hi_c = min(32, w - c0);  // in-image columns [lo_c, hi_c)
+        if (hi_c > lo_c)
+            in32 = (hi_c - lo_c == 32 ? 0xFFFFFFFFu : ((1u << (hi_c - lo_c)) - 1u)) << lo_c;
         lo &= in32;
         m |= static_cast<unsigned long long>(lo) << j;
         inb |= static_cast<unsigned long long>(in32) << j;
@@ -92,189 +95,170 @@ __device__ __forceinline__ unsigned long long row_bits(const InpaintEye& e, int 
     return m;
 }
 
-// One warp simulates kPasses Jacobi passes of one tile (+ halo) in its shared memory.
-__device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int round, int tiles_x,
-                             WarpSmem& S, uint32_t* counts_slot, uint8_t* next_flags) {
+// Loads the 64 colour bytes of region row r (image row gy, columns x0 .. x0+63) of the
+// channels the route needs. x0 is a multiple of 16; aligned planes use 16-byte loads.
+__device__ __forceinline__ void load_row(const InpaintEye& io, WarpSmem& S, int r, int gy, int x0,
+                                         int w) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const uint8_t* pl = io.plane[ch];
+        if (!pl) continue;
+        const uint8_t* src = pl + static_cast<size_t>(gy) * io.pitch;
+        const bool vec = ((reinterpret_cast<uintptr_t>(pl) | static_cast<uintptr_t>(io.pitch)) & 15) == 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = x0 + 16 * q;
+            if (c + 16 <= 0 || c >= w) continue;
+            if (vec && c >= 0 && c + 16 <= io.pitch) {
+                *reinterpret_cast<uint4*>(&S.col[ch][r][16 * q]) = __ldcg(reinterpret_cast<const uint4*>(src + c));
+            } else {
+                for (int k = 0; k < 16; ++k)
+                    if (c + k >= 0 && c + k < w) S.col[ch][r][16 * q + k] = src[c + k];
+            }
+        }
+    }
+}
+
+// Bits of pixels with at least two set bits among their 8 neighbours in (up, mid, dn).
+__device__ __forceinline__ unsigned long long two_plus(unsigned long long up, unsigned long long mid,
+                                                       unsigned long long dn) {
+    const unsigned long long v[8] = {up << 1, up, up >> 1, mid << 1, mid >> 1, dn << 1, dn, dn >> 1};
+    unsigned long long one = 0, two = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        two |= one & v[k];
+        one |= v[k];
+    }
+    return two;
+}
+
+// Repairs the bits `rep` of region row r from the pass-start intact words (iu, im, id).
+__device__ __forceinline__ void repair_row(const InpaintEye& io, WarpSmem& S, int r,
+                                           unsigned long long rep, unsigned long long iu,
+                                           unsigned long long im, unsigned long long id) {
+    while (rep) {
+        const int c = __ffsll(static_cast<long long>(rep)) - 1;
+        rep &= rep - 1;
+        unsigned cnt = 0, a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+            const unsigned long long iw = dy < 0 ? iu : (dy > 0 ? id : im);
+#pragma unroll
+            for (int dx = -1; dx <= 1; ++dx) {
+                if (!dx && !dy) continue;
+                const int cc = c + dx;
+                if (cc < 0 || cc >= kE || !((iw >> cc) & 1ull)) continue;
+                ++cnt;
+                a0 += S.col[0][r + dy][cc];
+                a1 += S.col[1][r + dy][cc];
+                a2 += S.col[2][r + dy][cc];
+            }
+        }
+        if (io.plane[0]) S.col[0][r][c] = static_cast<uint8_t>((2 * a0 + cnt) / (2 * cnt));
+        if (io.plane[1]) S.col[1][r][c] = static_cast<uint8_t>((2 * a1 + cnt) / (2 * cnt));
+        if (io.plane[2]) S.col[2][r][c] = static_cast<uint8_t>((2 * a2 + cnt) / (2 * cnt));
+    }
+}
+
+// One warp simulates up to kPasses Jacobi passes of one tile (+ halo) in shared memory.
+__device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int round, WarpSmem& S,
+                             uint32_t* counts_slot, bool& remains) {
     const InpaintEye& io = E.io;
     const int lane = threadIdx.x & 31;
     const int x0 = tx * kT - kPasses, y0 = ty * kT - kPasses;
     const long long pass0 = static_cast<long long>(round) * kPasses;
+    const unsigned long long kInner = 0x0000FFFFFFFF0000ull;  // interior columns 16..47
 
-    // 1. damage / in-image bits per extended row
-    for (int r = lane; r < kE; r += 32) {
-        const int gy = y0 + r;
-        unsigned long long inimg = 0, m = 0;
-        if (gy >= 0 && gy < h) m = row_bits(io, x0, gy, w, inimg);
+    // 1. damage / in-image words; in later rounds, pixels repaired in earlier rounds
+    //    (state word with pass <= pass0) are intact
+    unsigned long long d[2], img[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int r = lane + 32 * j, gy = y0 + r;
+        unsigned long long in = 0, m = 0;
+        if (gy >= 0 && gy < h) m = row_bits(io, x0, gy, w, in);
+        if (round > 0) {
+            for (unsigned long long b = m; b; b &= b - 1) {
+                const int c = __ffsll(static_cast<long long>(b)) - 1;
+                const unsigned long long v = __ldcg(E.state + static_cast<size_t>(gy) * w + (x0 + c));
+                if ((v & kRepaired) && static_cast<long long>((v >> 24) & 0xFFFFFFFFull) <= pass0)
+                    m &= ~(1ull << c);
+            }
+        }
+        d[j] = m;
+        img[j] = in;
         S.dmg[r] = m;
-        S.img[r] = inimg;
-    }
-    if (lane <= kPasses) S.rep[lane] = 0;
-    __syncwarp();
-    // 2. Lists built from the bits alone (no memory round trip): lst[0, n) = the initially
-    //    damaged pixels, lst[n, n + nn) = the in-image pixels of their 8-neighbourhood (a
-    //    one-pixel dilation of the damage bits). Nothing else in the region is ever read.
-    int n = 0, nn = 0;
-    {
-        // each lane owns rows lane and lane + 32
-        unsigned long long md[2], mn[2];
-        int cd = 0, cn = 0;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int r = lane + 32 * j;
-            const unsigned long long m = S.dmg[r];
-            const unsigned long long up = r > 0 ? S.dmg[r - 1] : 0, dn = r + 1 < kE ? S.dmg[r + 1] : 0;
-            const unsigned long long near = m | up | dn;
-            md[j] = m;
-            mn[j] = (near | (near << 1) | (near >> 1)) & S.img[r] & ~m;
-            cd += __popcll(md[j]);
-            cn += __popcll(mn[j]);
-        }
-        int id = cd, in_ = cn;  // inclusive warp scans
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int a1 = __shfl_up_sync(0xFFFFFFFFu, id, o);
-            const int a2 = __shfl_up_sync(0xFFFFFFFFu, in_, o);
-            if (lane >= o) {
-                id += a1;
-                in_ += a2;
-            }
-        }
-        n = __shfl_sync(0xFFFFFFFFu, id, 31);
-        nn = __shfl_sync(0xFFFFFFFFu, in_, 31);
-        int pd = id - cd, pn = n + in_ - cn;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int r = lane + 32 * j;
-            for (unsigned long long m = md[j]; m; m &= m - 1) S.lst[pd++] = static_cast<uint16_t>(r * kE + __ffsll(m) - 1);
-            for (unsigned long long m = mn[j]; m; m &= m - 1) S.lst[pn++] = static_cast<uint16_t>(r * kE + __ffsll(m) - 1);
-        }
+        S.img[r] = in;
     }
     __syncwarp();
-    // 3. loads, batched so each lane has several independent requests in flight
-    int max_future = 0;
-    constexpr int kB = 8;
-    for (int base = 0; base < n + nn; base += 32 * kB) {
-        unsigned long long v[kB];
-        uint8_t c0[kB], c1[kB], c2[kB];
+    // 2. colours of every row next to damage (intact pixels there feed the means)
 #pragma unroll
-        for (int j = 0; j < kB; ++j) {
-            const int i = base + lane + 32 * j;
-            v[j] = 0;
-            c0[j] = c1[j] = c2[j] = 0;
-            if (i < n + nn) {
-                const int e = S.lst[i];
-                const int ly = e / kE, lx = e - ly * kE;
-                const int gx = x0 + lx, gy = y0 + ly;
-                if (i < n) {
-                    v[j] = __ldcg(E.state + static_cast<size_t>(gy) * w + gx);
-                } else {
-                    const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
-                    if (io.plane[0]) c0[j] = io.plane[0][o];
-                    if (io.plane[1]) c1[j] = io.plane[1][o];
-                    if (io.plane[2]) c2[j] = io.plane[2][o];
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-            const int i = base + lane + 32 * j;
-            if (i >= n + nn) continue;
-            const int e = S.lst[i];
-            if (i < n) {
-                if (v[j] & kRepaired) {
-                    const long long g = static_cast<long long>((v[j] >> 24) & 0xFFFFFFFFull);
-                    const int sv = g <= pass0 ? 0 : static_cast<int>(g - pass0 + 1);
-                    if (sv > max_future) max_future = sv;
-                    S.st[e] = static_cast<uint8_t>(sv);
-                    S.col[0][e] = static_cast<uint8_t>(v[j]);
-                    S.col[1][e] = static_cast<uint8_t>(v[j] >> 8);
-                    S.col[2][e] = static_cast<uint8_t>(v[j] >> 16);
-                } else {
-                    S.st[e] = 1;
-                }
-            } else {
-                S.st[e] = 0;
-                S.col[0][e] = c0[j];
-                S.col[1][e] = c1[j];
-                S.col[2][e] = c2[j];
-            }
-        }
+    for (int j = 0; j < 2; ++j) {
+        const int r = lane + 32 * j, gy = y0 + r;
+        const unsigned long long near = d[j] | (r > 0 ? S.dmg[r - 1] : 0) | (r + 1 < kE ? S.dmg[r + 1] : 0);
+        if (near && gy >= 0 && gy < h) load_row(io, S, r, gy, x0, w);
     }
-    for (int o = 16; o; o >>= 1) max_future = max(max_future, __shfl_xor_sync(0xFFFFFFFFu, max_future, o));
     __syncwarp();
     // 3. passes
     for (int k = 1; k <= kPasses; ++k) {
-        int local = 0;
-        for (int i = lane; i < n; i += 32) {
-            const int e = S.lst[i];
-            if (S.st[e] != 1) continue;
-            const int ly = e / kE, lx = e - ly * kE;
-            unsigned cnt = 0, a0 = 0, a1 = 0, a2 = 0;
+        unsigned long long rep[2], iu[2], im[2], id[2];
+        int inner = 0, any = 0;
 #pragma unroll
-            for (int dy = -1; dy <= 1; ++dy) {
+        for (int j = 0; j < 2; ++j) {
+            const int r = lane + 32 * j;
+            iu[j] = r > 0 ? S.img[r - 1] & ~S.dmg[r - 1] : 0ull;
+            im[j] = img[j] & ~d[j];
+            id[j] = r + 1 < kE ? S.img[r + 1] & ~S.dmg[r + 1] : 0ull;
+            rep[j] = d[j] & two_plus(iu[j], im[j], id[j]);
+            any |= rep[j] != 0;
+            if (r >= kPasses && r < kPasses + kT) inner += __popcll(rep[j] & kInner);
+        }
+        if (!__any_sync(0xFFFFFFFFu, any)) break;  // fixed point of the region
+        // colours (reads pass-start intact neighbours only, so in-place writes are safe)
 #pragma unroll
-                for (int dx = -1; dx <= 1; ++dx) {
-                    if (!dx && !dy) continue;
-                    const int nx = lx + dx, ny = ly + dy;
-                    if (nx < 0 || nx >= kE || ny < 0 || ny >= kE) continue;  // unknown: not intact
-                    const int gx = x0 + nx, gy = y0 + ny;
-                    if (gx < 0 || gx >= w || gy < 0 || gy >= h) continue;  // outside the image
-                    const int ne = ny * kE + nx;
-                    const int s = S.st[ne];
-                    if (s == 0 || (s >= 2 && s <= k)) {
-                        ++cnt;
-                        a0 += S.col[0][ne];
-                        a1 += S.col[1][ne];
-                        a2 += S.col[2][ne];
-                    }
-                }
+        for (int j = 0; j < 2; ++j) repair_row(io, S, lane + 32 * j, rep[j], iu[j], im[j], id[j]);
+        // interior repairs: publish colour + state word; count per pass
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int r = lane + 32 * j;
+            if (r < kPasses || r >= kPasses + kT) continue;
+            const int gy = y0 + r;
+            for (unsigned long long b = rep[j] & kInner; b; b &= b - 1) {
+                const int c = __ffsll(static_cast<long long>(b)) - 1;
+                const int gx = x0 + c;
+                const uint8_t c0 = S.col[0][r][c], c1 = S.col[1][r][c], c2 = S.col[2][r][c];
+                const unsigned long long g = static_cast<unsigned long long>(pass0 + k);
+                E.state[static_cast<size_t>(gy) * w + gx] =
+                    kRepaired | (g << 24) | (static_cast<unsigned long long>(c2) << 16) |
+                    (static_cast<unsigned long long>(c1) << 8) | c0;
+                const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
+                if (io.plane[0]) io.plane[0][o] = c0;
+                if (io.plane[1]) io.plane[1][o] = c1;
+                if (io.plane[2]) io.plane[2][o] = c2;
             }
-            if (cnt >= 2) {
-                S.col[0][e] = static_cast<uint8_t>((2 * a0 + cnt) / (2 * cnt));
-                S.col[1][e] = static_cast<uint8_t>((2 * a1 + cnt) / (2 * cnt));
-                S.col[2][e] = static_cast<uint8_t>((2 * a2 + cnt) / (2 * cnt));
-                S.st[e] = static_cast<uint8_t>(k + 1);
-                ++local;
-                if (lx >= kPasses && lx < kPasses + kT && ly >= kPasses && ly < kPasses + kT)
-                    atomicAdd(&S.rep[k], 1);
-            }
+        }
+        inner = __reduce_add_sync(0xFFFFFFFFu, inner);
+        if (lane == 0 && inner) atomicAdd(&counts_slot[k], static_cast<uint32_t>(inner));
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            d[j] &= ~rep[j];
+            S.dmg[lane + 32 * j] = d[j];
         }
         __syncwarp();
-        const int any = __reduce_add_sync(0xFFFFFFFFu, local);
-        // no repair anywhere in the region and no neighbour-published repair still to come:
-        // the simulated state is a fixed point, later passes cannot change it
-        if (any == 0 && max_future <= k) break;
     }
-    __syncwarp();
-    // 4. publish the interior
+    // 4. interior damage left -> the tile runs again next round
     int left = 0;
-    for (int i = lane; i < n; i += 32) {
-        const int e = S.lst[i];
-        const int ly = e / kE, lx = e - ly * kE;
-        if (lx < kPasses || lx >= kPasses + kT || ly < kPasses || ly >= kPasses + kT) continue;
-        const int s = S.st[e];
-        if (s == 1) {
-            ++left;
-            continue;
-        }
-        const int gx = x0 + lx, gy = y0 + ly;
-        const unsigned long long g = static_cast<unsigned long long>(pass0 + s - 1);
-        const unsigned long long v = kRepaired | (g << 24) |
-                                     (static_cast<unsigned long long>(S.col[2][e]) << 16) |
-                                     (static_cast<unsigned long long>(S.col[1][e]) << 8) | S.col[0][e];
-        E.state[static_cast<size_t>(gy) * w + gx] = v;
-        const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
-        if (io.plane[0]) io.plane[0][o] = S.col[0][e];
-        if (io.plane[1]) io.plane[1][o] = S.col[1][e];
-        if (io.plane[2]) io.plane[2][o] = S.col[2][e];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int r = lane + 32 * j;
+        if (r >= kPasses && r < kPasses + kT) left |= (d[j] & kInner) != 0;
     }
-    left = __reduce_add_sync(0xFFFFFFFFu, left);
-    if (lane >= 1 && lane <= kPasses && S.rep[lane]) atomicAdd(&counts_slot[lane], static_cast<uint32_t>(S.rep[lane]));
-    if (lane == 0 && left) next_flags[ty * tiles_x + tx] = 1;
+    remains = __any_sync(0xFFFFFFFFu, left);
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, int w, int h,
+__global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Work wk, int w, int h,
                                                                int tiles_x, int tiles_y,
                                                                uint32_t* ctl, long long* stats) {
     cg::grid_group grid = cg::this_grid();
@@ -283,11 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, int
     const int ntiles = tiles_x * tiles_y;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gsize = gridDim.x * blockDim.x;
-    const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const int nwarps = gridDim.x * kWarps;
+    const int lane = threadIdx.x & 31;
     Eye eyes[2] = {L, R};
 
-    // init: state words of damaged pixels = 0, round-0 flags of tiles holding damage
+    // init: state words of damaged pixels = 0; tiles holding damage -> work list 0
     uint32_t cnt[2];
     for (int e = 0; e < 2; ++e) {
         cnt[e] = __ldcg(eyes[e].io.count);
@@ -296,7 +279,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, int
             eyes[e].state[idx] = 0ull;
             const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
             const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
-            eyes[e].flags[(y / kT) * tiles_x + x / kT] = 1;
+            const int t = (y / kT) * tiles_x + x / kT;
+            if (atomicExch(&wk.init_flags[e * ntiles + t], 1u) == 0u) {
+                const uint32_t pos = atomicAdd(&wk.counters[0], 1u);
+                wk.lists[pos] = static_cast<uint32_t>(e * ntiles + t);
+            }
         }
     }
     long long remaining[2] = {cnt[0], cnt[1]};
@@ -306,20 +293,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, int
 
     // ctl layout: [eye][slot 0..2][kPasses + 1] pass counts
     for (int round = 0; !(done[0] && done[1]); ++round) {
-        const int slot = round % 3, nslot = (round + 1) % 3;
+        const int slot = round % 3, nslot = (round + 1) % 3, rslot = (round + 2) % 3;
         if (gtid < 2 * (kPasses + 1)) {
             const int e = gtid / (kPasses + 1), k = gtid % (kPasses + 1);
             ctl[(e * 3 + nslot) * (kPasses + 1) + k] = 0;
         }
-        for (int item = gwarp; item < 2 * ntiles; item += nwarps) {
-            const int e = item / ntiles, t = item - e * ntiles;
+        if (gtid == 0) {  // list rslot was last read in round - 1; it is appended to in round + 1
+            wk.counters[2 * rslot] = 0;
+            wk.counters[2 * rslot + 1] = 0;
+        }
+        const uint32_t n = __ldcg(&wk.counters[2 * slot]);
+        const uint32_t* list = wk.lists + static_cast<size_t>(slot) * wk.cap;
+        uint32_t* next = wk.lists + static_cast<size_t>(nslot) * wk.cap;
+        for (;;) {
+            uint32_t i = 0;
+            if (lane == 0) i = atomicAdd(&wk.counters[2 * slot + 1], 1u);
+            i = __shfl_sync(0xFFFFFFFFu, i, 0);
+            if (i >= n) break;
+            const uint32_t item = __ldcg(list + i);
+            const int e = static_cast<int>(item) / ntiles, t = static_cast<int>(item) - e * ntiles;
             if (done[e]) continue;
-            uint8_t* cur = eyes[e].flags + (round & 1) * ntiles;
-            uint8_t* nxt = eyes[e].flags + ((round + 1) & 1) * ntiles;
-            if (!cur[t]) continue;
-            process_tile(eyes[e], t % tiles_x, t / tiles_x, w, h, round, tiles_x, S,
-                         ctl + (e * 3 + slot) * (kPasses + 1), nxt);
-            if ((threadIdx.x & 31) == 0) cur[t] = 0;
+            bool remains = false;
+            process_tile(e ? R : L, t % tiles_x, t / tiles_x, w, h, round, S,
+                         ctl + (e * 3 + slot) * (kPasses + 1), remains);
+            if (remains && lane == 0) {
+                const uint32_t pos = atomicAdd(&wk.counters[2 * nslot], 1u);
+                next[pos] = item;
+            }
         }
         grid.sync();
         for (int e = 0; e < 2; ++e) {
@@ -374,24 +374,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, int
 size_t inpaint_scratch_bytes(int w, int h) {
     const size_t n = static_cast<size_t>(w) * h;
     const size_t tiles = static_cast<size_t>((w + kT - 1) / kT) * ((h + kT - 1) / kT);
-    return 2 * (n * sizeof(unsigned long long) + 2 * tiles) + 256;
+    // state words [2][n] | init flags [2][tiles] | lists [3][2 * tiles] | counters [3][2]
+    return 2 * n * 8 + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 64 + 256;
 }
 
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
                     uint32_t* scratch, long long* stats, cudaStream_t st) {
     (void)capacity;
-    // scratch layout: ctl (2*3*(kPasses+1) u32, zeroed) lives in `scratch` (64+ words);
-    // state words and tile flags in the engine-provided inpaint arena (InpaintEye.repair
-    // of the left eye points at it; see engine.cpp).
+    // scratch: ctl (2*3*(kPasses+1) u32, zeroed here); the per-pixel state words, tile
+    // flags and work lists live in the engine-provided inpaint arena (InpaintEye.repair of
+    // the left eye points at it; see engine.cpp).
     const int tiles_x = (gm.w + kT - 1) / kT, tiles_y = (gm.h + kT - 1) / kT;
     const size_t n = static_cast<size_t>(gm.w) * gm.h;
     const size_t tiles = static_cast<size_t>(tiles_x) * tiles_y;
     unsigned char* arena = reinterpret_cast<unsigned char*>(left.repair);
-    Eye L{left, reinterpret_cast<unsigned long long*>(arena), arena + 2 * n * 8};
-    Eye R{right, reinterpret_cast<unsigned long long*>(arena + n * 8), arena + 2 * n * 8 + 2 * tiles};
+    Eye L{left, reinterpret_cast<unsigned long long*>(arena)};
+    Eye R{right, reinterpret_cast<unsigned long long*>(arena + n * 8)};
+    unsigned char* flags = arena + 2 * n * 8;
+    Work wk;
+    wk.init_flags = reinterpret_cast<uint32_t*>(flags);
+    wk.lists = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4);
+    wk.counters = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4);
+    wk.cap = static_cast<int>(2 * tiles);
     cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * 3 * (kPasses + 1) * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(arena + 2 * n * 8, 0, 4 * tiles, st);
+    e = cudaMemsetAsync(flags, 0, 2 * tiles * 4, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(wk.counters, 0, 6 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     const size_t smem = kWarps * sizeof(WarpSmem);
     static bool configured[64] = {false};
@@ -407,7 +416,7 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     const int blocks = per_sm * sm_count();
     int w = gm.w, h = gm.h, tx = tiles_x, ty = tiles_y;
-    void* args[] = {&L, &R, &w, &h, &tx, &ty, &scratch, &stats};
+    void* args[] = {&L, &R, &wk, &w, &h, &tx, &ty, &scratch, &stats};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_inpaint_tiles), dim3(blocks),
                                        dim3(kThreads), args, smem, st);
 }

@@ -164,3 +164,42 @@ def test_stream_and_plan_invariance(p3s, checker):
     c = p3s.convert(img, p3s.Config(formats=4, base=22))
     assert np.array_equal(a["anaglyph"], b["anaglyph"])
     assert np.array_equal(a["fsbs"], c["fsbs"])
+
+
+def _stress_mask(rng, w, h):
+    kind = int(rng.integers(0, 4))
+    if kind == 0:  # uniform random density (dense -> mid-course stalls + gray fallback)
+        return (rng.random((h, w)) < rng.choice([0.05, 0.3, 0.8, 0.97, 0.995])).astype(np.uint8)
+    m = np.zeros((h, w), np.uint8)
+    if kind == 1:  # wide vertical strips (many passes, multi-round temporal blocking)
+        for _ in range(int(rng.integers(1, 6))):
+            x = int(rng.integers(0, w))
+            m[:, x:x + int(rng.integers(1, 90))] = 1
+    elif kind == 2:  # DIBR-like staircase runs along a slanted edge
+        for y in range(h):
+            x = int((y * rng.uniform(0.2, 3.0)) % max(w, 1))
+            m[y, x:x + int(rng.integers(1, 40))] = 1
+    else:  # blobs + full-height border strip
+        m[:, : int(rng.integers(1, 20))] = 1
+        for _ in range(int(rng.integers(1, 8))):
+            cx, cy, r = int(rng.integers(0, w)), int(rng.integers(0, h)), int(rng.integers(2, 50))
+            yy, xx = np.ogrid[:h, :w]
+            m[(yy - cy) ** 2 + (xx - cx) ** 2 < r * r] = 1
+    return m
+
+
+def test_inpaint_stress_vs_oracle(p3s, checker):
+    """Jacobi inpaint on adversarial masks: wide strips needing many 16-pass rounds, dense
+    random damage that stalls mid-course (gray fallback), thin frames, tile-edge sizes."""
+    import oracle
+    rng = np.random.default_rng(2024)
+    sizes = [(1, 1), (1, 97), (97, 1), (2, 63), (31, 33), (64, 64), (65, 31), (200, 130),
+             (333, 211), (700, 300)]
+    for i in range(30):
+        w, h = sizes[i % len(sizes)]
+        img = rng.integers(0, 256, (3, h, w), dtype=np.uint8)
+        mask = _stress_mask(rng, w, h)
+        a, sa = p3s.inpaint(img, mask, p3s.Config())
+        b, sb = checker.inpaint(img, mask, oracle.Cfg())
+        assert np.array_equal(a, b), (i, w, h, int(mask.sum()))
+        assert tuple(sa) == tuple(sb), (i, w, h, sa, sb)
