@@ -577,7 +577,7 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     return v;
 }
 
-template <int R, int P, bool ALL>
+template <int R, int P, bool ALL, int U>
 __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t* __restrict__ row,
                                         int t, const uint32_t (&base)[P], double (&ws)[P],
                                         double (&vs)[P]) {
@@ -599,7 +599,7 @@ __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t
         }
     }
     const unsigned long long kBias = pack2(-8388608.0f, -8388608.0f);
-#pragma unroll 4
+#pragma unroll U
     for (int dx = 1; dx <= R; ++dx) {
         const uint32_t a = row[-dx], b = row[dx];
         const uint32_t ga = a >> 16, gb = b >> 16;
@@ -626,7 +626,7 @@ __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t
     }
 }
 
-template <int R, int P, int NW>
+template <int R, int P, int NW, int U>
 __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     const __grid_constant__ SepParam<R, P> sp, const uint8_t* __restrict__ depth,
     const uint8_t* __restrict__ guide, int pitch, int w, int h,
@@ -684,10 +684,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
         // rows (only some outputs inside their window) are unrolled with compile-time t, so
         // their per-output predicates fold away; the bulk rows run all P outputs.
 #pragma unroll
-        for (int t = 0; t < P - 1; ++t) sep_row<R, P, false>(sp, tile_col + t * SW, t, base, ws, vs);
-        for (int t = P - 1; t <= 2 * R; ++t) sep_row<R, P, true>(sp, tile_col + t * SW, t, base, ws, vs);
+        for (int t = 0; t < P - 1; ++t) sep_row<R, P, false, U>(sp, tile_col + t * SW, t, base, ws, vs);
+        for (int t = P - 1; t <= 2 * R; ++t) sep_row<R, P, true, U>(sp, tile_col + t * SW, t, base, ws, vs);
 #pragma unroll
-        for (int t = 2 * R + 1; t < 2 * R + P; ++t) sep_row<R, P, false>(sp, tile_col + t * SW, t, base, ws, vs);
+        for (int t = 2 * R + 1; t < 2 * R + P; ++t) sep_row<R, P, false, U>(sp, tile_col + t * SW, t, base, ws, vs);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
             const int y = yb + i;
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
 //    EDGE instance that routes out-of-image taps to the zero sentinel with a select.
 constexpr int kSep2Entries = 512;
 
-template <int R, int P, bool ALL, bool EDGE>
+template <int R, int P, bool ALL, bool EDGE, int U>
 __device__ __forceinline__ void sep2_row(const SepParam<R, P>& sp, const uint32_t* __restrict__ row,
                                          int t, int x, int w, uint32_t zaddr,
                                          const uint32_t (&base)[P], double (&ws)[P],
@@ -747,7 +747,7 @@ __device__ __forceinline__ void sep2_row(const SepParam<R, P>& sp, const uint32_
         }
     }
     const unsigned long long kBias = pack2(-8388608.0f, -8388608.0f);
-#pragma unroll 4
+#pragma unroll U
     for (int dx = 1; dx <= R; ++dx) {
         const uint32_t a = row[-dx], b = row[dx];
         const uint32_t ga = a >> 16, gb = b >> 16;
@@ -778,7 +778,7 @@ __device__ __forceinline__ void sep2_row(const SepParam<R, P>& sp, const uint32_
     }
 }
 
-template <int R, int P, bool EDGE>
+template <int R, int P, bool EDGE, int U>
 __device__ __forceinline__ void sep2_band(const SepParam<R, P>& sp, const uint32_t* tile_col,
                                           int yb, int h, int x, int w, uint32_t zaddr,
                                           const uint32_t (&base)[P], double (&ws)[P],
@@ -788,17 +788,17 @@ __device__ __forceinline__ void sep2_band(const SepParam<R, P>& sp, const uint32
 #pragma unroll
     for (int t = 0; t < P - 1; ++t)
         if (static_cast<unsigned>(yb - R + t) < static_cast<unsigned>(h))
-            sep2_row<R, P, false, EDGE>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
+            sep2_row<R, P, false, EDGE, U>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
     const int t0 = max(P - 1, R - yb), t1 = min(2 * R, h - 1 - yb + R);
     for (int t = t0; t <= t1; ++t)
-        sep2_row<R, P, true, EDGE>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
+        sep2_row<R, P, true, EDGE, U>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
 #pragma unroll
     for (int t = 2 * R + 1; t < 2 * R + P; ++t)
         if (static_cast<unsigned>(yb - R + t) < static_cast<unsigned>(h))
-            sep2_row<R, P, false, EDGE>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
+            sep2_row<R, P, false, EDGE, U>(sp, tile_col + t * SW, t, x, w, zaddr, base, ws, vs);
 }
 
-template <int R, int P, int NW, int MINB>
+template <int R, int P, int NW, int MINB, int U>
 __global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_sep2(
     const __grid_constant__ SepParam<R, P> sp, const uint8_t* __restrict__ depth,
     const uint8_t* __restrict__ guide, int pitch, int w, int h,
@@ -854,9 +854,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_sep2(
         }
         const bool edge = (tx0 - R < 0) || (tx0 + kTX - 1 + R >= w);
         if (edge)
-            sep2_band<R, P, true>(sp, tile_col, yb, h, x, w, zaddr, base, ws, vs);
+            sep2_band<R, P, true, U>(sp, tile_col, yb, h, x, w, zaddr, base, ws, vs);
         else
-            sep2_band<R, P, false>(sp, tile_col, yb, h, x, w, zaddr, base, ws, vs);
+            sep2_band<R, P, false, U>(sp, tile_col, yb, h, x, w, zaddr, base, ws, vs);
 #pragma unroll
         for (int i = 0; i < P; ++i) {
             const int y = yb + i;
@@ -1182,7 +1182,7 @@ cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
     return cudaGetLastError();
 }
 
-template <int R, int P, int NW>
+template <int R, int P, int NW, int U = 4>
 cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
                        const double* spatial_host, const double* spatial_dev, const double* range,
                        uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
@@ -1203,12 +1203,12 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured_dev[dev]) {
-        cudaFuncSetAttribute(k_bilateral_sep<R, P, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_bilateral_sep<R, P, NW, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
         configured_dev[dev] = 1;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_sep<R, P, NW>, NW * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_sep<R, P, NW, U>, NW * 32, smem);
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     const int tiles_x = (gm.w + kTX - 1) / kTX;
     const int tiles_y = (gm.h + TY - 1) / TY;
@@ -1216,7 +1216,7 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
     const int grid = min(ntiles, per_sm * sm_count());
     cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
-    k_bilateral_sep<R, P, NW><<<grid, NW * 32, smem, st>>>(
+    k_bilateral_sep<R, P, NW, U><<<grid, NW * 32, smem, st>>>(
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1225,7 +1225,7 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
     return cudaGetLastError();
 }
 
-template <int R, int P, int NW, int MINB>
+template <int R, int P, int NW, int MINB, int U = 4>
 cudaError_t launch_sep2(const uint8_t* depth, const uint8_t* guide, Geom gm,
                         const double* spatial_host, const double* spatial_dev, const double* range,
                         uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
@@ -1241,7 +1241,7 @@ cudaError_t launch_sep2(const uint8_t* depth, const uint8_t* guide, Geom gm,
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
     const size_t smem = kSep2Entries * kF32Copies * 4 + static_cast<size_t>(SW) * SH * 4;
-    auto kern = k_bilateral_sep2<R, P, NW, MINB>;
+    auto kern = k_bilateral_sep2<R, P, NW, MINB, U>;
     static int configured_dev[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1275,9 +1275,24 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
                            cudaStream_t st) {
     const char* v = getenv("P3S_BIL_FAST");
     const int var = v ? atoi(v) : 1;
-    if (radius == 16 && var == 1)
-        return launch_sep<16, 8, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out, list,
-                                     count, st);
+    if (radius == 16 && (var == 1 || var == 9))  // measured best (4K: 1.55 ms incl. fix-up)
+        return launch_sep<16, 8, 16, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                         list, count, st);
+    if (radius == 16 && var == 12)
+        return launch_sep2<16, 8, 8, 2, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                            list, count, st);
+    if (radius == 16 && var == 13)
+        return launch_sep<16, 12, 8, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                         list, count, st);
+    if (radius == 16 && var == 14)
+        return launch_sep2<16, 4, 16, 2, 16>(depth, guide, gm, spatial_host, spatial_dev, range,
+                                             out, list, count, st);
+    if (radius == 16 && var == 8)
+        return launch_sep<16, 8, 16, 8>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                        list, count, st);
+    if (radius == 16 && var == 10)
+        return launch_sep<16, 8, 16, 2>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                        list, count, st);
     if (radius == 16 && var == 5)
         return launch_sep2<16, 8, 8, 2>(depth, guide, gm, spatial_host, spatial_dev, range, out,
                                         list, count, st);
