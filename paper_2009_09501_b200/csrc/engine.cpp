@@ -10,6 +10,8 @@
 #include <array>
 #include <deque>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <mutex>
@@ -67,6 +69,61 @@ void shift_table(int base, int T, double* out) {
         else
             out[d] = -(hb * (1.0 - d / 255.0));
     }
+}
+
+// Integer form of the reference's destination columns (dibr.cpp:33-41, dibr.hpp:35):
+// for each depth d and direction (P: x + sigma, M: x - sigma) the truncated column
+// trunc(fl(x +- sigma)) over x in [0, w) is x + off + (x >= X), except 0 at x == z (where
+// fl(x +- sigma) lies in (-1, 0)), valid iff in [0, w). (off, X, z) are derived from the
+// exact double evaluation of EVERY x and the representation is verified against it; if
+// any (d, direction) does not fit (or w >= 32768), the function returns false and the plan
+// keeps the FP64 device path. Packed as {off & 0xFFFF | X << 16 (P), (M), zP, zM}.
+bool dibr_col_table(const double* sigma, int w, int (*out)[4]) {
+    if (w >= 32768) return false;
+    auto exact = [w](double v) -> int {  // the reference's column, or INT_MIN if outside
+        if (!(v > -1.0) || !(v < static_cast<double>(w))) return INT32_MIN;
+        return static_cast<int>(v);  // truncation toward zero, (-1, 0) -> 0
+    };
+    for (int d = 0; d < 256; ++d) {
+        int packed[2], zs[2];
+        for (int dir = 0; dir < 2; ++dir) {
+            const double sg = sigma[d];
+            auto eval = [&](int x) {
+                const double xd = x;
+                return exact(dir == 0 ? xd + sg : xd - sg);
+            };
+            const double c = dir == 0 ? sg : -sg;
+            const double fl = std::floor(c);
+            if (fl < -32768.0 || fl > 32767.0) return false;
+            const int off = static_cast<int>(fl);
+            int X = w, z = -1;
+            for (int x = 0; x < w; ++x) {
+                const double xd = x;
+                const double v = dir == 0 ? xd + sg : xd - sg;
+                if (v > -1.0 && v < 0.0) {  // truncates to column 0
+                    if (z < 0) z = x;
+                    continue;
+                }
+                // a rounding-up of x +- sigma shows as floor(v) == x + off + 1 (whether or not
+                // the column is then inside the image)
+                if (v >= 0.0 && X == w && std::floor(v) == static_cast<double>(x + off + 1)) X = x;
+            }
+            for (int x = 0; x < w; ++x) {  // verify the representation everywhere
+                const int e = eval(x);
+                int col = x == z ? 0 : x + off + (x >= X ? 1 : 0);
+                if (col < 0 || col >= w) col = INT32_MIN;
+                if (col != e) return false;
+            }
+            packed[dir] = static_cast<int>((static_cast<unsigned>(off) & 0xFFFFu) |
+                                           (static_cast<unsigned>(X) << 16));
+            zs[dir] = z;
+        }
+        out[d][0] = packed[0];
+        out[d][1] = packed[1];
+        out[d][2] = zs[0];
+        out[d][3] = zs[1];
+    }
+    return true;
 }
 
 // depth.cpp:82-102: centre list and locate(); the running index is monotone in v, so one
@@ -152,6 +209,7 @@ struct Pipeline::Impl {
     unsigned long long* sums = nullptr;
     double* values = nullptr;
     double *range = nullptr, *spatial = nullptr, *shift = nullptr;
+    int4* cols = nullptr;  // integer DIBR column tables (nullptr: FP64 device path)
     uint8_t *ana = nullptr, *hsbs = nullptr, *fsbs = nullptr, *eyes = nullptr;
     uint32_t* mbits = nullptr;
     uint32_t* lists = nullptr;  // [eye][N] damaged pixel lists
@@ -206,6 +264,12 @@ struct Pipeline::Impl {
         double h_range[256], h_shift[256];
         range_table(cfg, h_range);
         shift_table(base, cfg.pop_threshold, h_shift);
+        thread_local int cols_buf[256][4];
+        const char* fp64_env = std::getenv("P3S_DIBR_FP64");
+        const bool int_cols = !(fp64_env && std::atoi(fp64_env)) && dibr_col_table(h_shift, w, cols_buf);
+        if (std::getenv("P3S_DEBUG_PLAN"))
+            std::fprintf(stderr, "[p3s] plan %dx%d base %d: DIBR %s\n", w, h, base,
+                         int_cols ? "integer column tables" : "FP64");
 
         const std::size_t P = plane(), N = npix();
         Arena a;
@@ -218,6 +282,7 @@ struct Pipeline::Impl {
         const std::size_t o_ci0 = a.take<int>(w), o_ci1 = a.take<int>(w), o_cf = a.take<double>(w);
         const std::size_t o_ri0 = a.take<int>(h), o_ri1 = a.take<int>(h), o_rf = a.take<double>(h);
         const std::size_t o_range = a.take<double>(256), o_shift = a.take<double>(256);
+        const std::size_t o_cols = a.take<int4>(256);
         const std::size_t o_spat = a.take<double>(h_spatial.size());
         const std::size_t o_ana = (formats & kFormatAnaglyph) ? a.take<uint8_t>(3 * P) : 0;
         const std::size_t o_hsbs = (formats & kFormatHsbs) ? a.take<uint8_t>(3 * P) : 0;
@@ -242,6 +307,7 @@ struct Pipeline::Impl {
         values = reinterpret_cast<double*>(arena + o_vals);
         range = reinterpret_cast<double*>(arena + o_range);
         shift = reinterpret_cast<double*>(arena + o_shift);
+        if (int_cols) cols = reinterpret_cast<int4*>(arena + o_cols);
         spatial = reinterpret_cast<double*>(arena + o_spat);
         if (formats & kFormatAnaglyph) ana = arena + o_ana;
         if (formats & kFormatHsbs) hsbs = arena + o_hsbs;
@@ -269,6 +335,7 @@ struct Pipeline::Impl {
         up(o_rf, rf.data(), h * sizeof(double));
         up(o_range, h_range, sizeof(h_range));
         up(o_shift, h_shift, sizeof(h_shift));
+        if (int_cols) up(o_cols, cols_buf, sizeof(cols_buf));
         up(o_spat, h_spatial.data(), h_spatial.size() * sizeof(double));
         CK(cudaMemsetAsync(arena + o_stats, 0, 6 * sizeof(long long), stream));
         CK(cudaStreamSynchronize(stream));  // host vectors above go out of scope
@@ -372,7 +439,7 @@ struct Pipeline::Impl {
             eo[e].count = counts + e;
         }
         if (!backward) CK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), st));
-        CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, backward,
+        CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols, backward,
                     eo[0], eo[1], st));
         if (mid) CK(cudaEventRecord(mid, st));
         if (!backward) {
@@ -794,7 +861,7 @@ StereoFrames reconstruct(const ImageRGB8& src, const GrayMap& depth, const Conve
         eo[e].count = p->counts + e;
     }
     CK(cu::dibr(p->src, p->src + p->plane(), p->src + 2 * p->plane(), p->filt, p->gm, p->shift,
-                p->backward, eo[0], eo[1], st));
+                p->cols, p->backward, eo[0], eo[1], st));
     StereoFrames f;
     f.left = ImageRGB8(src.width, src.height, false);
     f.right = ImageRGB8(src.width, src.height, false);

@@ -18,6 +18,8 @@
 // on the host; p.left = x - sigma, p.right = x + sigma are single IEEE adds (__dadd_rn /
 // __dsub_rn, never contracted), truncated toward zero (__double2int_rz), so (-1, 0)
 // maps to column 0 as in dibr.hpp:35.
+#include <cstdlib>
+
 #include "p3s_cu.h"
 
 namespace p3s {
@@ -71,128 +73,277 @@ __device__ __forceinline__ int trunc_col(double v, int w) {
     return __double2loint(__dadd_rz(v, 4503599627370496.0));
 }
 
+// Integer column tables (engine.cpp dibr_col_table): for depth d and direction P (x + sigma)
+// or M (x - sigma), the reference's trunc(fl(x +- sigma)) over x in [0, w) equals
+//     col = x + off + (x >= X),  except col = 0 at x == z  (fl(x +- sigma) in (-1, 0)),
+// valid iff 0 <= col < w. The host derives (off, X, z) from the exact double evaluation of
+// every x and verifies the representation before a plan uses it (else the FP64 path runs).
+// Packed per d as int4 {off & 0xFFFF | X << 16 (P), same (M), zP, zM}.
+__device__ __forceinline__ int col_int(int packed, int z, int x) {
+    const int off = static_cast<int>(static_cast<short>(packed & 0xFFFF));
+    const int X = static_cast<int>(static_cast<unsigned>(packed) >> 16);
+    const int c = x + off + (x >= X ? 1 : 0);
+    return x == z ? 0 : c;
+}
+
 // ROUTE 0: anaglyph fused (left R, right G/B only, bit masks + lists).
 // ROUTE 1: general (any planes of either eye, byte or bit masks, optional lists).
-// Shared memory: the source row (R, G, B, depth) and two key rows, 12 bytes per pixel.
-// Phases use a lane-interleaved mapping (lane l handles pixel base + l): shared-memory
-// accesses are consecutive across the warp, a warp's 32 output bytes per plane are one
-// 32-byte sector store, and 32 pixels' damage flags are one __ballot_sync word.
-template <int ROUTE>
+// INT: integer column tables (int4 per d) instead of FP64 shifts.
+// Persistent CTAs walk the rows; the shift table is staged once per CTA. Shared memory per
+// row: the source row (R, G, B, depth) and two key rows, 12 bytes per pixel. Phases use a
+// lane-interleaved mapping (lane l handles pixel base + l): shared-memory accesses are
+// consecutive across the warp, a warp's 32 output bytes per plane are one 32-byte sector
+// store, and 32 pixels' damage flags are one __ballot_sync word.
+template <int ROUTE, bool INT>
 __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
                                               const uint8_t* __restrict__ G,
                                               const uint8_t* __restrict__ B,
-                                              const uint8_t* __restrict__ D, int pitch, int w,
-                                              const double* __restrict__ shift_g, int backward,
+                                              const uint8_t* __restrict__ D, int pitch, int w, int h,
+                                              const double* __restrict__ shift_g,
+                                              const int4* __restrict__ cols_g, int backward,
                                               EyeOut L, EyeOut Rt) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ double s_shift[256];
-    const int y = blockIdx.x;
+    __shared__ double s_shift[INT ? 1 : 256];
+    __shared__ int4 s_cols[INT ? 256 : 1];
     const int wpad = (w + 15) & ~15;
     const int nvec = wpad >> 4;
     uint8_t* s_src = smem;  // [4][wpad]: R, G, B, depth
     uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 4 * wpad);
     uint32_t* keyR = keyL + wpad;
     const int tid = threadIdx.x, lane = tid & 31;
-
-    for (int i = tid; i < 256; i += blockDim.x) s_shift[i] = shift_g[i];
-    const size_t row = static_cast<size_t>(y) * pitch;
-    const uint8_t* planes_in[4] = {R + row, G + row, B + row, D + row};
-#pragma unroll
-    for (int pl = 0; pl < 4; ++pl)
-        for (int v = tid; v < nvec; v += blockDim.x)
-            reinterpret_cast<uint4*>(s_src + pl * wpad)[v] =
-                __ldg(reinterpret_cast<const uint4*>(planes_in[pl]) + v);
-    if (!backward) {
-        const uint4 z = make_uint4(0, 0, 0, 0);
-        for (int c = tid; c < 2 * wpad / 4; c += blockDim.x) reinterpret_cast<uint4*>(keyL)[c] = z;
-    }
-    __syncthreads();
     const uint8_t* s_r = s_src;
     const uint8_t* s_g = s_src + wpad;
     const uint8_t* s_b = s_src + 2 * wpad;
     const uint8_t* s_d = s_src + 3 * wpad;
 
-    if (!backward) {
-        // Splat: a plain store per source, then atomicMax only for the sources whose key did
-        // not survive (depth discontinuities). Every slot ends at max over its sources of
-        // (d+1) << 22 | (0x3FFFFF - x): largest depth, then smallest column (dibr.cpp:88-99).
-        for (int x = tid; x < w; x += blockDim.x) {
-            const int d = s_d[x];
-            const double sigma = s_shift[d];
-            const double xd = exact_xd(x);
-            const int a = trunc_col(__dadd_rn(xd, sigma), w);  // left eye: trunc(p.right)
-            const int b = trunc_col(__dsub_rn(xd, sigma), w);  // right eye: trunc(p.left)
-            const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
-            if (a >= 0) keyL[a] = key;
-            if (b >= 0) keyR[b] = key;
-        }
-        __syncthreads();
-        for (int x = tid; x < w; x += blockDim.x) {
-            const int d = s_d[x];
-            const double sigma = s_shift[d];
-            const double xd = exact_xd(x);
-            const int a = trunc_col(__dadd_rn(xd, sigma), w);
-            const int b = trunc_col(__dsub_rn(xd, sigma), w);
-            const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
-            if (a >= 0 && keyL[a] != key) atomicMax(&keyL[a], key);
-            if (b >= 0 && keyR[b] != key) atomicMax(&keyR[b], key);
-        }
-        __syncthreads();
+    if (INT) {
+        for (int i = tid; i < 256; i += blockDim.x) s_cols[i] = cols_g[i];
+    } else {
+        for (int i = tid; i < 256; i += blockDim.x) s_shift[i] = shift_g[i];
     }
+    // destination columns of source x: a = trunc(x + sigma) (left eye / backward right),
+    // b = trunc(x - sigma) (right eye / backward left); -1 when outside [0, w)
+    auto cols = [&](int x, int& a, int& b) {
+        const int d = s_d[x];
+        if (INT) {
+            const int4 t = s_cols[d];
+            a = col_int(t.x, t.z, x);
+            b = col_int(t.y, t.w, x);
+            a = static_cast<unsigned>(a) < static_cast<unsigned>(w) ? a : -1;
+            b = static_cast<unsigned>(b) < static_cast<unsigned>(w) ? b : -1;
+        } else {
+            const double sigma = s_shift[d];
+            const double xd = exact_xd(x);
+            a = trunc_col(__dadd_rn(xd, sigma), w);
+            b = trunc_col(__dsub_rn(xd, sigma), w);
+        }
+    };
 
-    const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
-    const size_t lrow = static_cast<size_t>(y) * L.pitch;
-    const size_t rrow = static_cast<size_t>(y) * Rt.pitch;
-    for (int xb = tid - lane; xb < w; xb += blockDim.x) {
-        const int x = xb + lane;
-        const bool act = x < w;
-        int sl = -1, sr = -1;
-        if (act) {
-            if (backward) {
-                const double sigma = s_shift[s_d[x]];
-                const double xd = exact_xd(x);
-                const int xl = trunc_col(__dsub_rn(xd, sigma), w);  // trunc(p.left)
-                const int xr = trunc_col(__dadd_rn(xd, sigma), w);  // trunc(p.right)
-                sl = xl >= 0 ? xl : x;
-                sr = xr >= 0 ? xr : x;
-            } else {
-                const unsigned kl = keyL[x], kr = keyR[x];
-                sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
-                sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
+    for (int y = blockIdx.x; y < h; y += gridDim.x) {
+        __syncthreads();  // previous row's readers are done with shared memory
+        const size_t row = static_cast<size_t>(y) * pitch;
+        const uint8_t* planes_in[4] = {R + row, G + row, B + row, D + row};
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl)
+            for (int v = tid; v < nvec; v += blockDim.x)
+                reinterpret_cast<uint4*>(s_src + pl * wpad)[v] =
+                    __ldg(reinterpret_cast<const uint4*>(planes_in[pl]) + v);
+        if (!backward) {
+            const uint4 z = make_uint4(0, 0, 0, 0);
+            for (int c = tid; c < 2 * wpad / 4; c += blockDim.x) reinterpret_cast<uint4*>(keyL)[c] = z;
+        }
+        __syncthreads();
+
+        if (!backward) {
+            // Splat: a plain store per source, then atomicMax only for the sources whose key
+            // did not survive (depth discontinuities). Every slot ends at max over its sources
+            // of (d+1) << 22 | (0x3FFFFF - x): largest depth, then smallest column
+            // (dibr.cpp:88-99). Left eye splats to trunc(p.right), right eye to trunc(p.left).
+            for (int x = tid; x < w; x += blockDim.x) {
+                int a, b;
+                cols(x, a, b);
+                const unsigned key = (static_cast<unsigned>(s_d[x] + 1) << 22) | (kXMask - x);
+                if (a >= 0) keyL[a] = key;
+                if (b >= 0) keyR[b] = key;
             }
-            if (ROUTE == 0) {
-                L.plane[0][lrow + x] = sl >= 0 ? s_r[sl] : 0;
-                Rt.plane[1][rrow + x] = sr >= 0 ? s_g[sr] : 0;
-                Rt.plane[2][rrow + x] = sr >= 0 ? s_b[sr] : 0;
-            } else {
-                if (L.plane[0]) L.plane[0][lrow + x] = sl >= 0 ? s_r[sl] : 0;
-                if (L.plane[1]) L.plane[1][lrow + x] = sl >= 0 ? s_g[sl] : 0;
-                if (L.plane[2]) L.plane[2][lrow + x] = sl >= 0 ? s_b[sl] : 0;
-                if (Rt.plane[0]) Rt.plane[0][rrow + x] = sr >= 0 ? s_r[sr] : 0;
-                if (Rt.plane[1]) Rt.plane[1][rrow + x] = sr >= 0 ? s_g[sr] : 0;
-                if (Rt.plane[2]) Rt.plane[2][rrow + x] = sr >= 0 ? s_b[sr] : 0;
-                if (L.mask_bytes) L.mask_bytes[static_cast<size_t>(y) * L.mask_pitch + x] = sl < 0;
-                if (Rt.mask_bytes) Rt.mask_bytes[static_cast<size_t>(y) * Rt.mask_pitch + x] = sr < 0;
+            __syncthreads();
+            for (int x = tid; x < w; x += blockDim.x) {
+                int a, b;
+                cols(x, a, b);
+                const unsigned key = (static_cast<unsigned>(s_d[x] + 1) << 22) | (kXMask - x);
+                if (a >= 0 && keyL[a] != key) atomicMax(&keyL[a], key);
+                if (b >= 0 && keyR[b] != key) atomicMax(&keyR[b], key);
+            }
+            __syncthreads();
+        }
+
+        const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
+        const size_t lrow = static_cast<size_t>(y) * L.pitch;
+        const size_t rrow = static_cast<size_t>(y) * Rt.pitch;
+        for (int xb = tid - lane; xb < w; xb += blockDim.x) {
+            const int x = xb + lane;
+            const bool act = x < w;
+            int sl = -1, sr = -1;
+            if (act) {
+                if (backward) {
+                    int a, b;
+                    cols(x, a, b);
+                    sl = b >= 0 ? b : x;  // trunc(p.left)
+                    sr = a >= 0 ? a : x;  // trunc(p.right)
+                } else {
+                    const unsigned kl = keyL[x], kr = keyR[x];
+                    sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
+                    sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
+                }
+                if (ROUTE == 0) {
+                    L.plane[0][lrow + x] = sl >= 0 ? s_r[sl] : 0;
+                    Rt.plane[1][rrow + x] = sr >= 0 ? s_g[sr] : 0;
+                    Rt.plane[2][rrow + x] = sr >= 0 ? s_b[sr] : 0;
+                } else {
+                    if (L.plane[0]) L.plane[0][lrow + x] = sl >= 0 ? s_r[sl] : 0;
+                    if (L.plane[1]) L.plane[1][lrow + x] = sl >= 0 ? s_g[sl] : 0;
+                    if (L.plane[2]) L.plane[2][lrow + x] = sl >= 0 ? s_b[sl] : 0;
+                    if (Rt.plane[0]) Rt.plane[0][rrow + x] = sr >= 0 ? s_r[sr] : 0;
+                    if (Rt.plane[1]) Rt.plane[1][rrow + x] = sr >= 0 ? s_g[sr] : 0;
+                    if (Rt.plane[2]) Rt.plane[2][rrow + x] = sr >= 0 ? s_b[sr] : 0;
+                    if (L.mask_bytes) L.mask_bytes[static_cast<size_t>(y) * L.mask_pitch + x] = sl < 0;
+                    if (Rt.mask_bytes) Rt.mask_bytes[static_cast<size_t>(y) * Rt.mask_pitch + x] = sr < 0;
+                }
+            }
+            if (backward) continue;  // uniform: no damage, no masks or lists to write
+            const unsigned mL = __ballot_sync(0xFFFFFFFFu, act && sl < 0);
+            const unsigned mR = __ballot_sync(0xFFFFFFFFu, act && sr < 0);
+            if (lane == 0) {
+                if (L.mask_bits) L.mask_bits[static_cast<size_t>(y) * L.mask_pitch + (xb >> 5)] = mL;
+                if (Rt.mask_bits) Rt.mask_bits[static_cast<size_t>(y) * Rt.mask_pitch + (xb >> 5)] = mR;
+            }
+            if (L.list && mL) {
+                uint32_t start = 0;
+                if (lane == 0) start = atomicAdd(L.count, static_cast<uint32_t>(__popc(mL)));
+                start = __shfl_sync(0xFFFFFFFFu, start, 0);
+                if ((mL >> lane) & 1u) L.list[start + __popc(mL & ((1u << lane) - 1u))] = row_base + x;
+            }
+            if (Rt.list && mR) {
+                uint32_t start = 0;
+                if (lane == 0) start = atomicAdd(Rt.count, static_cast<uint32_t>(__popc(mR)));
+                start = __shfl_sync(0xFFFFFFFFu, start, 0);
+                if ((mR >> lane) & 1u) Rt.list[start + __popc(mR & ((1u << lane) - 1u))] = row_base + x;
             }
         }
-        if (backward) continue;  // uniform: no damage, no masks or lists to write
-        const unsigned mL = __ballot_sync(0xFFFFFFFFu, act && sl < 0);
-        const unsigned mR = __ballot_sync(0xFFFFFFFFu, act && sr < 0);
-        if (lane == 0) {
-            if (L.mask_bits) L.mask_bits[static_cast<size_t>(y) * L.mask_pitch + (xb >> 5)] = mL;
-            if (Rt.mask_bits) Rt.mask_bits[static_cast<size_t>(y) * Rt.mask_pitch + (xb >> 5)] = mR;
+    }
+}
+
+// Fused DIBR + anaglyph with integer column tables (the default route). Same semantics as
+// k_dibr<0, true>, organised around shared memory so that every phase is conflict-free and
+// HBM sees only 16-byte accesses:
+//   stage    R, G, B, depth rows in with 16-byte loads; keys zeroed with 16-byte stores;
+//   splat    lane-interleaved sources (lane l -> x = base + l): the destinations of a warp
+//            are consecutive, so the shared atomicMax on the packed key hits distinct banks;
+//            a single atomic pass (the maximum is order-independent);
+//   resolve  lane-interleaved destinations: winner -> gathered bytes into output staging
+//            rows, damage flags by ballot (one mask word and one list atomic per warp);
+//   store    staging rows out with 16-byte stores.
+// Requires 16-byte aligned output planes and pitches (the engine's arena guarantees it);
+// bytes past w inside the pitch are written 0.
+template <bool BACKWARD>
+__global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
+                                                  const uint8_t* __restrict__ G,
+                                                  const uint8_t* __restrict__ B,
+                                                  const uint8_t* __restrict__ D, int pitch, int w,
+                                                  int h, const int4* __restrict__ cols_g, EyeOut L,
+                                                  EyeOut Rt) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int4 s_cols[256];
+    const int wpad = (w + 15) & ~15;
+    const int nvec = wpad >> 4;
+    uint8_t* s_r = smem;
+    uint8_t* s_g = smem + wpad;
+    uint8_t* s_b = smem + 2 * wpad;
+    uint8_t* s_d = smem + 3 * wpad;
+    uint8_t* o_r = smem + 4 * wpad;
+    uint8_t* o_g = smem + 5 * wpad;
+    uint8_t* o_b = smem + 6 * wpad;
+    uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 7 * wpad + (16 - (7 * wpad) % 16) % 16);
+    uint32_t* keyR = keyL + wpad;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < 256; i += blockDim.x) s_cols[i] = cols_g[i];
+
+    for (int y = blockIdx.x; y < h; y += gridDim.x) {
+        __syncthreads();
+        const size_t row = static_cast<size_t>(y) * pitch;
+        for (int v = tid; v < nvec; v += blockDim.x) {
+            reinterpret_cast<uint4*>(s_r)[v] = __ldg(reinterpret_cast<const uint4*>(R + row) + v);
+            reinterpret_cast<uint4*>(s_g)[v] = __ldg(reinterpret_cast<const uint4*>(G + row) + v);
+            reinterpret_cast<uint4*>(s_b)[v] = __ldg(reinterpret_cast<const uint4*>(B + row) + v);
+            reinterpret_cast<uint4*>(s_d)[v] = __ldg(reinterpret_cast<const uint4*>(D + row) + v);
         }
-        if (L.list && mL) {
-            uint32_t start = 0;
-            if (lane == 0) start = atomicAdd(L.count, static_cast<uint32_t>(__popc(mL)));
-            start = __shfl_sync(0xFFFFFFFFu, start, 0);
-            if ((mL >> lane) & 1u) L.list[start + __popc(mL & ((1u << lane) - 1u))] = row_base + x;
+        if (!BACKWARD) {
+            const uint4 z = make_uint4(0, 0, 0, 0);
+            for (int v = tid; v < 2 * wpad / 4; v += blockDim.x) reinterpret_cast<uint4*>(keyL)[v] = z;
         }
-        if (Rt.list && mR) {
-            uint32_t start = 0;
-            if (lane == 0) start = atomicAdd(Rt.count, static_cast<uint32_t>(__popc(mR)));
-            start = __shfl_sync(0xFFFFFFFFu, start, 0);
-            if ((mR >> lane) & 1u) Rt.list[start + __popc(mR & ((1u << lane) - 1u))] = row_base + x;
+        __syncthreads();
+        if (!BACKWARD) {
+            for (int x = tid; x < w; x += blockDim.x) {
+                const int d = s_d[x];
+                const int4 t = s_cols[d];
+                const int a = col_int(t.x, t.z, x), b = col_int(t.y, t.w, x);
+                const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
+                if (static_cast<unsigned>(a) < static_cast<unsigned>(w)) atomicMax(&keyL[a], key);
+                if (static_cast<unsigned>(b) < static_cast<unsigned>(w)) atomicMax(&keyR[b], key);
+            }
+            __syncthreads();
+        }
+        const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
+        for (int xb = tid - lane; xb < wpad; xb += blockDim.x) {
+            const int x = xb + lane;
+            const bool act = x < w;
+            int sl = -1, sr = -1;
+            if (act) {
+                if (BACKWARD) {
+                    const int4 t = s_cols[s_d[x]];
+                    const int a = col_int(t.x, t.z, x), b = col_int(t.y, t.w, x);
+                    sl = static_cast<unsigned>(b) < static_cast<unsigned>(w) ? b : x;
+                    sr = static_cast<unsigned>(a) < static_cast<unsigned>(w) ? a : x;
+                } else {
+                    const unsigned kl = keyL[x], kr = keyR[x];
+                    sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
+                    sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
+                }
+            }
+            if (x < wpad) {  // (the last warp of a row may run past the padded width)
+                o_r[x] = sl >= 0 ? s_r[sl] : 0;
+                o_g[x] = sr >= 0 ? s_g[sr] : 0;
+                o_b[x] = sr >= 0 ? s_b[sr] : 0;
+            }
+            if (BACKWARD || xb >= w) continue;  // (warp-uniform)
+            const unsigned mL = __ballot_sync(0xFFFFFFFFu, act && sl < 0);
+            const unsigned mR = __ballot_sync(0xFFFFFFFFu, act && sr < 0);
+            if (lane == 0) {
+                L.mask_bits[static_cast<size_t>(y) * L.mask_pitch + (xb >> 5)] = mL;
+                Rt.mask_bits[static_cast<size_t>(y) * Rt.mask_pitch + (xb >> 5)] = mR;
+            }
+            if (mL) {
+                uint32_t start = 0;
+                if (lane == 0) start = atomicAdd(L.count, static_cast<uint32_t>(__popc(mL)));
+                start = __shfl_sync(0xFFFFFFFFu, start, 0);
+                if ((mL >> lane) & 1u) L.list[start + __popc(mL & ((1u << lane) - 1u))] = row_base + x;
+            }
+            if (mR) {
+                uint32_t start = 0;
+                if (lane == 0) start = atomicAdd(Rt.count, static_cast<uint32_t>(__popc(mR)));
+                start = __shfl_sync(0xFFFFFFFFu, start, 0);
+                if ((mR >> lane) & 1u) Rt.list[start + __popc(mR & ((1u << lane) - 1u))] = row_base + x;
+            }
+        }
+        __syncthreads();
+        for (int v = tid; v < nvec; v += blockDim.x) {
+            const size_t o = static_cast<size_t>(16 * v);
+            *reinterpret_cast<uint4*>(L.plane[0] + static_cast<size_t>(y) * L.pitch + o) =
+                reinterpret_cast<const uint4*>(o_r)[v];
+            *reinterpret_cast<uint4*>(Rt.plane[1] + static_cast<size_t>(y) * Rt.pitch + o) =
+                reinterpret_cast<const uint4*>(o_g)[v];
+            *reinterpret_cast<uint4*>(Rt.plane[2] + static_cast<size_t>(y) * Rt.pitch + o) =
+                reinterpret_cast<const uint4*>(o_b)[v];
         }
     }
 }
@@ -239,28 +390,59 @@ __global__ void k_hsbs(const uint8_t* __restrict__ l0, const uint8_t* __restrict
 }  // namespace
 
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
-                 Geom gm, const double* shift, bool backward, EyeOut left, EyeOut right,
-                 cudaStream_t st) {
+                 Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
+                 EyeOut right, cudaStream_t st) {
     const int wpad = (gm.w + 15) & ~15;
     const size_t smem = static_cast<size_t>(wpad) * (backward ? 4 : 12);
+    constexpr size_t kMax = 200 * 1024;
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
-        cudaFuncSetAttribute(k_dibr<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        cudaFuncSetAttribute(k_dibr<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_dibr<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+        cudaFuncSetAttribute(k_dibr<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+        cudaFuncSetAttribute(k_dibr<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+        cudaFuncSetAttribute(k_dibr<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         configured[dev] = true;
     }
-    if (smem > 220 * 1024) return cudaErrorInvalidValue;
+    if (smem > kMax) return cudaErrorInvalidValue;
     // the fused anaglyph route: left R and right G/B only, bit masks, lists
     const bool ana = left.plane[0] && !left.plane[1] && !left.plane[2] && !right.plane[0] &&
                      right.plane[1] && right.plane[2] && !left.mask_bytes && !right.mask_bytes;
-    if (ana)
-        k_dibr<0><<<gm.h, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, shift, backward ? 1 : 0,
-                                           left, right);
-    else
-        k_dibr<1><<<gm.h, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, shift, backward ? 1 : 0,
-                                           left, right);
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(left.plane[0]) | reinterpret_cast<uintptr_t>(right.plane[1]) |
+          reinterpret_cast<uintptr_t>(right.plane[2]) | static_cast<uintptr_t>(left.pitch) |
+          static_cast<uintptr_t>(right.pitch)) & 15) == 0;
+    const char* vec_env = getenv("P3S_DIBR_VEC");
+    if (ana && cols && aligned && (backward || (left.mask_bits && right.mask_bits && left.list &&
+                                                right.list)) &&
+        !(vec_env && atoi(vec_env) == 0)) {
+        void (*vk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
+                   const int4*, EyeOut, EyeOut) = backward ? k_dibr_ana<true> : k_dibr_ana<false>;
+        static bool vconf[64] = {false};
+        if (dev < 64 && !vconf[dev]) {
+            cudaFuncSetAttribute(k_dibr_ana<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+            cudaFuncSetAttribute(k_dibr_ana<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+            vconf[dev] = true;
+        }
+        const size_t vsmem = static_cast<size_t>(wpad) * (backward ? 7 : 15) + 16;
+        if (vsmem > kMax) return cudaErrorInvalidValue;
+        int vper = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, vk, 256, vsmem);
+        if (vper < 1) vper = 1;
+        vk<<<min(gm.h, vper * sm_count()), 256, vsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
+                                                             cols, left, right);
+        return cudaGetLastError();
+    }
+    void (*kern)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
+                 const double*, const int4*, int, EyeOut, EyeOut) =
+        ana ? (cols ? k_dibr<0, true> : k_dibr<0, false>) : (cols ? k_dibr<1, true> : k_dibr<1, false>);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int grid = min(gm.h, per_sm * sm_count());
+    kern<<<grid, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h, shift, cols,
+                                  backward ? 1 : 0, left, right);
     return cudaGetLastError();
 }
 

@@ -81,10 +81,12 @@ struct EyeOut {
 };
 
 // DIBR (dibr.cpp:43-104). shift: 256 doubles sigma[d] (p.left = x - sigma, p.right =
-// x + sigma; see engine.cpp). backward = cfg.dibr_mode == kBackwardFallback.
+// x + sigma; see engine.cpp). cols (optional, 256 int4): the host-verified integer column
+// tables (engine.cpp dibr_col_table); when given, no FP64 runs on the device.
+// backward = cfg.dibr_mode == kBackwardFallback.
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
-                 Geom gm, const double* shift, bool backward, EyeOut left, EyeOut right,
-                 cudaStream_t st);
+                 Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
+                 EyeOut right, cudaStream_t st);
 
 // Byte mask -> damaged list (stage-level inpaint entry point).
 cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* list,
