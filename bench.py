@@ -364,11 +364,11 @@ def main():
     if fast:
         smem = p3s.smem_peak(gather=True)
         achieved = taps * 4.0 / (bil_ns * 1e-9) / 1e9
-        roof = {"kernel": "k_bilateral_f32 + k_bilateral_fixup_warp (certified FP32 "
+        roof = {"kernel": "k_bilateral_sep + k_bilateral_fixup_warp (certified FP32 "
                           "cross-bilateral, exact FP64 recompute of uncertified pixels)",
                 "bound": "smem", "achieved": achieved, "peak": smem / 1e9, "unit": "GB/s",
                 "frac": achieved * 1e9 / smem,
-                "traffic": prof.get("k_bilateral_f32"),
+                "traffic": prof.get("k_bilateral_sep"),
                 "algorithmic": f"one 4-byte range-table lookup per tap: {taps:.4g} taps x 4 B "
                                f"per launch (SURVEY.md 8d tap count, r=16)",
                 "peak_source": "measured in this run: conflict-free data-dependent LDS.32 gathers, "
