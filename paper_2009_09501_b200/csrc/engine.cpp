@@ -565,6 +565,31 @@ struct Pipeline::Impl {
         CK(cudaMemcpy2DAsync(dev_plane, pitch, host, w, w, h, cudaMemcpyHostToDevice, st));
     }
 
+    // Download with the depth and filtered-depth copies on a second stream, each started as
+    // soon as its producer finished (events of the timed run), so they overlap the later
+    // stages; the outputs follow the last kernel on the compute stream.
+    void download_overlapped(ConversionResult& out, cudaStream_t st, cudaStream_t cs) {
+        if (last_slot < 0) return download(out, st);
+        const std::array<cudaEvent_t, 6>& ev = ring[last_slot];
+        out.depth = GrayMap(w, h, false);
+        out.filtered_depth = GrayMap(w, h, false);
+        CK(cudaStreamWaitEvent(cs, ev[1], 0));
+        d2h_plane(out.depth.data.data(), depth, pitch, w, cs);
+        CK(cudaStreamWaitEvent(cs, ev[2], 0));
+        d2h_plane(out.filtered_depth.data.data(), filt, pitch, w, cs);
+        for (StereoFormat f : {kFormatAnaglyph, kFormatHsbs, kFormatFsbs}) {
+            if (!(formats & f)) continue;
+            const int ow = output_width(f);
+            ImageRGB8 img(ow, h, false);
+            const std::size_t ps = static_cast<std::size_t>(output_pitch(f)) * h;
+            for (int c = 0; c < 3; ++c)
+                d2h_plane(img.plane(c).data(), output(f) + c * ps, output_pitch(f), ow, st);
+            out.outputs[f] = std::move(img);
+        }
+        CK(cudaStreamSynchronize(cs));
+        CK(cudaStreamSynchronize(st));
+    }
+
     void download(ConversionResult& out, cudaStream_t st) {
         out.depth = GrayMap(w, h, false);
         out.filtered_depth = GrayMap(w, h, false);
@@ -589,6 +614,7 @@ struct Pipeline::Impl {
 struct Device::Impl {
     int ordinal = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // D2H of intermediate results, overlapping compute
     std::list<std::pair<std::string, std::shared_ptr<Pipeline::Impl>>> plans;  // LRU
     static constexpr std::size_t kMaxPlans = 4;
 
@@ -620,6 +646,7 @@ Device::Device(int ordinal) : impl_(new Impl) {
     impl_->ordinal = ordinal;
     CK(cudaSetDevice(ordinal));
     CK(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&impl_->copy_stream, cudaStreamNonBlocking));
 }
 
 Device::~Device() {
@@ -627,6 +654,7 @@ Device::~Device() {
         impl_->plans.clear();
         cudaSetDevice(impl_->ordinal);
         if (impl_->stream) cudaStreamDestroy(impl_->stream);
+        if (impl_->copy_stream) cudaStreamDestroy(impl_->copy_stream);
     }
 }
 
@@ -966,7 +994,7 @@ ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg
     upload_image(*p, src, st);
     p->run(p->src, st, true);
     ConversionResult res;
-    p->download(res, st);
+    p->download_overlapped(res, st, dev.impl().copy_stream);
     res.timings = p->timings();
     return res;
 }
