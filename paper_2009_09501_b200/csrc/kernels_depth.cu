@@ -91,19 +91,22 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
     }
 
     // ---- Sobel magnitude (depth.cpp:21-41) and block sums (depth.cpp:64-67) ----
-    // thread -> row ty, 8 consecutive pixels starting at column 8*c8
+    // thread -> row ty, 8 consecutive pixels starting at column 8*c8. The block column of a
+    // pixel is tracked incrementally (one division per thread, not per pixel).
     {
         const int ty = tid >> 4, c8 = tid & 15;
         const int oy = y0 + ty;
         if (oy < h) {
             const int bx0 = x0 / block, by0 = y0 / block;
             const int lby = oy / block - by0;
+            const int ox0 = x0 + 8 * c8;
+            int lbx = ox0 / block - bx0;
+            int next = (bx0 + lbx + 1) * block;  // first column of the next block
             unsigned run = 0;
-            int run_bx = -1;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int c = 1 + 8 * c8 + k;  // smem column of this pixel
-                const int ox = x0 + c - 1;
+                const int ox = ox0 + k;
                 if (ox < w) {
                     const int p00 = s_y[ty][c - 1], p10 = s_y[ty][c], p20 = s_y[ty][c + 1];
                     const int p01 = s_y[ty + 1][c - 1], p21 = s_y[ty + 1][c + 1];
@@ -111,18 +114,17 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
                               p22 = s_y[ty + 2][c + 1];
                     const int gx = (p20 + 2 * p21 + p22) - (p00 + 2 * p01 + p02);
                     const int gy = (p02 + 2 * p12 + p22) - (p00 + 2 * p10 + p20);
-                    int mag = (abs(gx) + abs(gy)) / 4;
-                    mag = mag < 255 ? mag : 255;
-                    const int lbx = ox / block - bx0;
-                    if (lbx != run_bx) {
-                        if (run_bx >= 0 && run) atomicAdd(&s_sum[lby][run_bx], run);
-                        run_bx = lbx;
+                    const unsigned mag = min((static_cast<unsigned>(abs(gx)) + static_cast<unsigned>(abs(gy))) >> 2, 255u);
+                    if (ox == next) {
+                        if (run) atomicAdd(&s_sum[lby][lbx], run);
+                        ++lbx;
+                        next += block;
                         run = 0;
                     }
-                    run += static_cast<unsigned>(mag);
+                    run += mag;
                 }
             }
-            if (run_bx >= 0 && run) atomicAdd(&s_sum[lby][run_bx], run);
+            if (run) atomicAdd(&s_sum[lby][lbx], run);
         }
     }
     __syncthreads();
