@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the video / 8K config lines")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--reference-budget", type=float, default=150.0)
     args = ap.parse_args()
@@ -344,6 +345,54 @@ def main():
                              "inpaint_passes": [int(passes[0]), int(passes[3])]}
             del pb
 
+    # ---- the other BASELINE configs, measured alongside (not the headline) ----
+    extra = {}
+    if not args.no_extra:
+        # configs[2]: 4K video, 300 frames streamed H2D/compute/D2H on this GPU
+        vid = p3s.Video(W4K, H4K, cfg, streams=3)
+        fp = [src[i % RING].ptr for i in range(300)]
+        op = [dst[i % RING].ptr for i in range(300)]
+        vid.convert_ptrs(fp[:6], op[:6])
+        barrier(world)
+        t0 = time.perf_counter()
+        vid.convert_ptrs(fp, op)
+        vt = time.perf_counter() - t0
+        barrier(world)
+        (vt,) = allreduce_max([vt], world, use_dist)
+        extra["video_4k_300"] = {"frames_per_s": 300 * world / vt, "frames": 300 * world,
+                                 "path": "p3s_video_convert, 3 streams, pinned ring of 8 "
+                                         "distinct frames per GPU, anaglyph out (e2e)"}
+        del vid
+        # configs[4]: 8K anamorph (HSBS), 8 frames per GPU (64 over 8 GPUs)
+        W8, H8 = 7680, 4320
+        c8 = p3s.Config(formats=p3s.HSBS)
+        p8 = p3s.Pipeline(W8, H8, c8)
+        o8 = __import__("oracle").load("port")
+        ring8 = []
+        for i in range(4):
+            d = p3s.DeviceBuffer(p8.frame_bytes)
+            p8.upload(o8.synthetic_frame(W8, H8, frame_seed(1000 + 4 * rank + i)), d.addr)
+            ring8.append(d)
+        for i in range(2):
+            p8.run(ring8[i].addr, timed=True)
+        p3s.stream_sync(p8.stream)
+        p8.timing_sum(reset=True)
+        a8, z8 = p3s.Event(), p3s.Event()
+        barrier(world)
+        a8.record(p8.stream)
+        for i in range(8):
+            p8.run(ring8[i % 4].addr, timed=True)
+        z8.record(p8.stream)
+        p3s.stream_sync(p8.stream)
+        (ms8,) = allreduce_max([a8.elapsed_ms(z8)], world, use_dist)
+        st8, n8 = p8.timing_sum(reset=True)
+        extra["hsbs_8k_batch8"] = {"frames_per_s": 8 * world / (ms8 / 1e3), "frames": 8 * world,
+                                   "mpix_per_s": 8 * world * W8 * H8 / (ms8 / 1e3) / 1e6,
+                                   "stages_ms": {k: v / n8 / 1e6 for k, v in st8.items()},
+                                   "path": "device-resident Pipeline, 7680x4320, HSBS output, "
+                                           "4 distinct frames (398 MB > L2)"}
+        del p8, ring8
+
     if rank != 0:
         if use_dist:
             import torch.distributed as dist
@@ -421,6 +470,7 @@ def main():
         "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "clocks": clk,
         "sweep_base": sweep,
+        "configs_extra": extra,
     }
     if not args.no_cpu_baseline and world == 1:
         kind, threads, times = cpu_reference_rate(args.cpu_budget, 3, frames[0])

@@ -203,3 +203,10 @@ def test_inpaint_stress_vs_oracle(p3s, checker):
         b, sb = checker.inpaint(img, mask, oracle.Cfg())
         assert np.array_equal(a, b), (i, w, h, int(mask.sum()))
         assert tuple(sa) == tuple(sb), (i, w, h, sa, sb)
+
+
+def test_8k_hsbs_full(p3s, checker):
+    """BASELINE configs[4]: 7680x4320 anamorph (HSBS) output, bit-exact against the CPU
+    oracle (auto base 60)."""
+    img = checker.synthetic_frame(7680, 4320, 3)
+    compare_convert(p3s, checker, img, dict(formats=2))

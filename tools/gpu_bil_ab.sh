@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
 for V in $VARS; do
   echo "var $V parity: $(P3S_BIL_FAST=$V timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k 'golden or random or sweep or 4k' 2>&1 | tail -1)"
-  P3S_BIL_FAST=$V timeout 300 python bench.py --steps 60 --warmup 5 --no-sweep --no-cpu-baseline \
+  P3S_BIL_FAST=$V timeout 300 python bench.py --steps 60 --warmup 5 --no-sweep --no-cpu-baseline --no-extra \
       > gpurun_out/bench_${TAG}_v$V.json 2> gpurun_out/bench_${TAG}_v$V.err
   python - "$V" "gpurun_out/bench_${TAG}_v$V.json" <<'PY'
 import json, sys

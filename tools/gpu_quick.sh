@@ -3,7 +3,7 @@
 TAG=${1:-q}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 300 python bench.py --steps 100 --warmup 5 --no-sweep --no-cpu-baseline > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+timeout 300 python bench.py --steps 100 --warmup 5 --no-sweep --no-cpu-baseline --no-extra > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 tail -2 gpurun_out/bench_$TAG.err
 python - gpurun_out/bench_$TAG.json <<'PY'
 import json, sys
