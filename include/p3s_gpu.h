@@ -114,6 +114,13 @@ P3S_API p3s_status p3s_pipeline_upload(p3s_pipeline* p, const uint8_t* r, const 
 typedef struct p3s_video p3s_video;
 P3S_API p3s_status p3s_video_create(int w, int h, const p3s_config* cfg, int streams,
                                     p3s_video** out);
+/* Frame-sharded over several GPUs of one box: frame i runs on devices[i % ndev] (one host
+ * thread per device, `streams` plans each); frames are independent, so nothing crosses
+ * NVLink and no collective runs. A device may be listed more than once. */
+P3S_API p3s_status p3s_video_create_devices(int w, int h, const p3s_config* cfg,
+                                            const int* devices, int ndev, int streams,
+                                            p3s_video** out);
+P3S_API int p3s_video_shards(const p3s_video* v);
 P3S_API p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
                                      uint8_t* const* outs);
 P3S_API void p3s_video_free(p3s_video* v);

@@ -145,6 +145,9 @@ _SIGS = {
     "p3s_pipeline_upload": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "p3s_video_create": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),
     "p3s_video_convert": (C.c_int, [vp, C.POINTER(vp), C.c_int, C.POINTER(vp)]),
+    "p3s_video_create_devices": (C.c_int, [C.c_int, C.c_int, vp, C.POINTER(C.c_int), C.c_int,
+                                           C.c_int, C.POINTER(vp)]),
+    "p3s_video_shards": (C.c_int, [vp]),
     "p3s_video_free": (None, [vp]),
     "p3s_gpu_malloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
     "p3s_gpu_free": (None, [vp]),
@@ -474,10 +477,21 @@ class Pipeline:
 class Video:
     """p3s_video: frames pipelined over `streams` plans (H2D / kernels / D2H overlap)."""
 
-    def __init__(self, w: int, h: int, cfg: Config, streams: int = 3):
+    def __init__(self, w: int, h: int, cfg: Config, streams: int = 3, devices=None):
+        """devices: list of CUDA ordinals to shard frames over (frame i -> devices[i % n],
+        one host thread per device); None = the current device only."""
         self.w, self.h = w, h
         self.handle = vp()
-        _check(lib().p3s_video_create(w, h, cfg.h, streams, C.byref(self.handle)))
+        if devices is None:
+            _check(lib().p3s_video_create(w, h, cfg.h, streams, C.byref(self.handle)))
+        else:
+            arr = (C.c_int * len(devices))(*devices)
+            _check(lib().p3s_video_create_devices(w, h, cfg.h, arr, len(devices), streams,
+                                                  C.byref(self.handle)))
+
+    @property
+    def shards(self) -> int:
+        return lib().p3s_video_shards(self.handle)
 
     def __del__(self):
         if getattr(self, "handle", None) and _lib is not None:

@@ -14,6 +14,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "p3s/pipeline.hpp"
@@ -48,7 +49,13 @@ struct p3s_pipeline {
     std::unique_ptr<p3s::Pipeline> p;
 };
 struct p3s_video {
-    std::vector<std::unique_ptr<p3s::Pipeline>> pipes;
+    // One shard per GPU: frame i goes to shard i % shards.size() (frames are independent,
+    // reference sequence.cpp:59-77), and inside a shard to stream (i / G) % streams.
+    struct Shard {
+        int device = 0;
+        std::vector<std::unique_ptr<p3s::Pipeline>> pipes;
+    };
+    std::vector<Shard> shards;
     int w = 0, h = 0;
     unsigned format = 1;
 };
@@ -630,43 +637,115 @@ p3s_status p3s_pipeline_upload(p3s_pipeline* p, const uint8_t* r, const uint8_t*
 }
 
 // ---- video ----
-p3s_status p3s_video_create(int w, int h, const p3s_config* cfg, int streams, p3s_video** out) {
+namespace {
+
+p3s_status video_create(int w, int h, const p3s_config* cfg, const int* devices, int ndev,
+                        int streams, p3s_video** out) {
     NEED(cfg, out);
     return guarded([&] {
         if (streams < 1) throw std::invalid_argument("video needs at least one stream");
+        if (ndev < 1) throw std::invalid_argument("video needs at least one device");
         cfg->cfg.validate();
         auto v = std::make_unique<p3s_video>();
         v->w = w;
         v->h = h;
         const unsigned f = cfg->cfg.formats;
         v->format = (f & 1u) ? 1u : (f & 2u) ? 2u : 4u;
-        p3s::Device& dev = p3s::Device::current();
-        for (int i = 0; i < streams; ++i)
-            v->pipes.push_back(std::make_unique<p3s::Pipeline>(w, h, cfg->cfg, dev));
+        int caller = 0;
+        cudaGetDevice(&caller);
+        try {
+            for (int k = 0; k < ndev; ++k) {
+                const int d = devices ? devices[k] : caller;
+                if (cudaSetDevice(d) != cudaSuccess) {
+                    cudaGetLastError();
+                    throw p3s::DeviceError("cannot select CUDA device " + std::to_string(d));
+                }
+                p3s::Device& dev = p3s::Device::current();
+                p3s_video::Shard shard;
+                shard.device = d;
+                for (int i = 0; i < streams; ++i)
+                    shard.pipes.push_back(std::make_unique<p3s::Pipeline>(w, h, cfg->cfg, dev));
+                v->shards.push_back(std::move(shard));
+            }
+        } catch (...) {
+            cudaSetDevice(caller);
+            throw;
+        }
+        cudaSetDevice(caller);
         *out = v.release();
     });
 }
+
+// Frames k, k + G, k + 2G, ... of one shard, pipelined over its streams on its device.
+void video_shard(p3s_video& v, std::size_t k, const uint8_t* const* frames, int n,
+                 uint8_t* const* outs) {
+    p3s_video::Shard& sh = v.shards[k];
+    if (cudaSetDevice(sh.device) != cudaSuccess) {
+        cudaGetLastError();
+        throw p3s::DeviceError("cannot select CUDA device " + std::to_string(sh.device));
+    }
+    const std::size_t N = static_cast<std::size_t>(v.w) * v.h;
+    const std::size_t on = v.format == 4u ? 2 * N : N;
+    const std::size_t G = v.shards.size();
+    const std::size_t S = sh.pipes.size();
+    std::size_t j = 0;
+    for (std::size_t i = k; i < static_cast<std::size_t>(n); i += G, ++j) {
+        p3s::Pipeline& p = *sh.pipes[j % S];
+        const uint8_t* f = frames[i];
+        p.upload(f, f + N, f + 2 * N, p.d_input());
+        p.run(p.d_input());
+        uint8_t* o[3] = {outs[i], outs[i] + on, outs[i] + 2 * on};
+        p.download_to(nullptr, nullptr, static_cast<p3s::StereoFormat>(v.format), o, nullptr,
+                      false);
+    }
+    for (auto& p : sh.pipes) {
+        const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(p->stream()));
+        if (e != cudaSuccess) throw p3s::DeviceError(cudaGetErrorString(e));
+    }
+}
+
+}  // namespace
+
+p3s_status p3s_video_create(int w, int h, const p3s_config* cfg, int streams, p3s_video** out) {
+    return video_create(w, h, cfg, nullptr, 1, streams, out);
+}
+
+p3s_status p3s_video_create_devices(int w, int h, const p3s_config* cfg, const int* devices,
+                                    int ndev, int streams, p3s_video** out) {
+    NEED(devices);
+    return video_create(w, h, cfg, devices, ndev, streams, out);
+}
+
+int p3s_video_shards(const p3s_video* v) { return v ? static_cast<int>(v->shards.size()) : 0; }
 
 p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
                              uint8_t* const* outs) {
     NEED(v, frames, outs);
     return guarded([&] {
-        const std::size_t N = static_cast<std::size_t>(v->w) * v->h;
-        const std::size_t on = v->format == 4u ? 2 * N : N;
-        const int S = static_cast<int>(v->pipes.size());
-        for (int i = 0; i < n; ++i) {
-            p3s::Pipeline& p = *v->pipes[i % S];
-            const uint8_t* f = frames[i];
-            p.upload(f, f + N, f + 2 * N, p.d_input());
-            p.run(p.d_input());
-            uint8_t* o[3] = {outs[i], outs[i] + on, outs[i] + 2 * on};
-            p.download_to(nullptr, nullptr, static_cast<p3s::StereoFormat>(v->format), o, nullptr,
-                          false);
+        int caller = 0;
+        cudaGetDevice(&caller);
+        struct Restore {
+            int d;
+            ~Restore() { cudaSetDevice(d); }
+        } restore{caller};
+        if (v->shards.size() == 1) {
+            video_shard(*v, 0, frames, n, outs);
+            return;
         }
-        for (auto& p : v->pipes) {
-            const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(p->stream()));
-            if (e != cudaSuccess) throw p3s::DeviceError(cudaGetErrorString(e));
-        }
+        // one host thread per GPU; no data crosses between GPUs
+        std::vector<std::exception_ptr> errs(v->shards.size());
+        std::vector<std::thread> threads;
+        for (std::size_t k = 0; k < v->shards.size(); ++k)
+            threads.emplace_back([&, k] {
+                try {
+                    video_shard(*v, k, frames, n, outs);
+                } catch (...) {
+                    errs[k] = std::current_exception();
+                }
+            });
+        for (auto& t : threads) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
     });
 }
 

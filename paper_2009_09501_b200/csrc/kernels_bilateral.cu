@@ -1278,6 +1278,12 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
     if (radius == 16 && (var == 1 || var == 9))  // measured best (4K: 1.55 ms incl. fix-up)
         return launch_sep<16, 8, 16, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out,
                                          list, count, st);
+    if (radius == 16 && var == 15)
+        return launch_sep<16, 6, 16, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                         list, count, st);
+    if (radius == 16 && var == 17)
+        return launch_sep<16, 8, 12, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out,
+                                         list, count, st);
     if (radius == 16 && var == 12)
         return launch_sep2<16, 8, 8, 2, 16>(depth, guide, gm, spatial_host, spatial_dev, range, out,
                                             list, count, st);

@@ -210,3 +210,24 @@ def test_8k_hsbs_full(p3s, checker):
     oracle (auto base 60)."""
     img = checker.synthetic_frame(7680, 4320, 3)
     compare_convert(p3s, checker, img, dict(formats=2))
+
+
+def test_video_frame_sharding_matches_convert(p3s, checker):
+    """Multi-device frame sharding (p3s_video_create_devices): frame i -> devices[i % n], one
+    host thread per device. On a one-GPU box the device is listed several times, which runs
+    the same threading and ordering logic; bytes must equal per-frame p3s_convert."""
+    w, h = 320, 200
+    cfg = p3s.Config(base=18, formats=p3s.FSBS)
+    frames = [checker.synthetic_frame(w, h, s) for s in range(1, 10)]
+    expect = [p3s.convert(f, cfg)["fsbs"] for f in frames]
+    ndev = p3s.device_count()
+    devices = [i % ndev for i in range(3)]
+    vid = p3s.Video(w, h, cfg, streams=2, devices=devices)
+    assert vid.shards == 3
+    src = [p3s.PinnedBuffer(3 * w * h) for _ in frames]
+    dst = [p3s.PinnedBuffer(3 * 2 * w * h) for _ in frames]
+    for b, f in zip(src, frames):
+        b.array[:] = f.reshape(-1)
+    vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst])
+    for b, e in zip(dst, expect):
+        assert np.array_equal(b.array.reshape(3, h, 2 * w), e)
