@@ -138,6 +138,13 @@ public:
     // Async D2H of the last results into host planes (nullptr = skip); sync if asked.
     void download_to(std::uint8_t* depth, std::uint8_t* filtered, StereoFormat f,
                      std::uint8_t* const* out, void* stream = nullptr, bool sync = true);
+    // Interleaved RGB (the PPM payload, width*height*3 bytes) in and out: the payload is
+    // copied to a device staging buffer and split into planes on the GPU; outputs are
+    // interleaved on the GPU and copied back as ready-to-write payload
+    // (output width * height * 3 bytes). Async on `stream`.
+    void upload_interleaved(const std::uint8_t* rgb, std::uint8_t* d_dst, void* stream = nullptr);
+    void download_interleaved(StereoFormat f, std::uint8_t* rgb_out, void* stream = nullptr,
+                              bool sync = true);
     struct Impl;
 
 private:

@@ -123,6 +123,10 @@ P3S_API p3s_status p3s_video_create_devices(int w, int h, const p3s_config* cfg,
 P3S_API int p3s_video_shards(const p3s_video* v);
 P3S_API p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
                                      uint8_t* const* outs);
+/* Same with RGB-interleaved frames (the PPM payload: w*h*3 bytes, R,G,B per pixel) in and
+ * the output format interleaved out (ow*h*3 bytes): the (de)interleave runs on the GPU. */
+P3S_API p3s_status p3s_video_convert_interleaved(p3s_video* v, const uint8_t* const* frames,
+                                                 int n, uint8_t* const* outs);
 P3S_API void p3s_video_free(p3s_video* v);
 
 /* ---- helpers ---- */

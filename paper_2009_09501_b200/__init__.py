@@ -148,6 +148,7 @@ _SIGS = {
     "p3s_video_create_devices": (C.c_int, [C.c_int, C.c_int, vp, C.POINTER(C.c_int), C.c_int,
                                            C.c_int, C.POINTER(vp)]),
     "p3s_video_shards": (C.c_int, [vp]),
+    "p3s_video_convert_interleaved": (C.c_int, [vp, C.POINTER(vp), C.c_int, C.POINTER(vp)]),
     "p3s_video_free": (None, [vp]),
     "p3s_gpu_malloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
     "p3s_gpu_free": (None, [vp]),
@@ -498,11 +499,14 @@ class Video:
             _lib.p3s_video_free(self.handle)
             self.handle = None
 
-    def convert_ptrs(self, frame_ptrs, out_ptrs) -> None:
+    def convert_ptrs(self, frame_ptrs, out_ptrs, interleaved: bool = False) -> None:
+        """Planar frames (3 planes of w*h) or, with interleaved=True, RGB-interleaved
+        payloads (w*h*3 bytes) in; the first requested format out in the same layout."""
         n = len(frame_ptrs)
         fa = (vp * n)(*frame_ptrs)
         oa = (vp * n)(*out_ptrs)
-        _check(lib().p3s_video_convert(self.handle, fa, n, oa))
+        fn = lib().p3s_video_convert_interleaved if interleaved else lib().p3s_video_convert
+        _check(fn(self.handle, fa, n, oa))
 
 
 class PinnedBuffer:

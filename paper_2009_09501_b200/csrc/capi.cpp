@@ -677,8 +677,9 @@ p3s_status video_create(int w, int h, const p3s_config* cfg, const int* devices,
 }
 
 // Frames k, k + G, k + 2G, ... of one shard, pipelined over its streams on its device.
+// interleaved: frames/outs are RGB-interleaved payloads (converted on the device).
 void video_shard(p3s_video& v, std::size_t k, const uint8_t* const* frames, int n,
-                 uint8_t* const* outs) {
+                 uint8_t* const* outs, bool interleaved = false) {
     p3s_video::Shard& sh = v.shards[k];
     if (cudaSetDevice(sh.device) != cudaSuccess) {
         cudaGetLastError();
@@ -692,6 +693,12 @@ void video_shard(p3s_video& v, std::size_t k, const uint8_t* const* frames, int 
     for (std::size_t i = k; i < static_cast<std::size_t>(n); i += G, ++j) {
         p3s::Pipeline& p = *sh.pipes[j % S];
         const uint8_t* f = frames[i];
+        if (interleaved) {
+            p.upload_interleaved(f, p.d_input());
+            p.run(p.d_input());
+            p.download_interleaved(static_cast<p3s::StereoFormat>(v.format), outs[i], nullptr, false);
+            continue;
+        }
         p.upload(f, f + N, f + 2 * N, p.d_input());
         p.run(p.d_input());
         uint8_t* o[3] = {outs[i], outs[i] + on, outs[i] + 2 * on};
@@ -718,8 +725,9 @@ p3s_status p3s_video_create_devices(int w, int h, const p3s_config* cfg, const i
 
 int p3s_video_shards(const p3s_video* v) { return v ? static_cast<int>(v->shards.size()) : 0; }
 
-p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
-                             uint8_t* const* outs) {
+namespace {
+p3s_status video_convert(p3s_video* v, const uint8_t* const* frames, int n, uint8_t* const* outs,
+                         bool interleaved) {
     NEED(v, frames, outs);
     return guarded([&] {
         int caller = 0;
@@ -729,7 +737,7 @@ p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
             ~Restore() { cudaSetDevice(d); }
         } restore{caller};
         if (v->shards.size() == 1) {
-            video_shard(*v, 0, frames, n, outs);
+            video_shard(*v, 0, frames, n, outs, interleaved);
             return;
         }
         // one host thread per GPU; no data crosses between GPUs
@@ -738,7 +746,7 @@ p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
         for (std::size_t k = 0; k < v->shards.size(); ++k)
             threads.emplace_back([&, k] {
                 try {
-                    video_shard(*v, k, frames, n, outs);
+                    video_shard(*v, k, frames, n, outs, interleaved);
                 } catch (...) {
                     errs[k] = std::current_exception();
                 }
@@ -747,6 +755,17 @@ p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
     });
+}
+}  // namespace
+
+p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames, int n,
+                             uint8_t* const* outs) {
+    return video_convert(v, frames, n, outs, false);
+}
+
+p3s_status p3s_video_convert_interleaved(p3s_video* v, const uint8_t* const* frames, int n,
+                                         uint8_t* const* outs) {
+    return video_convert(v, frames, n, outs, true);
 }
 
 void p3s_video_free(p3s_video* v) { delete v; }

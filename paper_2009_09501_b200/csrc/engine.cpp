@@ -223,6 +223,7 @@ struct Pipeline::Impl {
     unsigned char* stage_arena = nullptr;
     uint8_t* stage_masks = nullptr;  // 2 byte masks
     double* stage_raw = nullptr;
+    uint8_t* ilv = nullptr;  // interleaved RGB staging (6N bytes: FSBS output is 2w wide)
 
     // Per-run stage events in a ring, so a long timed loop keeps every step's stage
     // times without synchronising between steps (harvested by accumulated()).
@@ -365,6 +366,12 @@ struct Pipeline::Impl {
                 if (e) cudaEventDestroy(e);
         if (arena) cudaFree(arena);
         if (stage_arena) cudaFree(stage_arena);
+        if (ilv) cudaFree(ilv);
+    }
+
+    uint8_t* interleave_buffer() {
+        if (!ilv) CK(cudaMalloc(&ilv, 6 * npix()));
+        return ilv;
     }
 
     uint8_t* src_plane(const uint8_t* s, int c) const { return const_cast<uint8_t*>(s) + c * plane(); }
@@ -732,6 +739,25 @@ void Pipeline::upload(const std::uint8_t* r, const std::uint8_t* g, const std::u
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : impl_->stream;
     const std::uint8_t* planes[3] = {r, g, b};
     for (int c = 0; c < 3; ++c) impl_->h2d_plane(d_dst + c * impl_->plane(), planes[c], st);
+}
+void Pipeline::upload_interleaved(const std::uint8_t* rgb, std::uint8_t* d_dst, void* stream) {
+    Impl& p = *impl_;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
+    uint8_t* buf = p.interleave_buffer();
+    CK(cudaMemcpyAsync(buf, rgb, 3 * p.npix(), cudaMemcpyHostToDevice, st));
+    CK(cu::deinterleave(buf, p.w, p.h, d_dst, d_dst + p.plane(), d_dst + 2 * p.plane(), p.pitch, st));
+}
+void Pipeline::download_interleaved(StereoFormat f, std::uint8_t* rgb_out, void* stream, bool sync) {
+    Impl& p = *impl_;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
+    if (!(p.formats & f)) throw std::invalid_argument("format was not requested in the configuration");
+    uint8_t* buf = p.interleave_buffer();
+    const int ow = p.output_width(f), op = p.output_pitch(f);
+    const std::size_t ps = static_cast<std::size_t>(op) * p.h;
+    const uint8_t* o = p.output(f);
+    CK(cu::interleave(o, o + ps, o + 2 * ps, op, ow, p.h, buf, st));
+    CK(cudaMemcpyAsync(rgb_out, buf, 3 * static_cast<std::size_t>(ow) * p.h, cudaMemcpyDeviceToHost, st));
+    if (sync) CK(cudaStreamSynchronize(st));
 }
 void Pipeline::download_to(std::uint8_t* depth, std::uint8_t* filtered, StereoFormat f,
                            std::uint8_t* const* out, void* stream, bool sync) {

@@ -88,6 +88,14 @@ std::string header_text(const char* magic, int w, int h) {
 
 }  // namespace
 
+PpmView ppm_view(const std::uint8_t* data, std::size_t size) {
+    const Header hd = parse(data, size, '6');
+    check_payload(hd.payload_size, 3 * static_cast<std::size_t>(hd.w) * hd.h);
+    return PpmView{hd.w, hd.h, hd.payload};
+}
+
+std::string ppm_header(int w, int h) { return header_text("P6", w, h); }
+
 ImageRGB8 decode_ppm(const std::uint8_t* data, std::size_t size) {
     const Header hd = parse(data, size, '6');
     const std::size_t n = static_cast<std::size_t>(hd.w) * hd.h;

@@ -5,13 +5,18 @@
 // failing frame with every earlier output already on disk. Unlike the reference's strictly
 // serial loop, file read + PPM decode of frame i+1 and encode + write of frame i-1 run on
 // host threads while frame i is on the GPU, so disk/codec time hides behind the device.
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <deque>
 #include <exception>
 #include <filesystem>
+#include <cstring>
 #include <functional>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -193,10 +198,19 @@ SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string
         return l;
     };
 
+    // Frames go to the GPU as raw PPM payload (de-interleaved on the device) and come back
+    // as ready-to-write interleaved payload (interleaved on the device): the host never
+    // touches pixels. One plan per frame size (two alternating); file reads of frame i+1
+    // and writes of frame i-1 run on host threads while frame i is on the device.
     Device& dev = Device::current();
+    struct Plan {
+        std::unique_ptr<Pipeline> pipe[2];
+    };
+    std::map<std::pair<int, int>, Plan> plans;
     Worker writer(2);
     std::int64_t written = 0;
     std::mutex written_mu;
+    std::int64_t ordinal = 0;
     Loaded cur = load(next);
     while (cur.present) {
         // prefetch the next frame's bytes while this one converts
@@ -212,9 +226,9 @@ SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string
             writer.drain();
             std::rethrow_exception(cur.read_error);
         }
-        ImageRGB8 frame;
+        PpmView view{};
         try {
-            frame = decode_ppm(cur.bytes.data(), cur.bytes.size());
+            view = ppm_view(cur.bytes.data(), cur.bytes.size());
         } catch (const PnmError& e) {
             writer.drain();
             if (auto err = writer.error()) std::rethrow_exception(err);
@@ -222,15 +236,42 @@ SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string
             throw SequenceError(cur.index, written,
                                 "frame " + std::to_string(cur.index) + ": " + e.what());
         }
-        auto result = std::make_shared<ConversionResult>(convert_image(frame, cfg, dev));
-        report.frames.push_back({cur.index, frame.width, frame.height, result->timings});
+        if ((cfg.formats & kFormatHsbs) && view.width % 2 != 0) {
+            writer.drain();
+            throw std::invalid_argument("side_by_side: half mode requires an even width");
+        }
+        Plan& plan = plans[{view.width, view.height}];
+        std::unique_ptr<Pipeline>& slot = plan.pipe[ordinal & 1];
+        if (!slot) slot = std::make_unique<Pipeline>(view.width, view.height, cfg, dev);
+        Pipeline& pipe = *slot;
+        pipe.upload_interleaved(view.payload, pipe.d_input());
+        pipe.run_timed(pipe.d_input());
+        struct Out {
+            StereoFormat fmt;
+            Plane bytes;
+        };
+        auto outs = std::make_shared<std::vector<Out>>();
+        for (StereoFormat f : {kFormatAnaglyph, kFormatHsbs, kFormatFsbs}) {
+            if (!(cfg.formats & f)) continue;
+            const int ow = f == kFormatFsbs ? 2 * view.width : view.width;
+            const std::string head = ppm_header(ow, view.height);
+            Out o{f, Plane(head.size() + 3 * static_cast<std::size_t>(ow) * view.height, false)};
+            std::memcpy(o.bytes.data(), head.data(), head.size());
+            pipe.download_interleaved(f, o.bytes.data() + head.size(), nullptr, false);
+            outs->push_back(std::move(o));
+        }
+        report.frames.push_back({cur.index, view.width, view.height, pipe.last_timings()});
+        {  // the outputs must be on the host before the writer sees them
+            const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(pipe.stream()));
+            if (e != cudaSuccess) throw DeviceError(std::string("CUDA error: ") + cudaGetErrorString(e));
+        }
+        ++ordinal;
         if (auto err = writer.error()) std::rethrow_exception(err);
         const std::int64_t idx = cur.index;
-        writer.push([&, result, idx] {
-            for (const auto& [fmt, img] : result->outputs) {
-                const std::string name = out_pat.stem(idx) + "_" + format_name(fmt) + ".ppm";
-                const std::vector<std::uint8_t> bytes = encode_ppm(img);
-                write_file((fs::path(out_dir) / name).string(), bytes.data(), bytes.size());
+        writer.push([&, outs, idx] {
+            for (const Out& o : *outs) {
+                const std::string name = out_pat.stem(idx) + "_" + format_name(o.fmt) + ".ppm";
+                write_file((fs::path(out_dir) / name).string(), o.bytes.data(), o.bytes.size());
                 std::lock_guard<std::mutex> lk(written_mu);
                 ++written;
             }

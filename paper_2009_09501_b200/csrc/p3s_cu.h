@@ -120,6 +120,12 @@ cudaError_t side_by_side_half(const uint8_t* const* left, const uint8_t* const* 
 cudaError_t side_by_side_full(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
                               uint8_t* const* out, int out_pitch, cudaStream_t st);
 
+// Interleaved RGB (PPM payload order, w*h*3 bytes) <-> planes of `pitch` (kernels_io.cu).
+cudaError_t deinterleave(const uint8_t* src, int w, int h, uint8_t* r, uint8_t* g, uint8_t* b,
+                         int pitch, cudaStream_t st);
+cudaError_t interleave(const uint8_t* r, const uint8_t* g, const uint8_t* b, int pitch, int w,
+                       int h, uint8_t* dst, cudaStream_t st);
+
 int sm_count();
 // Non-FMA FP64 issue-rate microbenchmark (independent DMUL/DADD chains), ops per second.
 cudaError_t fp64_peak(double* ops_per_s);

@@ -13,6 +13,14 @@
 namespace p3s {
 
 // ---- PNM and files (reference pnm.cpp, io.cpp) ----
+// A validated P6 file viewed in place: dimensions and the interleaved RGB payload (same
+// checks and PnmError messages as decode_ppm, no copy).
+struct PpmView {
+    int width, height;
+    const std::uint8_t* payload;
+};
+PpmView ppm_view(const std::uint8_t* data, std::size_t size);
+std::string ppm_header(int w, int h);
 ImageRGB8 decode_ppm(const std::uint8_t* data, std::size_t size);
 std::vector<std::uint8_t> encode_ppm(const ImageRGB8& img);
 GrayMap decode_pgm(const std::uint8_t* data, std::size_t size);

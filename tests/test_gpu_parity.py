@@ -231,3 +231,70 @@ def test_video_frame_sharding_matches_convert(p3s, checker):
     vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst])
     for b, e in zip(dst, expect):
         assert np.array_equal(b.array.reshape(3, h, 2 * w), e)
+
+
+def _ppm_bytes(img):
+    _, h, w = img.shape
+    return f"P6\n{w} {h}\n255\n".encode() + np.ascontiguousarray(img.transpose(1, 2, 0)).tobytes()
+
+
+def test_convert_sequence_files_match_oracle(p3s, checker, tmp_path):
+    """p3s_convert_sequence (reference sequence.cpp:52-145): PPM payloads go to the GPU
+    as raw bytes (de-interleaved there) and come back interleaved; every output file must
+    equal the oracle's frame encoded as P6. A corrupt frame stops the sequence with a decode
+    error after the earlier frames' outputs were written."""
+    import ctypes as C
+    import oracle
+    L = p3s.lib()
+    src, out = tmp_path / "in", tmp_path / "out"
+    src.mkdir()
+    out.mkdir()
+    sizes = [(96, 64), (96, 64), (50, 37), (96, 64)]  # a size change mid-sequence
+    frames = [checker.synthetic_frame(w, h, 10 + i) for i, (w, h) in enumerate(sizes)]
+    for i, f in enumerate(frames):
+        (src / f"f_{i + 1:03d}.ppm").write_bytes(_ppm_bytes(f))  # starts at 1 (no frame 0)
+    over = dict(base=10, formats=5)
+    cfg = p3s.Config(**over)
+    summ = p3s.SequenceSummary()
+    csv = C.c_void_p()
+    st = L.p3s_convert_sequence(str(src).encode(), b"f_%03d.ppm", str(out).encode(), cfg.h,
+                                C.byref(summ), C.byref(csv))
+    assert st == 0, L.p3s_last_error()
+    assert summ.frames == 4
+    text = C.string_at(L.p3s_buffer_data(csv), L.p3s_buffer_size(csv)).decode()
+    L.p3s_buffer_free(csv)
+    assert len(text.strip().splitlines()) == 5
+    for i, f in enumerate(frames):
+        ref = checker.convert(f, oracle.Cfg(**over))
+        for name in ("anaglyph", "fsbs"):
+            got = (out / f"f_{i + 1:03d}_{name}.ppm").read_bytes()
+            assert got == _ppm_bytes(ref[name]), (i, name)
+    # corrupt frame 3 -> DECODE error naming it; frames 1-2 written before
+    (src / "f_003.ppm").write_bytes(b"P6\n50 37\n255\n\x00\x01")
+    out2 = tmp_path / "out2"
+    out2.mkdir()
+    st = L.p3s_convert_sequence(str(src).encode(), b"f_%03d.ppm", str(out2).encode(), cfg.h,
+                                None, None)
+    assert st == 3
+    assert b"frame 3" in L.p3s_last_error()
+    assert sorted(p.name for p in out2.iterdir()) == sorted(
+        f"f_{i:03d}_{n}.ppm" for i in (1, 2) for n in ("anaglyph", "fsbs"))
+
+
+def test_video_interleaved_matches_convert(p3s, checker):
+    """p3s_video_convert_interleaved: PPM-order payloads in/out, (de)interleave on the GPU;
+    both the 16-pixel vector path (w % 16 == 0) and the per-pixel path (odd width)."""
+    for (w, h, fmt) in ((128, 72, p3s.ANAGLYPH), (97, 41, p3s.FSBS)):
+        cfg = p3s.Config(base=12, formats=fmt)
+        frames = [checker.synthetic_frame(w, h, s) for s in range(1, 5)]
+        key = "anaglyph" if fmt == p3s.ANAGLYPH else "fsbs"
+        expect = [p3s.convert(f, cfg)[key] for f in frames]
+        ow = 2 * w if fmt == p3s.FSBS else w
+        src = [p3s.PinnedBuffer(3 * w * h) for _ in frames]
+        dst = [p3s.PinnedBuffer(3 * ow * h) for _ in frames]
+        for b, f in zip(src, frames):
+            b.array[:] = f.transpose(1, 2, 0).reshape(-1)
+        vid = p3s.Video(w, h, cfg, streams=2)
+        vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst], interleaved=True)
+        for b, e in zip(dst, expect):
+            assert np.array_equal(b.array.reshape(h, ow, 3).transpose(2, 0, 1), e)
