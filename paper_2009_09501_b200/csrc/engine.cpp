@@ -399,9 +399,18 @@ struct Pipeline::Impl {
 
     void enq_bilateral(const uint8_t* dmap, const uint8_t* guide, uint8_t* out, double* raw,
                        cudaStream_t st) {
-        if (!raw && cu::bilateral_fast_available(radius))
+        if (!raw && cu::bilateral_fast_available(radius)) {
             CK(cu::bilateral_fast(dmap, guide, gm, radius, h_spatial.data(), spatial, range, out,
                                   bil_list, bil_count, st));
+            static const bool dbg = std::getenv("P3S_DEBUG_BIL") != nullptr;
+            if (dbg) {
+                uint32_t n = 0;
+                CK(cudaMemcpyAsync(&n, bil_count, sizeof(n), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                std::fprintf(stderr, "[p3s] bilateral %dx%d: %u uncertified pixels (%.4f%%)\n", w,
+                             h, n, 100.0 * n / npix());
+            }
+        }
         else if (tiled)
             CK(cu::bilateral_tiled(dmap, guide, gm, radius, h_spatial.data(), range, out, raw, st));
         else
