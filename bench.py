@@ -252,10 +252,11 @@ def main():
     stream = pipe.stream
 
     # ---- kernel path: inputs resident in HBM ----
-    for i in range(args.warmup):
-        pipe.run(ring[i % RING].addr, timed=True)
+    # untimed runs replay one CUDA graph per ring frame (captured during the warm-up);
+    # the per-stage breakdown comes from a separate event-timed pass below
+    for i in range(max(args.warmup, RING)):
+        pipe.run(ring[i % RING].addr)
     p3s.stream_sync(stream)
-    pipe.timing_sum(reset=True)
     ev0, ev1 = p3s.Event(), p3s.Event()
     clocks = ClockSampler(local)
     barrier(world)
@@ -264,12 +265,16 @@ def main():
     time.sleep(0.3)  # let nvidia-smi attach before the region
     ev0.record(stream)
     for i in range(args.steps):
-        pipe.run(ring[i % RING].addr, timed=True)
+        pipe.run(ring[i % RING].addr)
     ev1.record(stream)
     p3s.stream_sync(stream)
     elapsed_ms = ev0.elapsed_ms(ev1)
     clk = clocks.stop()
     barrier(world)
+    # stage breakdown (CUDA events between stages, direct launches)
+    pipe.timing_sum(reset=True)
+    for i in range(min(args.steps, 40)):
+        pipe.run(ring[i % RING].addr, timed=True)
     stage_sum, nruns = pipe.timing_sum(reset=True)
     (elapsed_max,) = allreduce_max([elapsed_ms], world, use_dist)
     total_frames = args.steps * world

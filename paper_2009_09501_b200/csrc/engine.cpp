@@ -357,6 +357,7 @@ struct Pipeline::Impl {
 
     ~Impl() {
         cudaSetDevice(dev);
+        for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
         if (own_stream && stream) {
             cudaStreamSynchronize(stream);
             cudaStreamDestroy(stream);
@@ -536,10 +537,69 @@ struct Pipeline::Impl {
         return &ring[slot];
     }
 
+    // Untimed runs replay a CUDA graph of the whole frame (captured once per input frame
+    // address; the ring of a video pipeline or bench is a handful of addresses), which
+    // removes the per-kernel launch gaps. Timed runs enqueue directly (their stage events
+    // differ per run). P3S_NO_GRAPHS=1 disables the graphs.
+    struct GraphEntry {
+        const uint8_t* src;
+        cudaGraphExec_t exec;
+    };
+    std::list<GraphEntry> graphs;  // LRU
+    static constexpr std::size_t kMaxGraphs = 16;
+
+    bool graphs_enabled() const {
+        static const bool off = [] {
+            const char* v = std::getenv("P3S_NO_GRAPHS");
+            return v && std::atoi(v) != 0;
+        }();
+        return !off;
+    }
+
+    void run_graph(const uint8_t* s, cudaStream_t st) {
+        for (auto it = graphs.begin(); it != graphs.end(); ++it) {
+            if (it->src == s) {
+                graphs.splice(graphs.begin(), graphs, it);
+                CK(cudaGraphLaunch(graphs.front().exec, st));
+                return;
+            }
+        }
+        cudaStream_t cap = stream;  // capture on the plan's own stream, launch on st
+        CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue(s, cap, nullptr);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(cap, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            throw;
+        }
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamEndCapture(cap, &g));
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        graphs.push_front(GraphEntry{s, exec});
+        while (graphs.size() > kMaxGraphs) {
+            cudaGraphExecDestroy(graphs.back().exec);
+            graphs.pop_back();
+        }
+        CK(cudaGraphLaunch(exec, st));
+    }
+
     void run(const uint8_t* s, cudaStream_t st, bool record) {
         if ((formats & kFormatHsbs) && (w % 2 != 0))
             throw std::invalid_argument("side_by_side: half mode requires an even width");
-        const std::array<cudaEvent_t, 6>* ev = record ? next_events() : nullptr;
+        if (!record && graphs_enabled()) {
+            run_graph(s, st);
+            return;
+        }
+        enqueue(s, st, record ? next_events() : nullptr);
+    }
+
+    void enqueue(const uint8_t* s, cudaStream_t st, const std::array<cudaEvent_t, 6>* ev) {
         if (ev) CK(cudaEventRecord((*ev)[0], st));
         enq_depth(s, st);
         if (ev) CK(cudaEventRecord((*ev)[1], st));
