@@ -60,6 +60,7 @@ struct WarpSmem {
     uint8_t col[3][kE][kE];      // colours (valid on intact pixels next to damage)
     unsigned long long dmg[kE];  // current damage bits per region row
     unsigned long long img[kE];  // in-image bits per region row
+    uint16_t rep[kE * kE];       // the pass's repaired pixels (row << 6 | column)
 };
 
 // 64 damage bits of row gy starting at column gx0 (may be negative / past the width).
@@ -132,34 +133,6 @@ __device__ __forceinline__ unsigned long long two_plus(unsigned long long up, un
     return two;
 }
 
-// Repairs the bits `rep` of region row r from the pass-start intact words (iu, im, id).
-__device__ __forceinline__ void repair_row(const InpaintEye& io, WarpSmem& S, int r,
-                                           unsigned long long rep, unsigned long long iu,
-                                           unsigned long long im, unsigned long long id) {
-    while (rep) {
-        const int c = __ffsll(static_cast<long long>(rep)) - 1;
-        rep &= rep - 1;
-        unsigned cnt = 0, a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy) {
-            const unsigned long long iw = dy < 0 ? iu : (dy > 0 ? id : im);
-#pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
-                if (!dx && !dy) continue;
-                const int cc = c + dx;
-                if (cc < 0 || cc >= kE || !((iw >> cc) & 1ull)) continue;
-                ++cnt;
-                a0 += S.col[0][r + dy][cc];
-                a1 += S.col[1][r + dy][cc];
-                a2 += S.col[2][r + dy][cc];
-            }
-        }
-        if (io.plane[0]) S.col[0][r][c] = static_cast<uint8_t>((2 * a0 + cnt) / (2 * cnt));
-        if (io.plane[1]) S.col[1][r][c] = static_cast<uint8_t>((2 * a1 + cnt) / (2 * cnt));
-        if (io.plane[2]) S.col[2][r][c] = static_cast<uint8_t>((2 * a2 + cnt) / (2 * cnt));
-    }
-}
-
 // One warp simulates up to kPasses Jacobi passes of one tile (+ halo) in shared memory.
 __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int round, WarpSmem& S,
                              uint32_t* counts_slot, bool& remains) {
@@ -214,28 +187,64 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
             if (r >= kPasses && r < kPasses + kT) inner += __popcll(rep[j] & kInner);
         }
         if (!__any_sync(0xFFFFFFFFu, any)) break;  // fixed point of the region
-        // colours (reads pass-start intact neighbours only, so in-place writes are safe)
+        // compact the pass's repairs into one list so the colour work spreads over the lanes
+        const int cnt = __popcll(rep[0]) + __popcll(rep[1]);
+        int incl = cnt;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) repair_row(io, S, lane + 32 * j, rep[j], iu[j], im[j], id[j]);
-        // interior repairs: publish colour + state word; count per pass
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        {
+            int pos = incl - cnt;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int r = lane + 32 * j;
-            if (r < kPasses || r >= kPasses + kT) continue;
-            const int gy = y0 + r;
-            for (unsigned long long b = rep[j] & kInner; b; b &= b - 1) {
-                const int c = __ffsll(static_cast<long long>(b)) - 1;
-                const int gx = x0 + c;
-                const uint8_t c0 = S.col[0][r][c], c1 = S.col[1][r][c], c2 = S.col[2][r][c];
-                const unsigned long long g = static_cast<unsigned long long>(pass0 + k);
-                E.state[static_cast<size_t>(gy) * w + gx] =
-                    kRepaired | (g << 24) | (static_cast<unsigned long long>(c2) << 16) |
-                    (static_cast<unsigned long long>(c1) << 8) | c0;
-                const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
-                if (io.plane[0]) io.plane[0][o] = c0;
-                if (io.plane[1]) io.plane[1][o] = c1;
-                if (io.plane[2]) io.plane[2][o] = c2;
+            for (int j = 0; j < 2; ++j)
+                for (unsigned long long b = rep[j]; b; b &= b - 1)
+                    S.rep[pos++] = static_cast<uint16_t>(((lane + 32 * j) << 6) | (__ffsll(static_cast<long long>(b)) - 1));
+        }
+        __syncwarp();
+        // colours from the pass-start intact neighbours (S.dmg is still the pass-start
+        // state; a repaired pixel is never an intact neighbour in its own pass, so the
+        // in-place writes cannot be read by another lane in this pass)
+        for (int i = lane; i < total; i += 32) {
+            const int e = S.rep[i], r = e >> 6, c = e & 63;
+            const unsigned long long iw[3] = {r > 0 ? S.img[r - 1] & ~S.dmg[r - 1] : 0ull,
+                                              S.img[r] & ~S.dmg[r],
+                                              r + 1 < kE ? S.img[r + 1] & ~S.dmg[r + 1] : 0ull};
+            unsigned cntn = 0, a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (!dx && !dy) continue;
+                    const int cc = c + dx;
+                    if (cc < 0 || cc >= kE || !((iw[dy + 1] >> cc) & 1ull)) continue;
+                    ++cntn;
+                    if (io.plane[0]) a0 += S.col[0][r + dy][cc];
+                    if (io.plane[1]) a1 += S.col[1][r + dy][cc];
+                    if (io.plane[2]) a2 += S.col[2][r + dy][cc];
+                }
             }
+            if (io.plane[0]) S.col[0][r][c] = static_cast<uint8_t>((2 * a0 + cntn) / (2 * cntn));
+            if (io.plane[1]) S.col[1][r][c] = static_cast<uint8_t>((2 * a1 + cntn) / (2 * cntn));
+            if (io.plane[2]) S.col[2][r][c] = static_cast<uint8_t>((2 * a2 + cntn) / (2 * cntn));
+        }
+        __syncwarp();
+        // interior repairs: publish colour + state word
+        for (int i = lane; i < total; i += 32) {
+            const int e = S.rep[i], r = e >> 6, c = e & 63;
+            if (r < kPasses || r >= kPasses + kT || c < kPasses || c >= kPasses + kT) continue;
+            const int gy = y0 + r, gx = x0 + c;
+            const uint8_t c0 = S.col[0][r][c], c1 = S.col[1][r][c], c2 = S.col[2][r][c];
+            const unsigned long long g = static_cast<unsigned long long>(pass0 + k);
+            E.state[static_cast<size_t>(gy) * w + gx] =
+                kRepaired | (g << 24) | (static_cast<unsigned long long>(c2) << 16) |
+                (static_cast<unsigned long long>(c1) << 8) | c0;
+            const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
+            if (io.plane[0]) io.plane[0][o] = c0;
+            if (io.plane[1]) io.plane[1][o] = c1;
+            if (io.plane[2]) io.plane[2][o] = c2;
         }
         inner = __reduce_add_sync(0xFFFFFFFFu, inner);
         if (lane == 0 && inner) atomicAdd(&counts_slot[k], static_cast<uint32_t>(inner));
