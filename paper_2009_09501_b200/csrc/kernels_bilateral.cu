@@ -626,6 +626,13 @@ __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t
     }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <int R, int P, int NW, int U>
 __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     const __grid_constant__ SepParam<R, P> sp, const uint8_t* __restrict__ depth,
@@ -635,9 +642,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R;
     constexpr int SH = TY + 2 * R;
+    static_assert(SW % 16 == 0, "tile rows are fetched as 16-byte chunks");
     extern __shared__ __align__(16) unsigned char smem[];
     char* tbl = reinterpret_cast<char*>(smem);  // [767][32] floats
     uint32_t* s_tile = reinterpret_cast<uint32_t*>(smem + kSepEntries * kF32Copies * 4);
+    // raw guide / depth bytes of the NEXT tile, fetched with cp.async while this one computes
+    uint8_t* s_raw = smem + kSepEntries * kF32Copies * 4 + SW * SH * 4;  // [2][SH][SW]
 
     for (int i = threadIdx.x; i < kSepEntries * kF32Copies; i += blockDim.x) {
         const int k = i / kF32Copies;
@@ -645,25 +655,38 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr double kRel = 44.0 / 16777216.0;
+    // 16-byte chunks of the tile window rows that lie inside the image rows and the pitch;
+    // the rest is never read (the packing step marks out-of-image pixels itself)
+    auto prefetch = [&](int tile) {
+        const int tx0 = (tile % tiles_x) * kTX, ty0 = (tile / tiles_x) * TY;
+        constexpr int kChunks = SW / 16;
+        for (int q = threadIdx.x; q < 2 * SH * kChunks; q += blockDim.x) {
+            const int plane = q / (SH * kChunks), rem = q - plane * (SH * kChunks);
+            const int sy = rem / kChunks, c = rem - sy * kChunks;
+            const int gy = ty0 - R + sy, gx = tx0 - R + 16 * c;
+            if (gy < 0 || gy >= h || gx < 0 || gx >= pitch) continue;
+            const uint8_t* src = (plane ? depth : guide) + static_cast<size_t>(gy) * pitch + gx;
+            cp_async16(s_raw + plane * SH * SW + sy * SW + 16 * c, src);
+        }
+        cp_async_commit();
+    };
+    if (blockIdx.x < ntiles) prefetch(blockIdx.x);
 
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int tx0 = (tile % tiles_x) * kTX;
         const int ty0 = (tile / tiles_x) * TY;
-        __syncthreads();
-        for (int sy = warp; sy < SH; sy += NW) {
-            const int gy = ty0 - R + sy;
-            const bool yin = gy >= 0 && gy < h;
-            const uint8_t* grow = guide + static_cast<size_t>(yin ? gy : 0) * pitch;
-            const uint8_t* drow = depth + static_cast<size_t>(yin ? gy : 0) * pitch;
-            for (int sx = lane; sx < SW; sx += 32) {
-                const int gx = tx0 - R + sx;
-                uint32_t v = static_cast<uint32_t>(kSepOob) << 16;
-                if (yin && gx >= 0 && gx < w)
-                    v = (static_cast<uint32_t>(grow[gx]) << 23) | drow[gx];
-                s_tile[sy * SW + sx] = v;
-            }
+        cp_async_wait_all();
+        __syncthreads();  // raw bytes of this tile landed; the previous tile's compute is done
+        for (int e = threadIdx.x; e < SH * SW; e += blockDim.x) {
+            const int sy = e / SW, sx = e - sy * SW;
+            const int gy = ty0 - R + sy, gx = tx0 - R + sx;
+            uint32_t v = static_cast<uint32_t>(kSepOob) << 16;
+            if (gy >= 0 && gy < h && gx >= 0 && gx < w)
+                v = (static_cast<uint32_t>(s_raw[e]) << 23) | s_raw[SH * SW + e];
+            s_tile[e] = v;
         }
         __syncthreads();
+        if (tile + static_cast<int>(gridDim.x) < ntiles) prefetch(tile + gridDim.x);
 
         const int x = tx0 + lane;
         const int yb = ty0 + warp * P;
@@ -1198,7 +1221,8 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
     for (int dy = -R; dy <= R; ++dy) sp.sy[dy + R] = static_cast<double>(static_cast<float>(row0[dy < 0 ? -dy : dy]));
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
-    const size_t smem = kSepEntries * kF32Copies * 4 + static_cast<size_t>(SW) * SH * 4;
+    const size_t smem = kSepEntries * kF32Copies * 4 + static_cast<size_t>(SW) * SH * 4 +
+                        2 * static_cast<size_t>(SW) * SH;
     static int configured_dev[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
