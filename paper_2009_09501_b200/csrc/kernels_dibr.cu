@@ -348,6 +348,134 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
     }
 }
 
+// Forward DIBR + anaglyph, quad version (the default route): the same z-buffer and output
+// bytes as k_dibr_ana<false> with far fewer instructions per pixel.
+//   stage    lane-contiguous 4-pixel words of R, G, B, depth (128-byte warp requests); the
+//            source row is kept as one packed 0x00BBGGRR word per pixel, so a gather is one
+//            LDS.32 for all channels;
+//   splat    lane-interleaved sources (consecutive destinations across the warp:
+//            conflict-free shared atomicMax on the packed key);
+//   resolve  each thread owns 4 consecutive destinations: one 16-byte key load per eye, two
+//            gathers per pixel, the output bytes assembled in registers and written with one
+//            4-byte store per plane (128-byte warp stores); 4-bit damage nibbles are merged
+//            into 32-bit mask words over 8-lane groups; one list atomic per warp and eye.
+__global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R,
+                                                   const uint8_t* __restrict__ G,
+                                                   const uint8_t* __restrict__ B,
+                                                   const uint8_t* __restrict__ D, int pitch,
+                                                   int w, int h, const int4* __restrict__ cols_g,
+                                                   EyeOut L, EyeOut Rt) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int4 s_cols[256];
+    const int wpad = (w + 15) & ~15;
+    const int nq = wpad >> 2;  // quads
+    uint32_t* s_rgb = reinterpret_cast<uint32_t*>(smem);      // [wpad]
+    uint32_t* keyL = s_rgb + wpad;                             // [wpad]
+    uint32_t* keyR = keyL + wpad;                              // [wpad]
+    uint8_t* s_d = reinterpret_cast<uint8_t*>(keyR + wpad);    // [wpad]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 256; i += blockDim.x) s_cols[i] = cols_g[i];
+    const int nqr = (nq + 31) & ~31;
+
+    for (int y = blockIdx.x; y < h; y += gridDim.x) {
+        __syncthreads();
+        const size_t row = static_cast<size_t>(y) * pitch;
+        for (int q = tid; q < nq; q += blockDim.x) {
+            const uint32_t r4 = __ldg(reinterpret_cast<const uint32_t*>(R + row) + q);
+            const uint32_t g4 = __ldg(reinterpret_cast<const uint32_t*>(G + row) + q);
+            const uint32_t b4 = __ldg(reinterpret_cast<const uint32_t*>(B + row) + q);
+            const uint32_t d4 = __ldg(reinterpret_cast<const uint32_t*>(D + row) + q);
+            const uint32_t rg_lo = __byte_perm(r4, g4, 0x5140), rg_hi = __byte_perm(r4, g4, 0x7362);
+            uint4 px;
+            px.x = __byte_perm(rg_lo, b4, 0x0410) & 0x00FFFFFFu;  // r0 g0 b0 0
+            px.y = __byte_perm(rg_lo, b4, 0x0532) & 0x00FFFFFFu;
+            px.z = __byte_perm(rg_hi, b4, 0x0610) & 0x00FFFFFFu;
+            px.w = __byte_perm(rg_hi, b4, 0x0732) & 0x00FFFFFFu;
+            reinterpret_cast<uint4*>(s_rgb)[q] = px;
+            reinterpret_cast<uint32_t*>(s_d)[q] = d4;
+            reinterpret_cast<uint4*>(keyL)[q] = make_uint4(0, 0, 0, 0);
+            reinterpret_cast<uint4*>(keyR)[q] = make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+        for (int x = tid; x < w; x += blockDim.x) {
+            const int d = s_d[x];
+            const int4 t = s_cols[d];
+            const int a = col_int(t.x, t.z, x), b = col_int(t.y, t.w, x);
+            const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
+            if (static_cast<unsigned>(a) < static_cast<unsigned>(w)) atomicMax(&keyL[a], key);
+            if (static_cast<unsigned>(b) < static_cast<unsigned>(w)) atomicMax(&keyR[b], key);
+        }
+        __syncthreads();
+        const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
+        for (int qb = warp * 32; qb < nqr; qb += blockDim.x) {
+            const int q = qb + lane;
+            const int x0 = 4 * q;
+            unsigned mL = 0, mR = 0;
+            if (q < nq) {
+                const uint4 kl = reinterpret_cast<const uint4*>(keyL)[q];
+                const uint4 kr = reinterpret_cast<const uint4*>(keyR)[q];
+                const uint32_t kla[4] = {kl.x, kl.y, kl.z, kl.w}, kra[4] = {kr.x, kr.y, kr.z, kr.w};
+                uint32_t oR = 0, oG = 0, oB = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (x0 + k >= w) continue;
+                    if (kla[k]) {
+                        const uint32_t v = s_rgb[kXMask - (kla[k] & kXMask)];
+                        oR |= (v & 0xFFu) << (8 * k);
+                    } else {
+                        mL |= 1u << k;
+                    }
+                    if (kra[k]) {
+                        const uint32_t v = s_rgb[kXMask - (kra[k] & kXMask)];
+                        oG |= ((v >> 8) & 0xFFu) << (8 * k);
+                        oB |= ((v >> 16) & 0xFFu) << (8 * k);
+                    } else {
+                        mR |= 1u << k;
+                    }
+                }
+                reinterpret_cast<uint32_t*>(L.plane[0] + static_cast<size_t>(y) * L.pitch)[q] = oR;
+                reinterpret_cast<uint32_t*>(Rt.plane[1] + static_cast<size_t>(y) * Rt.pitch)[q] = oG;
+                reinterpret_cast<uint32_t*>(Rt.plane[2] + static_cast<size_t>(y) * Rt.pitch)[q] = oB;
+            }
+            // mask words: 8 lanes x 4 pixels = 32 pixels; word index q >> 3
+            unsigned wL = mL << (4 * (lane & 7)), wR = mR << (4 * (lane & 7));
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                wL |= __shfl_xor_sync(0xFFFFFFFFu, wL, o);
+                wR |= __shfl_xor_sync(0xFFFFFFFFu, wR, o);
+            }
+            const int mwords = (w + 31) >> 5;
+            if ((lane & 7) == 0 && (q >> 3) < mwords) {
+                L.mask_bits[static_cast<size_t>(y) * L.mask_pitch + (q >> 3)] = wL;
+                Rt.mask_bits[static_cast<size_t>(y) * Rt.mask_pitch + (q >> 3)] = wR;
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                unsigned m = e ? mR : mL;
+                const EyeOut& eo = e ? Rt : L;
+                const int n = __popc(m);
+                if (!__any_sync(0xFFFFFFFFu, n)) continue;
+                int incl = n;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                uint32_t start = 0;
+                if (lane == 31) start = atomicAdd(eo.count, static_cast<uint32_t>(total));
+                start = __shfl_sync(0xFFFFFFFFu, start, 31);
+                uint32_t pos = start + static_cast<uint32_t>(incl - n);
+                while (m) {
+                    const int k = __ffs(m) - 1;
+                    m &= m - 1;
+                    eo.list[pos++] = row_base + static_cast<uint32_t>(x0 + k);
+                }
+            }
+        }
+    }
+}
+
 // Byte mask -> damaged list (stage-level inpaint entry point).
 __global__ void k_mask_to_list(const uint8_t* __restrict__ mask, int mpitch, int w, int h,
                                uint32_t* list, uint32_t* count) {
@@ -414,9 +542,26 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
           reinterpret_cast<uintptr_t>(right.plane[2]) | static_cast<uintptr_t>(left.pitch) |
           static_cast<uintptr_t>(right.pitch)) & 15) == 0;
     const char* vec_env = getenv("P3S_DIBR_VEC");
+    const int vec = vec_env ? atoi(vec_env) : 2;
+    if (ana && cols && aligned && !backward && left.mask_bits && right.mask_bits && left.list &&
+        right.list && vec == 2) {
+        static bool qconf[64] = {false};
+        if (dev < 64 && !qconf[dev]) {
+            cudaFuncSetAttribute(k_dibr_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+            qconf[dev] = true;
+        }
+        const size_t qsmem = static_cast<size_t>(wpad) * 13;
+        if (qsmem > kMax) return cudaErrorInvalidValue;
+        int qper = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, k_dibr_quad, 256, qsmem);
+        if (qper < 1) qper = 1;
+        k_dibr_quad<<<min(gm.h, qper * sm_count()), 256, qsmem, st>>>(
+            r, g, b, depth, gm.pitch, gm.w, gm.h, cols, left, right);
+        return cudaGetLastError();
+    }
     if (ana && cols && aligned && (backward || (left.mask_bits && right.mask_bits && left.list &&
                                                 right.list)) &&
-        !(vec_env && atoi(vec_env) == 0)) {
+        vec != 0) {
         void (*vk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
                    const int4*, EyeOut, EyeOut) = backward ? k_dibr_ana<true> : k_dibr_ana<false>;
         static bool vconf[64] = {false};
