@@ -35,6 +35,17 @@ void check(cudaError_t e, const char* what) {
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+// Stage events: inside a stream capture they must become event-record nodes of the graph
+// (cudaEventRecordExternal); outside a capture that flag is invalid.
+void record_event(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    check(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+    if (cs == cudaStreamCaptureStatusActive)
+        check(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "cudaEventRecordWithFlags");
+    else
+        check(cudaEventRecord(e, st), "cudaEventRecord");
+}
+
 // ---- exact host tables --------------------------------------------------------------------
 
 // bilateral.cpp:22-35: radius ceil(2 sigma_s); spatial exp(-(dx^2+dy^2) * inv_s) with the
@@ -358,6 +369,9 @@ struct Pipeline::Impl {
     ~Impl() {
         cudaSetDevice(dev);
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+        for (auto& g : timed_graphs) cudaGraphExecDestroy(g.exec);
+        for (auto& e : conv_ev)
+            if (e) cudaEventDestroy(e);
         if (own_stream && stream) {
             cudaStreamSynchronize(stream);
             cudaStreamDestroy(stream);
@@ -458,7 +472,7 @@ struct Pipeline::Impl {
         if (!backward) CK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), st));
         CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols, backward,
                     eo[0], eo[1], st));
-        if (mid) CK(cudaEventRecord(mid, st));
+        if (mid) record_event(mid, st);
         if (!backward) {
             cu::InpaintEye ie[2];
             for (int e = 0; e < 2; ++e) {
@@ -547,6 +561,11 @@ struct Pipeline::Impl {
     };
     std::list<GraphEntry> graphs;  // LRU
     static constexpr std::size_t kMaxGraphs = 16;
+    // convert_image's timed frame: one graph per input address with a FIXED event set whose
+    // record nodes are part of the graph (read back right after the synchronous call)
+    std::array<cudaEvent_t, 6> conv_ev{};
+    std::list<GraphEntry> timed_graphs;
+    bool last_conv = false;  // the last timed run used conv_ev
 
     bool graphs_enabled() const {
         static const bool off = [] {
@@ -556,18 +575,21 @@ struct Pipeline::Impl {
         return !off;
     }
 
-    void run_graph(const uint8_t* s, cudaStream_t st) {
-        for (auto it = graphs.begin(); it != graphs.end(); ++it) {
+    void run_graph(const uint8_t* s, cudaStream_t st, bool timed = false) {
+        std::list<GraphEntry>& cache = timed ? timed_graphs : graphs;
+        if (timed && !conv_ev[0])
+            for (auto& e : conv_ev) CK(cudaEventCreate(&e));
+        for (auto it = cache.begin(); it != cache.end(); ++it) {
             if (it->src == s) {
-                graphs.splice(graphs.begin(), graphs, it);
-                CK(cudaGraphLaunch(graphs.front().exec, st));
+                cache.splice(cache.begin(), cache, it);
+                CK(cudaGraphLaunch(cache.front().exec, st));
                 return;
             }
         }
         cudaStream_t cap = stream;  // capture on the plan's own stream, launch on st
         CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         try {
-            enqueue(s, cap, nullptr);
+            enqueue(s, cap, timed ? &conv_ev : nullptr);
         } catch (...) {
             cudaGraph_t g = nullptr;
             cudaStreamEndCapture(cap, &g);
@@ -581,12 +603,26 @@ struct Pipeline::Impl {
         const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
         cudaGraphDestroy(g);
         CK(e);
-        graphs.push_front(GraphEntry{s, exec});
-        while (graphs.size() > kMaxGraphs) {
-            cudaGraphExecDestroy(graphs.back().exec);
-            graphs.pop_back();
+        cache.push_front(GraphEntry{s, exec});
+        while (cache.size() > kMaxGraphs) {
+            cudaGraphExecDestroy(cache.back().exec);
+            cache.pop_back();
         }
         CK(cudaGraphLaunch(exec, st));
+    }
+
+    // A timed frame for a synchronous caller (convert_image): graph replay with the plan's
+    // fixed event set; timings()/download_overlapped() read those events.
+    void run_conv(const uint8_t* s, cudaStream_t st) {
+        if ((formats & kFormatHsbs) && (w % 2 != 0))
+            throw std::invalid_argument("side_by_side: half mode requires an even width");
+        if (!graphs_enabled()) {
+            run(s, st, true);
+            last_conv = false;
+            return;
+        }
+        run_graph(s, st, true);
+        last_conv = true;
     }
 
     void run(const uint8_t* s, cudaStream_t st, bool record) {
@@ -596,22 +632,24 @@ struct Pipeline::Impl {
             run_graph(s, st);
             return;
         }
+        if (record) last_conv = false;
         enqueue(s, st, record ? next_events() : nullptr);
     }
 
     void enqueue(const uint8_t* s, cudaStream_t st, const std::array<cudaEvent_t, 6>* ev) {
-        if (ev) CK(cudaEventRecord((*ev)[0], st));
+        if (ev) record_event((*ev)[0], st);
         enq_depth(s, st);
-        if (ev) CK(cudaEventRecord((*ev)[1], st));
+        if (ev) record_event((*ev)[1], st);
         enq_bilateral(depth, luma, filt, nullptr, st);
-        if (ev) CK(cudaEventRecord((*ev)[2], st));
+        if (ev) record_event((*ev)[2], st);
         enq_dibr_inpaint(s, st, ev ? (*ev)[3] : nullptr);
-        if (ev) CK(cudaEventRecord((*ev)[4], st));
+        if (ev) record_event((*ev)[4], st);
         enq_formats(st);
-        if (ev) CK(cudaEventRecord((*ev)[5], st));
+        if (ev) record_event((*ev)[5], st);
     }
 
     StageTimings timings() {
+        if (last_conv) return stage_times(conv_ev);
         if (last_slot < 0) return StageTimings{};
         return stage_times(ring[last_slot]);
     }
@@ -645,8 +683,8 @@ struct Pipeline::Impl {
     // soon as its producer finished (events of the timed run), so they overlap the later
     // stages; the outputs follow the last kernel on the compute stream.
     void download_overlapped(ConversionResult& out, cudaStream_t st, cudaStream_t cs) {
-        if (last_slot < 0) return download(out, st);
-        const std::array<cudaEvent_t, 6>& ev = ring[last_slot];
+        if (!last_conv && last_slot < 0) return download(out, st);
+        const std::array<cudaEvent_t, 6>& ev = last_conv ? conv_ev : ring[last_slot];
         out.depth = GrayMap(w, h, false);
         out.filtered_depth = GrayMap(w, h, false);
         CK(cudaStreamWaitEvent(cs, ev[1], 0));
@@ -1087,7 +1125,7 @@ ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg
     auto p = stage_plan(dev, src.width, src.height, cfg);
     cudaStream_t st = p->stream;
     upload_image(*p, src, st);
-    p->run(p->src, st, true);
+    p->run_conv(p->src, st);
     ConversionResult res;
     p->download_overlapped(res, st, dev.impl().copy_stream);
     res.timings = p->timings();
