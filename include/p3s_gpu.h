@@ -130,7 +130,7 @@ P3S_API p3s_status p3s_video_convert_interleaved(p3s_video* v, const uint8_t* co
 P3S_API void p3s_video_free(p3s_video* v);
 
 /* ---- helpers ---- */
-P3S_API p3s_status p3s_gpu_malloc(size_t bytes, void** out);
+P3S_API p3s_status p3s_gpu_malloc(size_t bytes, void** out); /* zero-filled */
 P3S_API void p3s_gpu_free(void* p);
 P3S_API p3s_status p3s_gpu_memset(void* p, int value, size_t bytes);
 P3S_API p3s_status p3s_gpu_stream_sync(void* stream);

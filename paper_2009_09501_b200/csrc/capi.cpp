@@ -779,6 +779,12 @@ p3s_status p3s_gpu_malloc(size_t bytes, void** out) {
             cudaGetLastError();
             throw std::bad_alloc();
         }
+        // zero-filled, so row padding of frames built in it is defined
+        if (cudaMemset(*out, 0, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(*out);
+            throw p3s::DeviceError("cudaMemset failed");
+        }
     });
 }
 void p3s_gpu_free(void* p) {

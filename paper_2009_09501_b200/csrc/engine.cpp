@@ -311,6 +311,9 @@ struct Pipeline::Impl {
         arena_bytes = a.off;
         CK(cudaSetDevice(dev));
         CK(cudaMalloc(&arena, arena_bytes));
+        // zeroed once: the row padding of every plane (pitch > w) is never written by a
+        // kernel but is read by 16-byte row loads (its bytes are ignored)
+        CK(cudaMemsetAsync(arena, 0, arena_bytes, stream));
         src = arena + o_src;
         luma = arena + o_luma;
         depth = arena + o_depth;

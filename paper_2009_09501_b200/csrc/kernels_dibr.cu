@@ -155,24 +155,16 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
         __syncthreads();
 
         if (!backward) {
-            // Splat: a plain store per source, then atomicMax only for the sources whose key
-            // did not survive (depth discontinuities). Every slot ends at max over its sources
-            // of (d+1) << 22 | (0x3FFFFF - x): largest depth, then smallest column
-            // (dibr.cpp:88-99). Left eye splats to trunc(p.right), right eye to trunc(p.left).
+            // Splat: shared atomicMax of (d+1) << 22 | (0x3FFFFF - x) into the destination
+            // slot; the maximum (largest depth, then smallest column, dibr.cpp:88-99) does not
+            // depend on the order the atomics land in. Left eye splats to trunc(p.right),
+            // right eye to trunc(p.left).
             for (int x = tid; x < w; x += blockDim.x) {
                 int a, b;
                 cols(x, a, b);
                 const unsigned key = (static_cast<unsigned>(s_d[x] + 1) << 22) | (kXMask - x);
-                if (a >= 0) keyL[a] = key;
-                if (b >= 0) keyR[b] = key;
-            }
-            __syncthreads();
-            for (int x = tid; x < w; x += blockDim.x) {
-                int a, b;
-                cols(x, a, b);
-                const unsigned key = (static_cast<unsigned>(s_d[x] + 1) << 22) | (kXMask - x);
-                if (a >= 0 && keyL[a] != key) atomicMax(&keyL[a], key);
-                if (b >= 0 && keyR[b] != key) atomicMax(&keyR[b], key);
+                if (a >= 0) atomicMax(&keyL[a], key);
+                if (b >= 0) atomicMax(&keyR[b], key);
             }
             __syncthreads();
         }
