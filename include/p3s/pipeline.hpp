@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "p3s/core.hpp"
@@ -100,6 +101,33 @@ ImageRGB8 side_by_side(const ImageRGB8& left, const ImageRGB8& right, bool half,
 // Full pipeline (reference pipeline.cpp:29-78): one H2D, all stages on the device, one
 // D2H of the requested outputs plus depth and filtered depth.
 ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg, Device& dev);
+
+// The depth and filtered-depth maps of a conversion kept on the GPU until first asked for
+// (the C ABI's p3s_result_depth / _filtered_depth): a device copy made right after the
+// frame, downloaded on demand. Holds device memory from a process-wide pool until released.
+class DeferredMaps {
+public:
+    DeferredMaps(int device, int w, int h, void* dev_buf);
+    ~DeferredMaps();
+    DeferredMaps(const DeferredMaps&) = delete;
+    DeferredMaps& operator=(const DeferredMaps&) = delete;
+    // Downloads both maps once (thread-safe); later calls return the cached host maps.
+    const GrayMap& depth();
+    const GrayMap& filtered();
+
+private:
+    void materialize();
+    int device_, w_, h_;
+    void* buf_;  // 2 * w * h bytes: depth then filtered depth (unpitched)
+    GrayMap depth_, filtered_;
+    bool ready_ = false;
+    std::mutex mu_;
+};
+
+// convert_image without the depth / filtered-depth downloads: outputs and timings come back
+// to the host, the two maps stay on the device in `maps`.
+ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionConfig& cfg,
+                                        Device& dev, std::shared_ptr<DeferredMaps>& maps);
 
 // ---- device-resident pipeline ------------------------------------------------------------
 // A plan for one (size, config) on one device: tables, device buffers, a stream. run()

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <new>
 #include <string>
@@ -38,8 +39,13 @@ struct p3s_config {
 };
 struct p3s_result {
     std::map<unsigned, p3s_image> outputs;
-    p3s_graymap depth;
-    p3s_graymap filtered_depth;
+    // depth / filtered depth stay on the GPU until first asked for (deferred); the host
+    // graymaps below are filled from it on first access
+    std::shared_ptr<p3s::DeferredMaps> deferred;
+    mutable std::mutex mu;
+    mutable p3s_graymap depth;
+    mutable p3s_graymap filtered_depth;
+    mutable bool maps_ready = false;
     p3s_timings timings{};
 };
 struct p3s_bench_report {
@@ -280,12 +286,11 @@ p3s_status p3s_config_set_threads(p3s_config* cfg, int threads) {
 p3s_status p3s_convert(const p3s_image* src, const p3s_config* cfg, p3s_result** out) {
     if (!src || !cfg || !out) return fail(P3S_ERR_INVALID, "null argument");
     return guarded([&] {
-        p3s::ConversionResult core = p3s::convert_image(src->img, cfg->cfg, p3s::Device::current());
         auto res = std::make_unique<p3s_result>();
+        p3s::ConversionResult core = p3s::convert_image_deferred(
+            src->img, cfg->cfg, p3s::Device::current(), res->deferred);
         for (auto& [fmt, img] : core.outputs)
             res->outputs.emplace(static_cast<unsigned>(fmt), p3s_image{std::move(img)});
-        res->depth.map = std::move(core.depth);
-        res->filtered_depth.map = std::move(core.filtered_depth);
         res->timings = to_c(core.timings);
         *out = res.release();
     });
@@ -298,9 +303,30 @@ p3s_status p3s_result_output(const p3s_result* r, p3s_format format, const p3s_i
     *out = &it->second;
     return P3S_OK;
 }
-const p3s_graymap* p3s_result_depth(const p3s_result* r) { return r ? &r->depth : nullptr; }
+namespace {
+// Downloads the deferred maps on first access. Returns false (last error set) on failure.
+bool result_maps(const p3s_result* r) {
+    std::lock_guard<std::mutex> lk(r->mu);
+    if (r->maps_ready) return true;
+    try {
+        if (r->deferred) {
+            r->depth.map = r->deferred->depth();
+            r->filtered_depth.map = r->deferred->filtered();
+        }
+        r->maps_ready = true;
+        return true;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("downloading the depth maps failed: ") + e.what();
+        return false;
+    }
+}
+}  // namespace
+
+const p3s_graymap* p3s_result_depth(const p3s_result* r) {
+    return r && result_maps(r) ? &r->depth : nullptr;
+}
 const p3s_graymap* p3s_result_filtered_depth(const p3s_result* r) {
-    return r ? &r->filtered_depth : nullptr;
+    return r && result_maps(r) ? &r->filtered_depth : nullptr;
 }
 p3s_status p3s_result_timings(const p3s_result* r, p3s_timings* out) {
     if (!r || !out) return fail(P3S_ERR_INVALID, "null argument");

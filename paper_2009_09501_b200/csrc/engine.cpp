@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <list>
+#include <map>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -1121,6 +1122,125 @@ ImageRGB8 side_by_side(const ImageRGB8& left, const ImageRGB8& right, bool half,
     if (half && left.width % 2 != 0)
         throw std::invalid_argument("side_by_side: half mode requires an even width");
     return format_common(left, right, half ? kFormatHsbs : kFormatFsbs, dev);
+}
+
+// ---- deferred depth maps ------------------------------------------------------------------
+namespace {
+
+// Process-wide pool of device buffers for deferred maps, per (device, bytes).
+struct MapPool {
+    std::mutex mu;
+    std::multimap<std::pair<int, std::size_t>, void*> free;
+    std::size_t cached = 0;
+    static constexpr std::size_t kMaxCached = std::size_t(1) << 30;
+
+    void* take(int dev, std::size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = free.find({dev, bytes});
+            if (it != free.end()) {
+                void* p = it->second;
+                free.erase(it);
+                cached -= bytes;
+                return p;
+            }
+        }
+        void* p = nullptr;
+        CK(cudaMalloc(&p, bytes));
+        return p;
+    }
+    void give(int dev, std::size_t bytes, void* p) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (cached + bytes <= kMaxCached) {
+                free.emplace(std::make_pair(dev, bytes), p);
+                cached += bytes;
+                return;
+            }
+        }
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        cudaFree(p);
+        cudaSetDevice(cur);
+    }
+};
+
+MapPool& map_pool() {
+    static MapPool* p = new MapPool();  // intentionally leaked: outlives static dtors
+    return *p;
+}
+
+}  // namespace
+
+DeferredMaps::DeferredMaps(int device, int w, int h, void* dev_buf)
+    : device_(device), w_(w), h_(h), buf_(dev_buf) {}
+
+DeferredMaps::~DeferredMaps() {
+    if (buf_) map_pool().give(device_, 2 * static_cast<std::size_t>(w_) * h_, buf_);
+}
+
+void DeferredMaps::materialize() {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (ready_) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    CK(cudaSetDevice(device_));
+    const std::size_t n = static_cast<std::size_t>(w_) * h_;
+    GrayMap d(w_, h_, false), f(w_, h_, false);
+    const cudaError_t e1 = cudaMemcpy(d.data.data(), buf_, n, cudaMemcpyDeviceToHost);
+    const cudaError_t e2 = cudaMemcpy(f.data.data(), static_cast<uint8_t*>(buf_) + n, n,
+                                      cudaMemcpyDeviceToHost);
+    cudaSetDevice(cur);
+    CK(e1);
+    CK(e2);
+    depth_ = std::move(d);
+    filtered_ = std::move(f);
+    ready_ = true;
+    map_pool().give(device_, 2 * n, buf_);
+    buf_ = nullptr;
+}
+
+const GrayMap& DeferredMaps::depth() {
+    materialize();
+    return depth_;
+}
+const GrayMap& DeferredMaps::filtered() {
+    materialize();
+    return filtered_;
+}
+
+ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionConfig& cfg,
+                                        Device& dev, std::shared_ptr<DeferredMaps>& maps) {
+    cfg.validate();
+    auto p = stage_plan(dev, src.width, src.height, cfg);
+    cudaStream_t st = p->stream;
+    upload_image(*p, src, st);
+    p->run_conv(p->src, st);
+    const std::size_t n = p->npix();
+    uint8_t* buf = static_cast<uint8_t*>(map_pool().take(dev.ordinal(), 2 * n));
+    try {
+        // device copies of the maps (unpitched), then the outputs to the host
+        CK(cudaMemcpy2DAsync(buf, p->w, p->depth, p->pitch, p->w, p->h, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpy2DAsync(buf + n, p->w, p->filt, p->pitch, p->w, p->h, cudaMemcpyDeviceToDevice, st));
+        ConversionResult res;
+        for (StereoFormat f : {kFormatAnaglyph, kFormatHsbs, kFormatFsbs}) {
+            if (!(p->formats & f)) continue;
+            const int ow = p->output_width(f);
+            ImageRGB8 img(ow, p->h, false);
+            const std::size_t ps = static_cast<std::size_t>(p->output_pitch(f)) * p->h;
+            for (int c = 0; c < 3; ++c)
+                p->d2h_plane(img.plane(c).data(), p->output(f) + c * ps, p->output_pitch(f), ow, st);
+            res.outputs[f] = std::move(img);
+        }
+        CK(cudaStreamSynchronize(st));
+        res.timings = p->timings();
+        maps = std::make_shared<DeferredMaps>(dev.ordinal(), p->w, p->h, buf);
+        return res;
+    } catch (...) {
+        map_pool().give(dev.ordinal(), 2 * n, buf);
+        throw;
+    }
 }
 
 ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg, Device& dev) {
