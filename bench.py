@@ -402,6 +402,32 @@ def main():
                                    "path": "device-resident Pipeline, 7680x4320, HSBS output, "
                                            "4 distinct frames (398 MB > L2)"}
         del p8, ring8
+        # the exact-FP64 bilateral (no FP32 certificate) on the same 4K frames, for the FP64
+        # roofline of that kernel: 4 separately rounded DMUL/DADD per tap
+        os.environ["P3S_BIL_FAST"] = "0"
+        try:
+            px = p3s.Pipeline(W4K, H4K, cfg)
+            for i in range(2):
+                px.run(ring[i % RING].addr, timed=True)
+            p3s.stream_sync(px.stream)
+            px.timing_sum(reset=True)
+            for i in range(6):
+                px.run(ring[i % RING].addr, timed=True)
+            stx, nx = px.timing_sum(reset=True)
+            fil = stx["filter_ns"] / nx
+            fp64 = p3s.fp64_peak()
+            ops = 4.0 * bilateral_flops(W4K, H4K) / 4.0
+            extra["bilateral_exact_fp64"] = {
+                "filter_ms": fil / 1e6, "frames_per_s_pipeline": nx / (sum(stx[k] for k in (
+                    "depth_gen_ns", "filter_ns", "dibr_ns", "inpaint_left_ns", "inpaint_right_ns",
+                    "format_ns")) / 1e9),
+                "fp64_tflops": ops / (fil * 1e-9) / 1e12, "fp64_peak_tflops": fp64 / 1e12,
+                "frac": ops / (fil * 1e-9) / fp64,
+                "path": "k_bilateral_r (P3S_BIL_FAST=0): the reference tap order in FP64 for "
+                        "every pixel; same output bytes as the certified kernel"}
+            del px
+        finally:
+            del os.environ["P3S_BIL_FAST"]
         # configs[0]: 1920x1080 -> depth + views + anaglyph (device-resident frames/s)
         W1, H1 = 1920, 1080
         p1 = p3s.Pipeline(W1, H1, cfg)
