@@ -29,6 +29,11 @@
 // from a per-round work list with one atomic per claim (dynamic load balance).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "p3s_cu.h"
 
 namespace cg = cooperative_groups;
@@ -43,6 +48,7 @@ constexpr int kE = kT + 2 * kPasses;   // region side (64: one u64 per row)
 constexpr int kWarps = 8;              // one tile per warp
 constexpr int kThreads = 32 * kWarps;
 constexpr unsigned long long kRepaired = 1ull << 63;
+constexpr uint32_t kHeavy = 128;       // damaged pixels that make a tile "heavy"
 
 struct Eye {
     InpaintEye io;
@@ -50,7 +56,8 @@ struct Eye {
 };
 
 struct Work {
-    uint32_t* init_flags;  // [2][tiles] (dedupe of the initial work list)
+    uint32_t* init_flags;  // [2][tiles] damaged-pixel count per tile (initial work list)
+    uint32_t* heavy;       // [2 * tiles] tiles with >= kHeavy damaged pixels (run first)
     uint32_t* lists;       // [3][2 * tiles] (eye * tiles + tile)
     uint32_t* counters;    // [3][2]: count, claim
     int cap;               // 2 * tiles
@@ -249,12 +256,18 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
         inner = __reduce_add_sync(0xFFFFFFFFu, inner);
         if (lane == 0 && inner) atomicAdd(&counts_slot[k], static_cast<uint32_t>(inner));
         __syncwarp();
+        int inner_left = 0;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             d[j] &= ~rep[j];
             S.dmg[lane + 32 * j] = d[j];
+            const int r = lane + 32 * j;
+            if (r >= kPasses && r < kPasses + kT) inner_left |= (d[j] & kInner) != 0;
         }
         __syncwarp();
+        // interior complete: its pixels never change again (repairs are final), so later
+        // passes add no interior repairs; the halo's evolution is discarded anyway
+        if (!__any_sync(0xFFFFFFFFu, inner_left)) break;
     }
     // 4. interior damage left -> the tile runs again next round
     int left = 0;
@@ -267,6 +280,15 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
     __syncwarp();
 }
 
+// Debug timeline (P3S_DEBUG_INPAINT): per warp, globaltimer ns at the phase boundaries of
+// round 0 plus tile statistics. nullptr in normal runs.
+__device__ unsigned long long* g_inp_dbg = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Work wk, int w, int h,
                                                                int tiles_x, int tiles_y,
                                                                uint32_t* ctl, long long* stats) {
@@ -274,6 +296,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem& S = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
     const int ntiles = tiles_x * tiles_y;
+    unsigned long long* dbg = g_inp_dbg;
+    unsigned long long dt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (dbg) dt[0] = gtimer();
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gsize = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
@@ -289,7 +314,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
             const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
             const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
             const int t = (y / kT) * tiles_x + x / kT;
-            if (atomicExch(&wk.init_flags[e * ntiles + t], 1u) == 0u) {
+            const uint32_t old = atomicAdd(&wk.init_flags[e * ntiles + t], 1u);
+            if (old + 1 == kHeavy) {  // round 0 starts with these (longest first)
+                const uint32_t pos = atomicAdd(&wk.counters[6], 1u);
+                wk.heavy[pos] = static_cast<uint32_t>(e * ntiles + t);
+            }
+            if (old == 0u) {
                 const uint32_t pos = atomicAdd(&wk.counters[0], 1u);
                 wk.lists[pos] = static_cast<uint32_t>(e * ntiles + t);
             }
@@ -298,7 +328,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
     long long remaining[2] = {cnt[0], cnt[1]};
     bool done[2] = {cnt[0] == 0, cnt[1] == 0};
     long long passes[2] = {0, 0}, fallback[2] = {0, 0};
+    if (dbg) dt[1] = gtimer();
     grid.sync();
+    if (dbg) dt[2] = gtimer();
 
     // ctl layout: [eye][slot 0..2][kPasses + 1] pass counts
     for (int round = 0; !(done[0] && done[1]); ++round) {
@@ -312,25 +344,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
             wk.counters[2 * rslot + 1] = 0;
         }
         const uint32_t n = __ldcg(&wk.counters[2 * slot]);
+        const uint32_t nheavy = round == 0 ? __ldcg(&wk.counters[6]) : 0u;
         const uint32_t* list = wk.lists + static_cast<size_t>(slot) * wk.cap;
         uint32_t* next = wk.lists + static_cast<size_t>(nslot) * wk.cap;
         for (;;) {
+            // round 0 takes the heavy tiles first (they bound the round), then the rest
             uint32_t i = 0;
             if (lane == 0) i = atomicAdd(&wk.counters[2 * slot + 1], 1u);
             i = __shfl_sync(0xFFFFFFFFu, i, 0);
-            if (i >= n) break;
-            const uint32_t item = __ldcg(list + i);
+            if (i >= nheavy + n) break;
+            uint32_t item;
+            if (i < nheavy) {
+                item = __ldcg(wk.heavy + i);
+            } else {
+                item = __ldcg(list + (i - nheavy));
+                if (round == 0 && __ldcg(wk.init_flags + item) >= kHeavy) continue;  // done above
+            }
             const int e = static_cast<int>(item) / ntiles, t = static_cast<int>(item) - e * ntiles;
             if (done[e]) continue;
             bool remains = false;
+            const unsigned long long tt0 = dbg ? gtimer() : 0;
             process_tile(e ? R : L, t % tiles_x, t / tiles_x, w, h, round, S,
                          ctl + (e * 3 + slot) * (kPasses + 1), remains);
+            if (dbg && round == 0) {
+                const unsigned long long d = gtimer() - tt0;
+                dt[5] += 1;
+                dt[6] += d;
+                dt[7] = d > dt[7] ? d : dt[7];
+            }
             if (remains && lane == 0) {
                 const uint32_t pos = atomicAdd(&wk.counters[2 * nslot], 1u);
                 next[pos] = item;
             }
         }
+        if (dbg && round == 0) dt[3] = gtimer();
         grid.sync();
+        if (dbg && round == 0) {
+            dt[4] = gtimer();
+            if ((threadIdx.x & 31) == 0) {
+                const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+                for (int q = 0; q < 8; ++q) dbg[gw * 8 + q] = dt[q];
+            }
+        }
         for (int e = 0; e < 2; ++e) {
             if (done[e]) continue;
             const uint32_t* c = ctl + (e * 3 + slot) * (kPasses + 1);
@@ -383,8 +438,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
 size_t inpaint_scratch_bytes(int w, int h) {
     const size_t n = static_cast<size_t>(w) * h;
     const size_t tiles = static_cast<size_t>((w + kT - 1) / kT) * ((h + kT - 1) / kT);
-    // state words [2][n] | init flags [2][tiles] | lists [3][2 * tiles] | counters [3][2]
-    return 2 * n * 8 + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 64 + 256;
+    // state words [2][n] | tile counts [2][tiles] | lists [3][2 * tiles] | counters [4][2] |
+    // heavy list [2 * tiles]
+    return 2 * n * 8 + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 64 + 2 * tiles * 4 + 256;
 }
 
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
@@ -404,12 +460,13 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     wk.init_flags = reinterpret_cast<uint32_t*>(flags);
     wk.lists = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4);
     wk.counters = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4);
+    wk.heavy = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 64);
     wk.cap = static_cast<int>(2 * tiles);
     cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * 3 * (kPasses + 1) * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(flags, 0, 2 * tiles * 4, st);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(wk.counters, 0, 6 * sizeof(uint32_t), st);
+    e = cudaMemsetAsync(wk.counters, 0, 8 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     const size_t smem = kWarps * sizeof(WarpSmem);
     static bool configured[64] = {false};
@@ -426,8 +483,37 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     const int blocks = per_sm * sm_count();
     int w = gm.w, h = gm.h, tx = tiles_x, ty = tiles_y;
     void* args[] = {&L, &R, &wk, &w, &h, &tx, &ty, &scratch, &stats};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_inpaint_tiles), dim3(blocks),
-                                       dim3(kThreads), args, smem, st);
+    static unsigned long long* dbg = nullptr;
+    const bool want = getenv("P3S_DEBUG_INPAINT") != nullptr;
+    if (want && !dbg) {
+        cudaMalloc(&dbg, static_cast<size_t>(blocks) * kWarps * 8 * sizeof(unsigned long long));
+        cudaMemcpyToSymbol(g_inp_dbg, &dbg, sizeof(dbg));
+    }
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_inpaint_tiles), dim3(blocks),
+                                    dim3(kThreads), args, smem, st);
+    if (want && e == cudaSuccess) {
+        cudaStreamSynchronize(st);
+        const int nw = blocks * kWarps;
+        std::vector<unsigned long long> hb(static_cast<size_t>(nw) * 8);
+        cudaMemcpy(hb.data(), dbg, hb.size() * 8, cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull, init = 0, s1 = 0, rnd = 0, s2 = 0, maxtile = 0, tiles = 0, busy = 0;
+        for (int i = 0; i < nw; ++i) t0 = std::min(t0, hb[8 * i]);
+        for (int i = 0; i < nw; ++i) {
+            const unsigned long long* d = &hb[8 * i];
+            init = std::max(init, d[1] - t0);
+            s1 = std::max(s1, d[2] - t0);
+            rnd = std::max(rnd, d[3] - t0);
+            s2 = std::max(s2, d[4] - t0);
+            tiles += d[5];
+            busy += d[6];
+            maxtile = std::max(maxtile, d[7]);
+        }
+        fprintf(stderr, "[p3s] inpaint round0 (ns from first warp start): init done %llu, sync1 %llu, "
+                        "tiles done %llu, sync2 %llu; tiles %llu, mean tile %llu ns, max tile %llu ns, "
+                        "busy %.1f%%\n", init, s1, rnd, s2, tiles, tiles ? busy / tiles : 0ull, maxtile,
+                100.0 * busy / (static_cast<double>(nw) * (rnd - s1 + 1)));
+    }
+    return e;
 }
 
 }  // namespace cu
