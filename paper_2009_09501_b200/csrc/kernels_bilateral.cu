@@ -585,9 +585,7 @@ __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t
     {
         const uint32_t c = row[0];
         const uint32_t goff = c >> 16;
-        float dc, dummy;
-        unpack2(depth_pair(c, c), dc, dummy);
-        dc -= 8388608.0f;
+        const float dc = static_cast<float>(c & 0xFFu);  // I2F on the XU pipe (idle here)
 #pragma unroll
         for (int i = 0; i < P; ++i) {
             SW[i] = 0ull;
@@ -598,12 +596,11 @@ __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t
             SV[i] = pack2(__fmul_rn(wc, dc), 0.0f);
         }
     }
-    const unsigned long long kBias = pack2(-8388608.0f, -8388608.0f);
 #pragma unroll U
     for (int dx = 1; dx <= R; ++dx) {
         const uint32_t a = row[-dx], b = row[dx];
         const uint32_t ga = a >> 16, gb = b >> 16;
-        const unsigned long long D2 = fadd2(depth_pair(a, b), kBias);
+        const unsigned long long D2 = pack2(static_cast<float>(a & 0xFFu), static_cast<float>(b & 0xFFu));
         const unsigned long long S2 = sp.sx2[dx];
         const unsigned long long SD2 = fmul2(S2, D2);  // sx(dx) * d, shared by the P outputs
 #pragma unroll
