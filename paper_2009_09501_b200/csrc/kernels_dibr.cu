@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
 //            gathers per pixel, the output bytes assembled in registers and written with one
 //            4-byte store per plane (128-byte warp stores); 4-bit damage nibbles are merged
 //            into 32-bit mask words over 8-lane groups; one list atomic per warp and eye.
+// MODE 0: anaglyph planes (left R, right G/B); MODE 1: all six eye planes (HSBS / FSBS
+// routes), same z-buffer, masks and lists.
+template <int MODE>
 __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R,
                                                    const uint8_t* __restrict__ G,
                                                    const uint8_t* __restrict__ B,
@@ -407,13 +410,17 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                 const uint4 kl = reinterpret_cast<const uint4*>(keyL)[q];
                 const uint4 kr = reinterpret_cast<const uint4*>(keyR)[q];
                 const uint32_t kla[4] = {kl.x, kl.y, kl.z, kl.w}, kra[4] = {kr.x, kr.y, kr.z, kr.w};
-                uint32_t oR = 0, oG = 0, oB = 0;
+                uint32_t oR = 0, oG = 0, oB = 0, lG = 0, lB = 0, rR = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     if (x0 + k >= w) continue;
                     if (kla[k]) {
                         const uint32_t v = s_rgb[kXMask - (kla[k] & kXMask)];
                         oR |= (v & 0xFFu) << (8 * k);
+                        if (MODE == 1) {
+                            lG |= ((v >> 8) & 0xFFu) << (8 * k);
+                            lB |= ((v >> 16) & 0xFFu) << (8 * k);
+                        }
                     } else {
                         mL |= 1u << k;
                     }
@@ -421,13 +428,31 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                         const uint32_t v = s_rgb[kXMask - (kra[k] & kXMask)];
                         oG |= ((v >> 8) & 0xFFu) << (8 * k);
                         oB |= ((v >> 16) & 0xFFu) << (8 * k);
+                        if (MODE == 1) rR |= (v & 0xFFu) << (8 * k);
                     } else {
                         mR |= 1u << k;
                     }
                 }
-                reinterpret_cast<uint32_t*>(L.plane[0] + static_cast<size_t>(y) * L.pitch)[q] = oR;
-                reinterpret_cast<uint32_t*>(Rt.plane[1] + static_cast<size_t>(y) * Rt.pitch)[q] = oG;
-                reinterpret_cast<uint32_t*>(Rt.plane[2] + static_cast<size_t>(y) * Rt.pitch)[q] = oB;
+                // never write past w: in the direct-FSBS route the left eye's row continues
+                // with the right eye's pixels
+                const size_t lo = static_cast<size_t>(y) * L.pitch, ro = static_cast<size_t>(y) * Rt.pitch;
+                auto put = [&](uint8_t* plane, size_t row, uint32_t v) {
+                    if (x0 + 4 <= w) {
+                        reinterpret_cast<uint32_t*>(plane + row)[q] = v;
+                    } else {
+                        for (int k = 0; x0 + k < w; ++k) plane[row + x0 + k] = static_cast<uint8_t>(v >> (8 * k));
+                    }
+                };
+                if (x0 < w) {
+                    put(L.plane[0], lo, oR);
+                    put(Rt.plane[1], ro, oG);
+                    put(Rt.plane[2], ro, oB);
+                    if (MODE == 1) {
+                        put(L.plane[1], lo, lG);
+                        put(L.plane[2], lo, lB);
+                        put(Rt.plane[0], ro, rR);
+                    }
+                }
             }
             // mask words: 8 lanes x 4 pixels = 32 pixels; word index q >> 3
             unsigned wL = mL << (4 * (lane & 7)), wR = mR << (4 * (lane & 7));
@@ -507,6 +532,37 @@ __global__ void k_hsbs(const uint8_t* __restrict__ l0, const uint8_t* __restrict
     }
 }
 
+// HSBS, 16 output pixels per thread from two 16-byte loads per plane: the column-pair
+// rounded-up mean (a + b + 1) / 2 of 4 pairs at a time with SWAR byte arithmetic,
+// (a | b) - ((a ^ b) >> 1) on the even/odd bytes gathered by PRMT (exact per byte).
+__device__ __forceinline__ uint32_t pair_avg(uint32_t w0, uint32_t w1) {
+    const uint32_t ev = __byte_perm(w0, w1, 0x6420), od = __byte_perm(w0, w1, 0x7531);
+    return (ev | od) - (((ev ^ od) & 0xFEFEFEFEu) >> 1);
+}
+
+__global__ void k_hsbs16(const uint8_t* __restrict__ l0, const uint8_t* __restrict__ l1,
+                         const uint8_t* __restrict__ l2, const uint8_t* __restrict__ r0,
+                         const uint8_t* __restrict__ r1, const uint8_t* __restrict__ r2, int pitch,
+                         int w, int h, uint8_t* o0, uint8_t* o1, uint8_t* o2, int opitch) {
+    const int hw = w / 2;
+    const int nchunk = hw / 16;  // full 16-pixel chunks per eye (hw % 16 == 0 here)
+    const long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long per_row = 2LL * 3 * nchunk;
+    if (item >= per_row * h) return;
+    const int y = static_cast<int>(item / per_row);
+    int rem = static_cast<int>(item % per_row);
+    const int eye = rem / (3 * nchunk);
+    rem -= eye * 3 * nchunk;
+    const int ch = rem / nchunk, c = rem - ch * nchunk;
+    const uint8_t* src = (ch == 0 ? (eye ? r0 : l0) : ch == 1 ? (eye ? r1 : l1) : (eye ? r2 : l2)) +
+                         static_cast<size_t>(y) * pitch + 32 * c;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(src));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+    uint8_t* dst = (ch == 0 ? o0 : ch == 1 ? o1 : o2) + static_cast<size_t>(y) * opitch + eye * hw + 16 * c;
+    *reinterpret_cast<uint4*>(dst) =
+        make_uint4(pair_avg(a.x, a.y), pair_avg(a.z, a.w), pair_avg(b.x, b.y), pair_avg(b.z, b.w));
+}
+
 }  // namespace
 
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
@@ -535,20 +591,30 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
           static_cast<uintptr_t>(right.pitch)) & 15) == 0;
     const char* vec_env = getenv("P3S_DIBR_VEC");
     const int vec = vec_env ? atoi(vec_env) : 2;
-    if (ana && cols && aligned && !backward && left.mask_bits && right.mask_bits && left.list &&
-        right.list && vec == 2) {
+    // all six eye planes, 4-byte aligned rows (the materialised-eyes and direct-FSBS routes)
+    const bool six = left.plane[0] && left.plane[1] && left.plane[2] && right.plane[0] &&
+                     right.plane[1] && right.plane[2] && !left.mask_bytes && !right.mask_bytes &&
+                     ((reinterpret_cast<uintptr_t>(left.plane[0]) | reinterpret_cast<uintptr_t>(left.plane[1]) |
+                       reinterpret_cast<uintptr_t>(left.plane[2]) | reinterpret_cast<uintptr_t>(right.plane[0]) |
+                       reinterpret_cast<uintptr_t>(right.plane[1]) | reinterpret_cast<uintptr_t>(right.plane[2]) |
+                       static_cast<uintptr_t>(left.pitch) | static_cast<uintptr_t>(right.pitch)) & 3) == 0;
+    if (cols && !backward && left.mask_bits && right.mask_bits && left.list && right.list &&
+        vec == 2 && ((ana && aligned) || six)) {
+        void (*qk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
+                   const int4*, EyeOut, EyeOut) = ana ? k_dibr_quad<0> : k_dibr_quad<1>;
         static bool qconf[64] = {false};
         if (dev < 64 && !qconf[dev]) {
-            cudaFuncSetAttribute(k_dibr_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+            cudaFuncSetAttribute(k_dibr_quad<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+            cudaFuncSetAttribute(k_dibr_quad<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
             qconf[dev] = true;
         }
         const size_t qsmem = static_cast<size_t>(wpad) * 13;
         if (qsmem > kMax) return cudaErrorInvalidValue;
         int qper = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, k_dibr_quad, 256, qsmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, qk, 256, qsmem);
         if (qper < 1) qper = 1;
-        k_dibr_quad<<<min(gm.h, qper * sm_count()), 256, qsmem, st>>>(
-            r, g, b, depth, gm.pitch, gm.w, gm.h, cols, left, right);
+        qk<<<min(gm.h, qper * sm_count()), 256, qsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
+                                                             cols, left, right);
         return cudaGetLastError();
     }
     if (ana && cols && aligned && (backward || (left.mask_bits && right.mask_bits && left.list &&
@@ -605,6 +671,19 @@ cudaError_t anaglyph(const uint8_t* const* left, const uint8_t* const* right, Ge
 cudaError_t side_by_side_half(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
                               uint8_t* const* out, int out_pitch, cudaStream_t st) {
     const int hw = gm.w / 2;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(left[0]) | reinterpret_cast<uintptr_t>(left[1]) |
+                         reinterpret_cast<uintptr_t>(left[2]) | reinterpret_cast<uintptr_t>(right[0]) |
+                         reinterpret_cast<uintptr_t>(right[1]) | reinterpret_cast<uintptr_t>(right[2]) |
+                         reinterpret_cast<uintptr_t>(out[0]) | reinterpret_cast<uintptr_t>(out[1]) |
+                         reinterpret_cast<uintptr_t>(out[2]) | static_cast<uintptr_t>(gm.pitch) |
+                         static_cast<uintptr_t>(out_pitch);
+    if (hw % 16 == 0 && (al & 15) == 0) {
+        const long long items = 2LL * 3 * (hw / 16) * gm.h;
+        k_hsbs16<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(
+            left[0], left[1], left[2], right[0], right[1], right[2], gm.pitch, gm.w, gm.h, out[0],
+            out[1], out[2], out_pitch);
+        return cudaGetLastError();
+    }
     const int items = 2 * ((hw + 15) / 16);
     dim3 grid((items + 127) / 128, gm.h);
     k_hsbs<<<grid, 128, 0, st>>>(left[0], left[1], left[2], right[0], right[1], right[2],
