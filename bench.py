@@ -43,7 +43,7 @@ RING = 8
 SWEEP = [0, 2, 16, 30, 60, 120, 254, 510]
 L2_BYTES = 126 * 2**20
 # kernels per step on the default route: k_depth_front, k_block_values, k_upsample,
-# k_bilateral_f32, k_bilateral_fixup_warp, k_dibr<0>, k_inpaint_tiles (ncu launch list in
+# k_bilateral_sep, k_bilateral_fixup2, k_dibr_quad<0>, k_inpaint_tiles (ncu launch list in
 # profiles/)
 LAUNCHES_PER_STEP = 7
 
@@ -475,7 +475,7 @@ def main():
     if fast:
         smem = p3s.smem_peak(gather=True)
         achieved = taps * 4.0 / (bil_ns * 1e-9) / 1e9
-        roof = {"kernel": "k_bilateral_sep + k_bilateral_fixup_warp (certified FP32 "
+        roof = {"kernel": "k_bilateral_sep + k_bilateral_fixup2 (certified FP32 "
                           "cross-bilateral, exact FP64 recompute of uncertified pixels)",
                 "bound": "smem", "achieved": achieved, "peak": smem / 1e9, "unit": "GB/s",
                 "frac": achieved * 1e9 / smem,

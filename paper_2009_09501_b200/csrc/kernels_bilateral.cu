@@ -905,151 +905,107 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_sep2(
     }
 }
 
-// Exact recompute of the uncertified pixels, one thread per pixel, the reference's order.
-__device__ __forceinline__ double bilateral_exact_px(const uint8_t* __restrict__ depth,
-                                                     const uint8_t* __restrict__ guide, int pitch,
-                                                     int w, int h, int R,
-                                                     const double* __restrict__ spatial,
-                                                     const double* __restrict__ range_g, int x,
-                                                     int y) {
-    const int side = R + 1;
-    const int gp = guide[static_cast<size_t>(y) * pitch + x];
-    double ws = 0.0, vs = 0.0;
-    const int dy0 = y - R < 0 ? -y : -R;
-    const int dy1 = y + R >= h ? h - 1 - y : R;
-    for (int dy = dy0; dy <= dy1; ++dy) {
-        const uint8_t* grow = guide + static_cast<size_t>(y + dy) * pitch;
-        const uint8_t* drow = depth + static_cast<size_t>(y + dy) * pitch;
-        const double* s = spatial + static_cast<size_t>(dy + R) * side;
-        {
-            const double wc = __dmul_rn(s[0], range_g[__usad(gp, grow[x], 0)]);
-            ws = __dadd_rn(ws, wc);
-            vs = __dadd_rn(vs, __dmul_rn(wc, static_cast<double>(drow[x])));
-        }
-        for (int dx = 1; dx <= R; ++dx) {
-            const bool lin = x - dx >= 0, rin = x + dx < w;
-            if (lin && rin) {
-                const double wl = __dmul_rn(s[dx], range_g[__usad(gp, grow[x - dx], 0)]);
-                const double wr = __dmul_rn(s[dx], range_g[__usad(gp, grow[x + dx], 0)]);
-                ws = __dadd_rn(ws, __dadd_rn(wl, wr));
-                vs = __dadd_rn(vs, __dadd_rn(__dmul_rn(wl, static_cast<double>(drow[x - dx])),
-                                             __dmul_rn(wr, static_cast<double>(drow[x + dx]))));
-            } else if (lin) {
-                const double wl = __dmul_rn(s[dx], range_g[__usad(gp, grow[x - dx], 0)]);
-                ws = __dadd_rn(ws, wl);
-                vs = __dadd_rn(vs, __dmul_rn(wl, static_cast<double>(drow[x - dx])));
-            } else if (rin) {
-                const double wr = __dmul_rn(s[dx], range_g[__usad(gp, grow[x + dx], 0)]);
-                ws = __dadd_rn(ws, wr);
-                vs = __dadd_rn(vs, __dmul_rn(wr, static_cast<double>(drow[x + dx])));
-            }
-        }
-    }
-    return __ddiv_rn(vs, ws);
-}
-
-// Exact recompute of the uncertified pixels, one warp per pixel. The warp stages the
-// pixel's (2R+1)^2 window in shared memory, then for each window row (dy ascending) lanes
-// 0..R compute that row's terms in parallel — lane 0 the centre (wc, wc*d), lane dx the
-// mirrored pair (wl + wr, wl*dl + wr*dr) or the single in-image side — with the
-// reference's separately rounded operations, and lane 0 adds them to the running sums in
-// the reference order (centre, then dx = 1..R). A pair with both sides outside the image
-// contributes +0, which leaves the non-negative sums unchanged, exactly like the
-// reference's skipped update. The serial FP64 chain is the only latency left.
+// Exact recompute of the uncertified pixels (reference order), sized so that every listed
+// pixel gets its own warp in one wave (4 warps per block, ~6 KB of shared memory per warp).
+// The window is staged with 16-byte loads. The terms of a batch of window rows — per row
+// the centre (wc, wc*d), then per dx the mirrored pair (wl + wr, wl*dl + wr*dr) or the single
+// in-image side, each separately rounded — are computed by all lanes in parallel; lane 0
+// then adds them to the two running sums in the reference order (rows dy ascending; centre,
+// dx = 1..R). Only that serial DADD chain remains on the critical path.
 template <int R>
-__global__ void __launch_bounds__(128) k_bilateral_fixup_warp(
+__global__ void __launch_bounds__(128) k_bilateral_fixup2(
     const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
     int h, const double* __restrict__ spatial, const double* __restrict__ range_g,
     uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
     const uint32_t* __restrict__ count) {
-    constexpr int S = 2 * R + 1;
-    __shared__ uint8_t s_g[4][S * S];
-    __shared__ uint8_t s_d[4][S * S];
-    __shared__ double s_t[4][R + 1], s_u[4][R + 1];
+    constexpr int S = 2 * R + 1, SP = S + 15;  // window side, staged row length
+    constexpr int kBatch = (S + 1) / 2;        // window rows per term batch
+    constexpr int WPB = 4;
+    __shared__ __align__(16) uint8_t s_g[WPB][S][SP];
+    __shared__ __align__(16) uint8_t s_d[WPB][S][SP];
+    __shared__ double2 s_tu[WPB][kBatch][R + 1];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t n = *count;
-    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t k = blockIdx.x * (blockDim.x >> 5) + wib; k < n; k += nwarps) {
+    const uint32_t nwarps = gridDim.x * WPB;
+    for (uint32_t k = blockIdx.x * WPB + wib; k < n; k += nwarps) {
         const uint32_t idx = list[k];
         const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
         const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
-        const int dy0 = y - R < 0 ? -y : -R;
-        const int dy1 = y + R >= h ? h - 1 - y : R;
-        for (int e = lane; e < S * S; e += 32) {
-            const int r = e / S, c = e - r * S;
-            const int gy = y - R + r, gx = x - R + c;
-            uint8_t gv = 0, dv = 0;
-            if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-                gv = __ldg(guide + static_cast<size_t>(gy) * pitch + gx);
-                dv = __ldg(depth + static_cast<size_t>(gy) * pitch + gx);
-            }
-            s_g[wib][e] = gv;
-            s_d[wib][e] = dv;
+        // stage: 16-byte chunks from the aligned column c0 <= x - R; window column j of the
+        // pixel sits at staged offset j + off
+        const int c0 = (x - R) & ~15, off = (x - R) - c0;
+        constexpr int kCh = (S + 15 + 15) / 16;
+#pragma unroll
+        for (int q0 = 0; q0 < (2 * S * kCh + 31) / 32; ++q0) {
+            const int q = lane + 32 * q0;
+            if (q >= 2 * S * kCh) break;
+            const int plane = q / (S * kCh), rem = q - plane * (S * kCh);
+            const int r = rem / kCh, ch = rem - r * kCh;
+            const int gy = y - R + r, gx = c0 + 16 * ch;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (gy >= 0 && gy < h && gx >= 0 && gx < pitch)
+                v = __ldg(reinterpret_cast<const uint4*>((plane ? depth : guide) +
+                                                         static_cast<size_t>(gy) * pitch + gx));
+            if (16 * ch + 16 <= SP)
+                *reinterpret_cast<uint4*>(plane ? &s_d[wib][r][16 * ch] : &s_g[wib][r][16 * ch]) = v;
         }
         __syncwarp();
-        const int gp = s_g[wib][R * S + R];
+        const int gp = s_g[wib][R][R + off];
+        const int dy0 = y - R < 0 ? -y : -R;
+        const int dy1 = y + R >= h ? h - 1 - y : R;
         double ws = 0.0, vs = 0.0;
-        for (int dy = dy0; dy <= dy1; ++dy) {
-            const int r = dy + R;
-            if (lane <= R) {
-                const double* srow = spatial + static_cast<size_t>(r) * (R + 1);
-                const uint8_t* gr = s_g[wib] + r * S + R;
-                const uint8_t* dr = s_d[wib] + r * S + R;
+        for (int rb = 0; rb < S; rb += kBatch) {
+            const int nr = min(kBatch, S - rb);
+            for (int e = lane; e < nr * (R + 1); e += 32) {
+                const int rr = e / (R + 1), j = e - rr * (R + 1);
+                const int r = rb + rr, dy = r - R;
                 double t = 0.0, u = 0.0;
-                if (lane == 0) {
-                    const double wc = __dmul_rn(__ldg(srow), __ldg(range_g + __usad(gp, gr[0], 0)));
-                    t = wc;
-                    u = __dmul_rn(wc, static_cast<double>(dr[0]));
-                } else {
-                    const int dx = lane;
-                    const bool lin = x - dx >= 0, rin = x + dx < w;
-                    const double sdx = __ldg(srow + dx);
-                    if (lin && rin) {
-                        const double wl = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[-dx], 0)));
-                        const double wr = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[dx], 0)));
-                        t = __dadd_rn(wl, wr);
-                        u = __dadd_rn(__dmul_rn(wl, static_cast<double>(dr[-dx])),
-                                      __dmul_rn(wr, static_cast<double>(dr[dx])));
-                    } else if (lin) {
-                        const double wl = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[-dx], 0)));
-                        t = wl;
-                        u = __dmul_rn(wl, static_cast<double>(dr[-dx]));
-                    } else if (rin) {
-                        const double wr = __dmul_rn(sdx, __ldg(range_g + __usad(gp, gr[dx], 0)));
-                        t = wr;
-                        u = __dmul_rn(wr, static_cast<double>(dr[dx]));
+                if (dy >= dy0 && dy <= dy1) {
+                    const uint8_t* gr = &s_g[wib][r][R + off];
+                    const uint8_t* dr = &s_d[wib][r][R + off];
+                    const double sj = __ldg(spatial + r * (R + 1) + j);
+                    if (j == 0) {
+                        t = __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[0], 0)));
+                        u = __dmul_rn(t, static_cast<double>(dr[0]));
+                    } else {
+                        const bool lin = x - j >= 0, rin = x + j < w;
+                        const double wl = lin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[-j], 0))) : 0.0;
+                        const double wr = rin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[j], 0))) : 0.0;
+                        if (lin && rin) {
+                            t = __dadd_rn(wl, wr);
+                            u = __dadd_rn(__dmul_rn(wl, static_cast<double>(dr[-j])),
+                                          __dmul_rn(wr, static_cast<double>(dr[j])));
+                        } else if (lin) {
+                            t = wl;
+                            u = __dmul_rn(wl, static_cast<double>(dr[-j]));
+                        } else if (rin) {
+                            t = wr;
+                            u = __dmul_rn(wr, static_cast<double>(dr[j]));
+                        }
+                        // both sides outside: +0 leaves the non-negative sums unchanged
                     }
                 }
-                s_t[wib][lane] = t;
-                s_u[wib][lane] = u;
+                s_tu[wib][rr][j] = make_double2(t, u);
             }
             __syncwarp();
             if (lane == 0) {
+                for (int rr = 0; rr < nr; ++rr) {
+                    const int dy = rb + rr - R;
+                    if (dy < dy0 || dy > dy1) continue;
+                    double2 v[R + 1];
 #pragma unroll
-                for (int j = 0; j <= R; ++j) {
-                    ws = __dadd_rn(ws, s_t[wib][j]);
-                    vs = __dadd_rn(vs, s_u[wib][j]);
+                    for (int j = 0; j <= R; ++j) v[j] = s_tu[wib][rr][j];
+#pragma unroll
+                    for (int j = 0; j <= R; ++j) {
+                        ws = __dadd_rn(ws, v[j].x);
+                        vs = __dadd_rn(vs, v[j].y);
+                    }
                 }
             }
             __syncwarp();
         }
         if (lane == 0) out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(__ddiv_rn(vs, ws));
         __syncwarp();
-    }
-}
-
-__global__ void __launch_bounds__(128) k_bilateral_fixup(
-    const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
-    int h, int R, const double* __restrict__ spatial, const double* __restrict__ range_g,
-    uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
-    const uint32_t* __restrict__ count) {
-    const uint32_t n = *count;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        const uint32_t idx = list[k];
-        const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
-        const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
-        const double v = bilateral_exact_px(depth, guide, pitch, w, h, R, spatial, range_g, x, y);
-        out[static_cast<size_t>(y) * pitch + x] = round_half_up_u8(v);
     }
 }
 
@@ -1197,7 +1153,7 @@ cudaError_t launch_f32(const uint8_t* depth, const uint8_t* guide, Geom gm,
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_bilateral_fixup_warp<R><<<sm_count() * 8, 128, 0, st>>>(
+    k_bilateral_fixup2<R><<<sm_count() * 8, 128, 0, st>>>(
         depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
 }
@@ -1241,7 +1197,7 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_bilateral_fixup_warp<R><<<sm_count() * 8, 128, 0, st>>>(
+    k_bilateral_fixup2<R><<<sm_count() * 8, 128, 0, st>>>(
         depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
 }
@@ -1283,7 +1239,7 @@ cudaError_t launch_sep2(const uint8_t* depth, const uint8_t* guide, Geom gm,
                                       count, tiles_x, ntiles);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_bilateral_fixup_warp<R><<<sm_count() * 8, 128, 0, st>>>(
+    k_bilateral_fixup2<R><<<sm_count() * 8, 128, 0, st>>>(
         depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
 }
