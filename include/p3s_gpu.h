@@ -137,6 +137,8 @@ P3S_API p3s_status p3s_gpu_stream_sync(void* stream);
 P3S_API p3s_status p3s_gpu_device_sync(void);
 P3S_API p3s_status p3s_gpu_event_create(void** out);
 P3S_API p3s_status p3s_gpu_event_record(void* ev, void* stream);
+/* Makes `stream` wait for the work recorded in `ev` (cudaStreamWaitEvent). */
+P3S_API p3s_status p3s_gpu_stream_wait_event(void* stream, void* ev);
 P3S_API p3s_status p3s_gpu_event_elapsed_ms(void* start, void* stop, float* ms);
 P3S_API void p3s_gpu_event_destroy(void* ev);
 P3S_API void* p3s_host_alloc(size_t bytes); /* pinned pool */

@@ -157,6 +157,7 @@ _SIGS = {
     "p3s_gpu_device_sync": (C.c_int, []),
     "p3s_gpu_event_create": (C.c_int, [C.POINTER(vp)]),
     "p3s_gpu_event_record": (C.c_int, [vp, vp]),
+    "p3s_gpu_stream_wait_event": (C.c_int, [vp, vp]),
     "p3s_gpu_event_elapsed_ms": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
     "p3s_gpu_event_destroy": (None, [vp]),
     "p3s_host_alloc": (vp, [C.c_size_t]),
@@ -548,6 +549,10 @@ class Event:
 
     def record(self, stream=None) -> None:
         _check(lib().p3s_gpu_event_record(self.h, stream))
+
+    def wait(self, stream) -> None:
+        """Make `stream` wait for this event."""
+        _check(lib().p3s_gpu_stream_wait_event(stream, self.h))
 
     def elapsed_ms(self, end: "Event") -> float:
         ms = C.c_float()

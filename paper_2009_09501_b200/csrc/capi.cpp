@@ -851,6 +851,14 @@ p3s_status p3s_gpu_event_record(void* ev, void* stream) {
             throw p3s::DeviceError("cudaEventRecord failed");
     });
 }
+p3s_status p3s_gpu_stream_wait_event(void* stream, void* ev) {
+    NEED(ev);
+    return guarded([&] {
+        if (cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev), 0) !=
+            cudaSuccess)
+            throw p3s::DeviceError("cudaStreamWaitEvent failed");
+    });
+}
 p3s_status p3s_gpu_event_elapsed_ms(void* a, void* b, float* ms) {
     NEED(a, b, ms);
     return guarded([&] {
