@@ -47,6 +47,13 @@ L2_BYTES = 126 * 2**20
 # profiles/)
 LAUNCHES_PER_STEP = 7
 
+# The workload both arms measure (BASELINE.json metric on configs[1]); the arms add how
+# they ran it under "parallelism".
+WORKLOAD = {"workload": "UHD 3840x2160 synthetic_frame -> depth -> cross-bilateral (bit-exact) "
+                        "-> forward DIBR -> inpaint -> anaglyph (BASELINE configs[1]), default "
+                        "config, auto base 30",
+            "width": W4K, "height": H4K, "base": 30, "format": "anaglyph"}
+
 
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
@@ -194,9 +201,9 @@ def run_reference_arm(args, rank, world):
         "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f64",
         "data": "synthetic", "mpix_per_s": fps * W4K * H4K / 1e6,
-        "config": {"workload": "UHD 3840x2160 synthetic_frame(seed=1) -> anaglyph, default "
-                               "config (auto base 30), reference CPU path", "width": W4K,
-                   "height": H4K, "base": 30, "format": "anaglyph"},
+        "config": dict(WORKLOAD, parallelism=f"reference CPU path (oracle/_ref, compiled "
+                                                f"from the reference sources), {threads} host "
+                                                f"threads, synthetic_frame seed 1"),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads,
                          "kind": o.kind,
                          "sample": f"{len(times)} whole UHD frames (time budget {budget:.0f}s), "
@@ -527,14 +534,11 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_max / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32+f64",
         "data": "synthetic", "mpix_per_s": fps * N / 1e6,
-        "config": {"workload": "UHD 3840x2160 synthetic_frame -> depth -> cross-bilateral "
-                               "(bit-exact) -> forward DIBR -> inpaint -> anaglyph (BASELINE "
-                               "configs[1]), default config, auto base 30",
-                   "width": W4K, "height": H4K, "base": 30, "format": "anaglyph",
-                   "l2": f"input ring {RING} frames x {3 * N / 1e6:.1f} MB = "
-                         f"{RING * 3 * N / 1e6:.0f} MB > 126 MB L2",
-                   "parallelism": f"frame-sharded x{world}, no collectives; frames pipelined "
-                                  f"over {len(lanes)} streams per GPU"},
+        "config": dict(WORKLOAD,
+                       l2=f"input ring {RING} frames x {3 * N / 1e6:.1f} MB = "
+                          f"{RING * 3 * N / 1e6:.0f} MB > 126 MB L2",
+                       parallelism=f"frame-sharded x{world}, no collectives; frames pipelined "
+                                   f"over {len(lanes)} streams per GPU"),
         "stages_ms": {k: v / 1e6 for k, v in per.items()},
         "streams": len(lanes),
         "single_stream": {"frames_per_s": min(args.steps, 100) / (single_ms / 1e3),
