@@ -149,6 +149,9 @@ public:
     StageTimings last_timings();
     // Sum of the stage times of every timed run since the last reset (synchronises).
     StageTimings accumulated_timings(long long* count, bool reset = true);
+    // Sum of the main bilateral kernel's time (without the exact fix-up) over the same timed
+    // runs, for the roofline of the dominant kernel.
+    long long bilateral_kernel_ns(long long* count, bool reset = true);
     // Device pointers of the results of the last run (pitch(), or fsbs_pitch() for FSBS).
     const std::uint8_t* d_depth() const;
     const std::uint8_t* d_filtered() const;

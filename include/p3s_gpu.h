@@ -95,6 +95,9 @@ P3S_API p3s_status p3s_pipeline_timings(p3s_pipeline* p, p3s_timings* out);
  * events, so a timed loop needs no per-step synchronisation); count = runs summed. */
 P3S_API p3s_status p3s_pipeline_timing_sum(p3s_pipeline* p, p3s_timings* sum, int64_t* count,
                                            int reset);
+/* Same accumulation for the main bilateral kernel alone (without the exact fix-up). */
+P3S_API p3s_status p3s_pipeline_bilateral_kernel_sum(p3s_pipeline* p, int64_t* sum_ns,
+                                                     int64_t* count, int reset);
 /* Copies results of the last run to host planes (any pointer may be NULL), then syncs. */
 P3S_API p3s_status p3s_pipeline_download(p3s_pipeline* p, uint8_t* depth, uint8_t* filtered,
                                          p3s_format format, uint8_t* outr, uint8_t* outg,

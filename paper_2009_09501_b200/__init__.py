@@ -158,6 +158,7 @@ _SIGS = {
     "p3s_gpu_event_create": (C.c_int, [C.POINTER(vp)]),
     "p3s_gpu_event_record": (C.c_int, [vp, vp]),
     "p3s_gpu_stream_wait_event": (C.c_int, [vp, vp]),
+    "p3s_pipeline_bilateral_kernel_sum": (C.c_int, [vp, i64p, i64p, C.c_int]),
     "p3s_gpu_event_elapsed_ms": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
     "p3s_gpu_event_destroy": (None, [vp]),
     "p3s_host_alloc": (vp, [C.c_size_t]),
@@ -469,6 +470,13 @@ class Pipeline:
         _check(lib().p3s_pipeline_download(self.handle, _p(depth), _p(filt), fmt,
                                            *[_p(out[c]) for c in range(3)]))
         return depth, filt, out
+
+    def bilateral_kernel_sum(self, reset: bool = True):
+        """(sum of the main bilateral kernel's ns, runs) over the timed runs (no fix-up)."""
+        v, n = C.c_int64(), C.c_int64()
+        _check(lib().p3s_pipeline_bilateral_kernel_sum(self.handle, C.byref(v), C.byref(n),
+                                                       int(reset)))
+        return v.value, n.value
 
     def inpaint_stats(self):
         st = np.zeros(6, np.int64)

@@ -632,6 +632,16 @@ p3s_status p3s_pipeline_timing_sum(p3s_pipeline* p, p3s_timings* sum, int64_t* c
     });
 }
 
+p3s_status p3s_pipeline_bilateral_kernel_sum(p3s_pipeline* p, int64_t* sum_ns, int64_t* count,
+                                             int reset) {
+    NEED(p, sum_ns);
+    return guarded([&] {
+        long long n = 0;
+        *sum_ns = p->p->bilateral_kernel_ns(&n, reset != 0);
+        if (count) *count = n;
+    });
+}
+
 p3s_status p3s_pipeline_download(p3s_pipeline* p, uint8_t* depth, uint8_t* filtered,
                                  p3s_format format, uint8_t* outr, uint8_t* outg, uint8_t* outb) {
     NEED(p);

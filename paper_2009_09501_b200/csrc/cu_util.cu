@@ -4,6 +4,15 @@
 namespace p3s {
 namespace cu {
 
+void record_event_any(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, st);
+}
+
 int sm_count() {
     static int cache[64] = {0};
     int dev = 0;

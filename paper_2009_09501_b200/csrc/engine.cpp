@@ -240,11 +240,12 @@ struct Pipeline::Impl {
     // Per-run stage events in a ring, so a long timed loop keeps every step's stage
     // times without synchronising between steps (harvested by accumulated()).
     static constexpr int kRing = 64;
-    std::vector<std::array<cudaEvent_t, 6>> ring;
+    std::vector<std::array<cudaEvent_t, 7>> ring;
     int ring_next = 0, last_slot = -1;
     std::deque<int> pending;
     StageTimings acc;
     long long acc_n = 0;
+    long long acc_bil_ns = 0, acc_bil_n = 0;  // main bilateral kernel (without the fix-up)
     bool own_stream = false;
 
     std::size_t plane() const { return static_cast<std::size_t>(pitch) * h; }
@@ -417,10 +418,10 @@ struct Pipeline::Impl {
     }
 
     void enq_bilateral(const uint8_t* dmap, const uint8_t* guide, uint8_t* out, double* raw,
-                       cudaStream_t st) {
+                       cudaStream_t st, cudaEvent_t after_main = nullptr) {
         if (!raw && cu::bilateral_fast_available(radius)) {
             CK(cu::bilateral_fast(dmap, guide, gm, radius, h_spatial.data(), spatial, range, out,
-                                  bil_list, bil_count, st));
+                                  bil_list, bil_count, st, after_main));
             static const bool dbg = std::getenv("P3S_DEBUG_BIL") != nullptr;
             if (dbg) {
                 uint32_t n = 0;
@@ -434,6 +435,7 @@ struct Pipeline::Impl {
             CK(cu::bilateral_tiled(dmap, guide, gm, radius, h_spatial.data(), range, out, raw, st));
         else
             CK(cu::bilateral(dmap, guide, gm, radius, spatial, range, out, raw, st));
+        if (after_main && !(!raw && cu::bilateral_fast_available(radius))) record_event(after_main, st);
     }
 
     void eye_planes(uint8_t* (&L)[3], uint8_t* (&R)[3], int& lp) const {
@@ -513,7 +515,7 @@ struct Pipeline::Impl {
         }
     }
 
-    StageTimings stage_times(const std::array<cudaEvent_t, 6>& ev) {
+    StageTimings stage_times(const std::array<cudaEvent_t, 7>& ev) {
         StageTimings t;
         CK(cudaEventSynchronize(ev[5]));
         float ms[5] = {0, 0, 0, 0, 0};
@@ -539,9 +541,13 @@ struct Pipeline::Impl {
         acc.inpaint_right_ns += t.inpaint_right_ns;
         acc.format_ns += t.format_ns;
         ++acc_n;
+        float bm = 0.f;  // the dominant kernel alone: depth-stage end -> bilateral main kernel end
+        CK(cudaEventElapsedTime(&bm, ring[slot][1], ring[slot][6]));
+        acc_bil_ns += ms_to_ns(bm);
+        ++acc_bil_n;
     }
 
-    const std::array<cudaEvent_t, 6>* next_events() {
+    const std::array<cudaEvent_t, 7>* next_events() {
         if (ring.empty()) {
             ring.resize(kRing);
             for (auto& set : ring)
@@ -567,7 +573,7 @@ struct Pipeline::Impl {
     static constexpr std::size_t kMaxGraphs = 16;
     // convert_image's timed frame: one graph per input address with a FIXED event set whose
     // record nodes are part of the graph (read back right after the synchronous call)
-    std::array<cudaEvent_t, 6> conv_ev{};
+    std::array<cudaEvent_t, 7> conv_ev{};
     std::list<GraphEntry> timed_graphs;
     bool last_conv = false;  // the last timed run used conv_ev
 
@@ -640,11 +646,11 @@ struct Pipeline::Impl {
         enqueue(s, st, record ? next_events() : nullptr);
     }
 
-    void enqueue(const uint8_t* s, cudaStream_t st, const std::array<cudaEvent_t, 6>* ev) {
+    void enqueue(const uint8_t* s, cudaStream_t st, const std::array<cudaEvent_t, 7>* ev) {
         if (ev) record_event((*ev)[0], st);
         enq_depth(s, st);
         if (ev) record_event((*ev)[1], st);
-        enq_bilateral(depth, luma, filt, nullptr, st);
+        enq_bilateral(depth, luma, filt, nullptr, st, ev ? (*ev)[6] : nullptr);
         if (ev) record_event((*ev)[2], st);
         enq_dibr_inpaint(s, st, ev ? (*ev)[3] : nullptr);
         if (ev) record_event((*ev)[4], st);
@@ -656,6 +662,17 @@ struct Pipeline::Impl {
         if (last_conv) return stage_times(conv_ev);
         if (last_slot < 0) return StageTimings{};
         return stage_times(ring[last_slot]);
+    }
+
+    long long bilateral_kernel_sum(long long* count, bool reset) {
+        while (!pending.empty()) harvest_one();
+        const long long t = acc_bil_ns;
+        if (count) *count = acc_bil_n;
+        if (reset) {
+            acc_bil_ns = 0;
+            acc_bil_n = 0;
+        }
+        return t;
     }
 
     StageTimings accumulated(long long* count, bool reset) {
@@ -688,7 +705,7 @@ struct Pipeline::Impl {
     // stages; the outputs follow the last kernel on the compute stream.
     void download_overlapped(ConversionResult& out, cudaStream_t st, cudaStream_t cs) {
         if (!last_conv && last_slot < 0) return download(out, st);
-        const std::array<cudaEvent_t, 6>& ev = last_conv ? conv_ev : ring[last_slot];
+        const std::array<cudaEvent_t, 7>& ev = last_conv ? conv_ev : ring[last_slot];
         out.depth = GrayMap(w, h, false);
         out.filtered_depth = GrayMap(w, h, false);
         CK(cudaStreamWaitEvent(cs, ev[1], 0));
@@ -826,6 +843,9 @@ void Pipeline::run_timed(const std::uint8_t* d_src, void* stream) {
 StageTimings Pipeline::last_timings() { return impl_->timings(); }
 StageTimings Pipeline::accumulated_timings(long long* count, bool reset) {
     return impl_->accumulated(count, reset);
+}
+long long Pipeline::bilateral_kernel_ns(long long* count, bool reset) {
+    return impl_->bilateral_kernel_sum(count, reset);
 }
 const std::uint8_t* Pipeline::d_depth() const { return impl_->depth; }
 const std::uint8_t* Pipeline::d_filtered() const { return impl_->filt; }

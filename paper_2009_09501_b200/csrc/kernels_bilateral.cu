@@ -796,7 +796,8 @@ cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
 template <int R, int P, int NW, int U = 4>
 cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
                        const double* spatial_host, const double* spatial_dev, const double* range,
-                       uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st) {
+                       uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st,
+                       cudaEvent_t after_main) {
     SepParam<R, P> sp;
     // sx(d) = exp(-(d*d) * inv_s): the dy = 0 row of the host spatial table (same formula)
     const double* row0 = spatial_host + static_cast<size_t>(R) * (R + 1);
@@ -834,6 +835,7 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (after_main) record_event_any(after_main, st);
     k_bilateral_fixup2<R><<<sm_count() * 8, 128, 0, st>>>(
         depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
@@ -844,20 +846,22 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
 cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                            const double* spatial_host, const double* spatial_dev,
                            const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
-                           cudaStream_t st) {
+                           cudaStream_t st, cudaEvent_t after_main) {
     // the certified kernel for radii 7..16 (sigma_s in (3, 8]); P = 8 outputs per thread,
     // 16 warps, the dx loop fully unrolled
 #define P3S_SEP(RR)                                                                          \
     case RR:                                                                                 \
         return launch_sep<RR, 8, 16, RR>(depth, guide, gm, spatial_host, spatial_dev, range,  \
-                                         out, list, count, st);
+                                         out, list, count, st, after_main);
     switch (radius) {
         P3S_SEP(7) P3S_SEP(8) P3S_SEP(9) P3S_SEP(10) P3S_SEP(11) P3S_SEP(12) P3S_SEP(13)
         P3S_SEP(14) P3S_SEP(15) P3S_SEP(16)
         default: break;
     }
 #undef P3S_SEP
-    return bilateral_tiled(depth, guide, gm, radius, spatial_host, range, out, nullptr, st);
+    const cudaError_t e = bilateral_tiled(depth, guide, gm, radius, spatial_host, range, out, nullptr, st);
+    if (after_main) record_event_any(after_main, st);
+    return e;
 }
 
 bool bilateral_fast_available(int radius) {

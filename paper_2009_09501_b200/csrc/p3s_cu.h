@@ -62,7 +62,9 @@ int bilateral_tiled_max_radius();
 cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                            const double* spatial_host, const double* spatial_dev,
                            const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
-                           cudaStream_t st);
+                           cudaStream_t st, cudaEvent_t after_main = nullptr);
+// cudaEventRecord, or an event-record graph node while `st` is being captured.
+void record_event_any(cudaEvent_t e, cudaStream_t st);
 bool bilateral_fast_available(int radius);
 cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                       const double* spatial, const double* range, uint8_t* out, double* raw,
