@@ -589,15 +589,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
 // in-image side, each separately rounded — are computed by all lanes in parallel; lane 0
 // then adds them to the two running sums in the reference order (rows dy ascending; centre,
 // dx = 1..R). Only that serial DADD chain remains on the critical path.
-template <int R>
-__global__ void __launch_bounds__(128) k_bilateral_fixup2(
+template <int R, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_bilateral_fixup2(
     const uint8_t* __restrict__ depth, const uint8_t* __restrict__ guide, int pitch, int w,
     int h, const double* __restrict__ spatial, const double* __restrict__ range_g,
     uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
     const uint32_t* __restrict__ count) {
     constexpr int S = 2 * R + 1, SP = (S + 15 + 15) / 16 * 16;  // window side, staged row length
     constexpr int kBatch = (S + 1) / 2;        // window rows per term batch
-    constexpr int WPB = 4;
     __shared__ __align__(16) uint8_t s_g[WPB][S][SP];
     __shared__ __align__(16) uint8_t s_d[WPB][S][SP];
     __shared__ double2 s_tu[WPB][kBatch][R + 1];
@@ -836,7 +835,9 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (after_main) record_event_any(after_main, st);
-    k_bilateral_fixup2<R><<<sm_count() * 8, 128, 0, st>>>(
+    // 4 warps per block up to R = 16 (static smem < 48 KB), 2 beyond
+    constexpr int WPB = R <= 16 ? 4 : 2;
+    k_bilateral_fixup2<R, WPB><<<sm_count() * 32 / WPB, WPB * 32, 0, st>>>(
         depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
 }
@@ -847,7 +848,7 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
                            const double* spatial_host, const double* spatial_dev,
                            const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
                            cudaStream_t st, cudaEvent_t after_main) {
-    // the certified kernel for radii 7..16 (sigma_s in (3, 8]); P = 8 outputs per thread,
+    // the certified kernel for radii 7..24 (sigma_s in (3, 12]); P = 8 outputs per thread,
     // 16 warps, the dx loop fully unrolled
 #define P3S_SEP(RR)                                                                          \
     case RR:                                                                                 \
@@ -855,7 +856,8 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
                                          out, list, count, st, after_main);
     switch (radius) {
         P3S_SEP(7) P3S_SEP(8) P3S_SEP(9) P3S_SEP(10) P3S_SEP(11) P3S_SEP(12) P3S_SEP(13)
-        P3S_SEP(14) P3S_SEP(15) P3S_SEP(16)
+        P3S_SEP(14) P3S_SEP(15) P3S_SEP(16) P3S_SEP(17) P3S_SEP(18) P3S_SEP(19) P3S_SEP(20)
+        P3S_SEP(21) P3S_SEP(22) P3S_SEP(23) P3S_SEP(24)
         default: break;
     }
 #undef P3S_SEP
@@ -866,7 +868,7 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
 
 bool bilateral_fast_available(int radius) {
     const char* v = getenv("P3S_BIL_FAST");
-    return radius >= 7 && radius <= 16 && !(v && atoi(v) == 0);
+    return radius >= 7 && radius <= 24 && !(v && atoi(v) == 0);
 }
 
 // spatial: device table for the generic kernel, in the layout s[(dy+R)*(R+1)+dx] (dx>=0).

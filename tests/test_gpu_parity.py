@@ -300,9 +300,10 @@ def test_video_interleaved_matches_convert(p3s, checker):
             assert np.array_equal(b.array.reshape(h, ow, 3).transpose(2, 0, 1), e)
 
 
-@pytest.mark.parametrize("sigma_s", [3.1, 4.0, 4.3, 5.0, 5.5, 6.0, 6.5, 7.0, 7.4, 8.0])
+@pytest.mark.parametrize("sigma_s", [3.1, 4.0, 4.3, 5.0, 5.5, 6.0, 6.5, 7.0, 7.4, 8.0, 8.3, 9.0,
+                                     9.5, 10.0, 10.3, 11.0, 11.4, 12.0])
 def test_certified_bilateral_radii(p3s, checker, sigma_s):
-    """The certified FP32 bilateral covers radii 7..16 (ceil(2 sigma_s)); every radius must
+    """The certified FP32 bilateral covers radii 7..24 (ceil(2 sigma_s)); every radius must
     give the reference's filtered depth and anaglyph (odd size: clipped windows, edge tiles,
     a partial last tile row)."""
     img = checker.synthetic_frame(333, 277, int(sigma_s * 10))
