@@ -255,6 +255,10 @@ struct Pipeline::Impl {
         : dev(device), w(width), h(height), cfg(c), stream(st) {
         cfg.validate();
         pixel_count(w, h);
+        if (w > cu::dibr_max_width())
+            throw std::invalid_argument("frame width " + std::to_string(w) +
+                                        " exceeds the GPU DIBR row limit of " +
+                                        std::to_string(cu::dibr_max_width()) + " pixels");
         pitch = round_up(w, 16);
         fpitch = round_up(2 * w, 16);
         mwords = (w + 31) / 32;

@@ -570,7 +570,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                  EyeOut right, cudaStream_t st) {
     const int wpad = (gm.w + 15) & ~15;
     const size_t smem = static_cast<size_t>(wpad) * (backward ? 4 : 12);
-    constexpr size_t kMax = 200 * 1024;
+    constexpr size_t kMax = kDibrMaxSmem;
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -599,7 +599,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                        reinterpret_cast<uintptr_t>(right.plane[1]) | reinterpret_cast<uintptr_t>(right.plane[2]) |
                        static_cast<uintptr_t>(left.pitch) | static_cast<uintptr_t>(right.pitch)) & 3) == 0;
     if (cols && !backward && left.mask_bits && right.mask_bits && left.list && right.list &&
-        vec == 2 && ((ana && aligned) || six)) {
+        vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 <= kMax) {
         void (*qk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
                    const int4*, EyeOut, EyeOut) = ana ? k_dibr_quad<0> : k_dibr_quad<1>;
         static bool qconf[64] = {false};
@@ -609,7 +609,6 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
             qconf[dev] = true;
         }
         const size_t qsmem = static_cast<size_t>(wpad) * 13;
-        if (qsmem > kMax) return cudaErrorInvalidValue;
         int qper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, qk, 256, qsmem);
         if (qper < 1) qper = 1;
@@ -619,7 +618,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
     }
     if (ana && cols && aligned && (backward || (left.mask_bits && right.mask_bits && left.list &&
                                                 right.list)) &&
-        vec != 0) {
+        vec != 0 && static_cast<size_t>(wpad) * (backward ? 7 : 15) + 16 <= kMax) {
         void (*vk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
                    const int4*, EyeOut, EyeOut) = backward ? k_dibr_ana<true> : k_dibr_ana<false>;
         static bool vconf[64] = {false};
@@ -629,7 +628,6 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
             vconf[dev] = true;
         }
         const size_t vsmem = static_cast<size_t>(wpad) * (backward ? 7 : 15) + 16;
-        if (vsmem > kMax) return cudaErrorInvalidValue;
         int vper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, vk, 256, vsmem);
         if (vper < 1) vper = 1;

@@ -86,6 +86,10 @@ struct EyeOut {
 // x + sigma; see engine.cpp). cols (optional, 256 int4): the host-verified integer column
 // tables (engine.cpp dibr_col_table); when given, no FP64 runs on the device.
 // backward = cfg.dibr_mode == kBackwardFallback.
+// A DIBR row lives in one CTA's shared memory (12 bytes per pixel for the general kernel):
+// frames wider than dibr_max_width() are rejected at plan creation.
+constexpr size_t kDibrMaxSmem = 220 * 1024;  // + the kernels' static tables <= 227 KB
+inline int dibr_max_width() { return static_cast<int>(kDibrMaxSmem / 12) & ~15; }
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
                  EyeOut right, cudaStream_t st);

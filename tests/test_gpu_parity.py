@@ -308,3 +308,16 @@ def test_certified_bilateral_radii(p3s, checker, sigma_s):
     a partial last tile row)."""
     img = checker.synthetic_frame(333, 277, int(sigma_s * 10))
     compare_convert(p3s, checker, img, dict(sigma_spatial=sigma_s, sigma_range=float(6 + sigma_s)))
+
+
+def test_widest_supported_rows(p3s, checker):
+    """A DIBR row lives in one CTA's shared memory: the widest supported frame (18768 px)
+    converts bit-exactly in every route; one column more is rejected with INVALID and a
+    message (never a silent wrong result)."""
+    wmax = 18768
+    img = checker.synthetic_frame(wmax, 6, 5)
+    compare_convert(p3s, checker, img, dict(formats=7, base=60))
+    compare_convert(p3s, checker, img, dict(formats=1))
+    with pytest.raises(p3s.P3SError) as e:
+        p3s.convert(np.zeros((3, 2, wmax + 16), np.uint8), p3s.Config())
+    assert e.value.status == 1 and "exceeds the GPU DIBR row limit" in e.value.message
