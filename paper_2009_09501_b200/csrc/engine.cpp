@@ -47,6 +47,24 @@ void record_event(cudaEvent_t e, cudaStream_t st) {
         check(cudaEventRecord(e, st), "cudaEventRecord");
 }
 
+// Waits for an event recorded outside the stream's capture (an external event-wait node
+// while capturing, a plain wait otherwise).
+void wait_event_any(cudaStream_t st, cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    check(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+    check(cudaStreamWaitEvent(st, e, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0),
+          "cudaStreamWaitEvent");
+}
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 // ---- exact host tables --------------------------------------------------------------------
 
 // bilateral.cpp:22-35: radius ceil(2 sigma_s); spatial exp(-(dx^2+dy^2) * inv_s) with the
@@ -228,7 +246,7 @@ struct Pipeline::Impl {
     unsigned char* ipa = nullptr;  // inpaint arena (state words + tile flags)
     uint32_t* counts = nullptr;  // 2
     uint32_t* bil_list = nullptr;   // bilateral fast path: uncertified pixels (N)
-    uint32_t* bil_count = nullptr;  // 1
+    uint32_t* bil_count = nullptr;  // 4: count, tile-claim counters of the bilateral launches
     uint32_t* ctl = nullptr;     // 128
     long long* stats = nullptr;  // 6
     // stage-API extras (allocated on first use)
@@ -247,6 +265,17 @@ struct Pipeline::Impl {
     long long acc_n = 0;
     long long acc_bil_ns = 0, acc_bil_n = 0;  // main bilateral kernel (without the fix-up)
     bool own_stream = false;
+
+    // Row-banded synchronous conversion (convert_image on pinned host planes): the upload is
+    // split at row in_rows_a; band A (depth tile rows [0, dtile_a), block rows [0, brow_a),
+    // depth rows [0, urow_a), bilateral tile rows [0, btile_a)) computes while the rest of the
+    // frame is still crossing PCIe; band B (the remainder) runs on a second stream so its
+    // bilateral CTAs fill the SMs as band A's retire. Same kernels, same bytes.
+    bool band_ok = false;
+    int in_rows_a = 0, dtile_a = 0, brow_a = 0, urow_a = 0, btile_a = 0;
+    cudaStream_t band_stream = nullptr, h2d_stream = nullptr;
+    std::array<cudaEvent_t, 5> band_ev{};  // 0, 1: upload parts done; 2: fork; 3: join; 4: prior work
+    cudaGraphExec_t band_exec = nullptr;
 
     std::size_t plane() const { return static_cast<std::size_t>(pitch) * h; }
     std::size_t npix() const { return static_cast<std::size_t>(w) * h; }
@@ -278,6 +307,7 @@ struct Pipeline::Impl {
         std::vector<double> cf, rf;
         locate_axis(w, bx, blk, ci0, ci1, cf);
         locate_axis(h, by, blk, ri0, ri1, rf);
+        plan_bands(ri1, by, blk);
         h_spatial = spatial_table(cfg, radius);
         double h_range[256], h_shift[256];
         range_table(cfg, h_range);
@@ -311,7 +341,7 @@ struct Pipeline::Impl {
         const std::size_t o_lists = a.take<uint32_t>(backward ? 0 : 2 * N);
         const std::size_t o_ipa = a.take<unsigned char>(backward ? 0 : cu::inpaint_scratch_bytes(w, h));
         const std::size_t o_cnt = a.take<uint32_t>(2);
-        const std::size_t o_bil = a.take<uint32_t>(N + 1);
+        const std::size_t o_bil = a.take<uint32_t>(N + 4);
         const std::size_t o_ctl = a.take<uint32_t>(128);
         const std::size_t o_stats = a.take<long long>(6);
         arena_bytes = a.off;
@@ -341,7 +371,7 @@ struct Pipeline::Impl {
         }
         counts = reinterpret_cast<uint32_t*>(arena + o_cnt);
         bil_count = reinterpret_cast<uint32_t*>(arena + o_bil);
-        bil_list = bil_count + 1;
+        bil_list = bil_count + 4;
         ctl = reinterpret_cast<uint32_t*>(arena + o_ctl);
         stats = reinterpret_cast<long long*>(arena + o_stats);
 
@@ -375,8 +405,45 @@ struct Pipeline::Impl {
         dt.row_denom = h > 1 ? h - 1 : 1;
     }
 
+    void plan_bands(const std::vector<int>& ri1, int by, int blk) {
+        band_ok = false;
+        const char* env = std::getenv("P3S_BANDED");
+        if (env && std::atoi(env) == 0) return;
+        if (!cu::bilateral_fast_available(radius)) return;
+        const int TYb = cu::bilateral_sep_tile_rows(), TD = cu::depth_tile_rows();
+        const int tiles_y = (h + TYb - 1) / TYb;
+        // band A's bilateral should last about as long as the rest of the upload
+        // (PCIe ~54 GB/s vs the filter's ~0.17 ns/px at r = 16): ~1/4 of the rows
+        const char* fr = std::getenv("P3S_BAND_FRAC");
+        const double frac = fr ? std::atof(fr) : 0.24;
+        const int a = static_cast<int>(std::lround(tiles_y * frac));
+        if (a < 1 || a >= tiles_y) return;
+        const int need = a * TYb + radius;  // depth / luma rows band A's filter reads
+        if (need >= h) return;
+        // fewest block rows whose upsampled rows (ri1[y] < brow) cover [0, need)
+        int b = 1;
+        auto urows = [&](int bb) {
+            return static_cast<int>(std::lower_bound(ri1.begin(), ri1.end(), bb) - ri1.begin());
+        };
+        while (b < by && urows(b) < need) ++b;
+        if (b >= by) return;
+        const int dt_a = (b * blk + TD - 1) / TD;  // depth tile rows completing block rows < b
+        if (dt_a * TD >= h) return;
+        btile_a = a;
+        brow_a = b;
+        urow_a = urows(b);
+        dtile_a = dt_a;
+        in_rows_a = std::min(h, dt_a * TD + 1);  // + the Sobel row below
+        band_ok = true;
+    }
+
     ~Impl() {
         cudaSetDevice(dev);
+        if (band_exec) cudaGraphExecDestroy(band_exec);
+        for (auto& e : band_ev)
+            if (e) cudaEventDestroy(e);
+        if (band_stream) cudaStreamDestroy(band_stream);
+        if (h2d_stream) cudaStreamDestroy(h2d_stream);
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
         for (auto& g : timed_graphs) cudaGraphExecDestroy(g.exec);
         for (auto& e : conv_ev)
@@ -660,6 +727,104 @@ struct Pipeline::Impl {
         if (ev) record_event((*ev)[4], st);
         enq_formats(st);
         if (ev) record_event((*ev)[5], st);
+    }
+
+    void ensure_band_resources() {
+        if (band_stream) return;
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&band_stream, cudaStreamNonBlocking, hi));
+        CK(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
+        for (auto& e : band_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        if (!conv_ev[0])
+            for (auto& e : conv_ev) CK(cudaEventCreate(&e));
+    }
+
+    // Host planes -> src in two row parts on h2d_stream (band_ev[0], band_ev[1]).
+    void upload_banded(const ImageRGB8& img, cudaStream_t st) {
+        CK(cudaEventRecord(band_ev[4], st));  // earlier work on st (reads src) comes first
+        CK(cudaStreamWaitEvent(h2d_stream, band_ev[4], 0));
+        for (int part = 0; part < 2; ++part) {
+            const int r0 = part ? in_rows_a : 0, r1 = part ? h : in_rows_a;
+            for (int c = 0; c < 3; ++c)
+                CK(cudaMemcpy2DAsync(src + c * plane() + static_cast<std::size_t>(r0) * pitch, pitch,
+                                     img.plane(c).data() + static_cast<std::size_t>(r0) * w, w, w,
+                                     r1 - r0, cudaMemcpyHostToDevice, h2d_stream));
+            CK(cudaEventRecord(band_ev[part], h2d_stream));
+        }
+    }
+
+    void enqueue_banded(cudaStream_t st, const std::array<cudaEvent_t, 7>& ev) {
+        const uint8_t* s = src;
+        cudaStream_t sb = band_stream;
+        wait_event_any(st, band_ev[0]);
+        record_event(ev[0], st);
+        CK(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * dt.bx * dt.by, st));
+        CK(cudaMemsetAsync(bil_count, 0, 4 * sizeof(uint32_t), st));
+        CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
+                           dt.block, dt.bx, st, 0, dtile_a));
+        CK(cu::block_values(sums, gm, dt, values, st, 0, brow_a));
+        CK(cu::upsample(values, gm, dt, depth, st, 0, urow_a));
+        record_event(ev[1], st);
+        CK(cudaEventRecord(band_ev[2], st));  // fork
+        CK(cudaStreamWaitEvent(sb, band_ev[2], 0));
+        CK(cu::bilateral_sep_main(depth, luma, gm, radius, h_spatial.data(), range, filt, bil_list,
+                                  bil_count, bil_count + 1, 0, btile_a, st));
+        wait_event_any(sb, band_ev[1]);
+        CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
+                           dt.block, dt.bx, sb, dtile_a, -1));
+        CK(cu::block_values(sums, gm, dt, values, sb, brow_a, -1));
+        CK(cu::upsample(values, gm, dt, depth, sb, urow_a, -1));
+        CK(cu::bilateral_sep_main(depth, luma, gm, radius, h_spatial.data(), range, filt, bil_list,
+                                  bil_count, bil_count + 2, btile_a, -1, sb));
+        CK(cudaEventRecord(band_ev[3], sb));  // join
+        CK(cudaStreamWaitEvent(st, band_ev[3], 0));
+        record_event(ev[6], st);
+        CK(cu::bilateral_sep_fixup(depth, luma, gm, radius, spatial, range, filt, bil_list, bil_count,
+                                   st));
+        record_event(ev[2], st);
+        enq_dibr_inpaint(s, st, ev[3]);
+        record_event(ev[4], st);
+        enq_formats(st);
+        record_event(ev[5], st);
+    }
+
+    // convert_image's frame: upload + run, banded when the plan and the host planes allow.
+    void upload_run_conv(const ImageRGB8& img, cudaStream_t st) {
+        bool pinned = band_ok;
+        for (int c = 0; c < 3 && pinned; ++c) pinned = host_pinned(img.plane(c).data());
+        if (!pinned) {
+            for (int c = 0; c < 3; ++c) h2d_plane(src + c * plane(), img.plane(c).data(), st);
+            run_conv(src, st);
+            return;
+        }
+        if ((formats & kFormatHsbs) && (w % 2 != 0))
+            throw std::invalid_argument("side_by_side: half mode requires an even width");
+        ensure_band_resources();
+        upload_banded(img, st);
+        last_conv = true;
+        if (!graphs_enabled()) {
+            enqueue_banded(st, conv_ev);
+            return;
+        }
+        if (!band_exec) {
+            CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_banded(stream, conv_ev);
+            } catch (...) {
+                cudaGraph_t g = nullptr;
+                cudaStreamEndCapture(stream, &g);
+                if (g) cudaGraphDestroy(g);
+                cudaGetLastError();
+                throw;
+            }
+            cudaGraph_t g = nullptr;
+            CK(cudaStreamEndCapture(stream, &g));
+            const cudaError_t e = cudaGraphInstantiate(&band_exec, g, 0);
+            cudaGraphDestroy(g);
+            CK(e);
+        }
+        CK(cudaGraphLaunch(band_exec, st));
     }
 
     StageTimings timings() {
@@ -1239,8 +1404,7 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
     cfg.validate();
     auto p = stage_plan(dev, src.width, src.height, cfg);
     cudaStream_t st = p->stream;
-    upload_image(*p, src, st);
-    p->run_conv(p->src, st);
+    p->upload_run_conv(src, st);
     const std::size_t n = p->npix();
     uint8_t* buf = static_cast<uint8_t*>(map_pool().take(dev.ordinal(), 2 * n));
     try {
@@ -1271,8 +1435,7 @@ ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg
     cfg.validate();
     auto p = stage_plan(dev, src.width, src.height, cfg);
     cudaStream_t st = p->stream;
-    upload_image(*p, src, st);
-    p->run_conv(p->src, st);
+    p->upload_run_conv(src, st);
     ConversionResult res;
     p->download_overlapped(res, st, dev.impl().copy_stream);
     res.timings = p->timings();

@@ -471,7 +471,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     const __grid_constant__ SepParam<R, P> sp, const uint8_t* __restrict__ depth,
     const uint8_t* __restrict__ guide, int pitch, int w, int h,
     const double* __restrict__ range_g, uint8_t* __restrict__ out, uint32_t* __restrict__ list,
-    uint32_t* __restrict__ count, int tiles_x, int ntiles) {
+    uint32_t* __restrict__ count, int tiles_x, int tile_begin, int tile_end,
+    uint32_t* __restrict__ tile_ctr) {
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R;
     constexpr int SH = TY + 2 * R;
@@ -511,12 +512,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
         }
         cp_async_commit();
     };
-    if (blockIdx.x < ntiles) prefetch(blockIdx.x);
+    // tiles [tile_begin, tile_end): the first one per CTA is blockIdx-based, the rest are
+    // claimed from tile_ctr (dynamic: CTAs that start late, e.g. behind another launch's
+    // tail, simply take fewer tiles)
+    __shared__ int s_next;
+    int tile = tile_begin + static_cast<int>(blockIdx.x);
+    if (tile < tile_end) prefetch(tile);
 
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    while (tile < tile_end) {
         const int tx0 = (tile % tiles_x) * kTX;
         const int ty0 = (tile / tiles_x) * TY;
         cp_async_wait_all();
+        if (threadIdx.x == 0)
+            s_next = tile_begin + static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(tile_ctr, 1u));
         __syncthreads();  // raw bytes of this tile landed; the previous tile's compute is done
         for (int e = threadIdx.x; e < SH * SW; e += blockDim.x) {
             const int sy = e / SW, sx = e - sy * SW;
@@ -529,7 +537,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
             s_tile[e] = v;
         }
         __syncthreads();
-        if (tile + static_cast<int>(gridDim.x) < ntiles) prefetch(tile + gridDim.x);
+        const int next = s_next;
+        if (next < tile_end) prefetch(next);
+        tile = next;
 
         const int x = tx0 + lane;
         const int yb = ty0 + warp * P;
@@ -793,10 +803,10 @@ cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
 }
 
 template <int R, int P, int NW, int U = 4>
-cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
-                       const double* spatial_host, const double* spatial_dev, const double* range,
-                       uint8_t* out, uint32_t* list, uint32_t* count, cudaStream_t st,
-                       cudaEvent_t after_main) {
+cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
+                            const double* spatial_host, const double* range, uint8_t* out,
+                            uint32_t* list, uint32_t* count, uint32_t* tile_ctr, int tr0, int tr1,
+                            cudaStream_t st) {
     SepParam<R, P> sp;
     // sx(d) = exp(-(d*d) * inv_s): the dy = 0 row of the host spatial table (same formula)
     const double* row0 = spatial_host + static_cast<size_t>(R) * (R + 1);
@@ -826,15 +836,19 @@ cudaError_t launch_sep(const uint8_t* depth, const uint8_t* guide, Geom gm,
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     const int tiles_x = (gm.w + kTX - 1) / kTX;
     const int tiles_y = (gm.h + TY - 1) / TY;
-    const int ntiles = tiles_x * tiles_y;
-    const int grid = min(ntiles, per_sm * sm_count());
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
-    if (e != cudaSuccess) return e;
+    if (tr1 < 0 || tr1 > tiles_y) tr1 = tiles_y;
+    if (tr1 <= tr0) return cudaSuccess;
+    const int t0 = tr0 * tiles_x, t1 = tr1 * tiles_x;
+    const int grid = min(t1 - t0, per_sm * sm_count());
     k_bilateral_sep<R, P, NW, U><<<grid, NW * 32, smem, st>>>(
-        sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, ntiles);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (after_main) record_event_any(after_main, st);
+        sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, t0, t1, tile_ctr);
+    return cudaGetLastError();
+}
+
+template <int R>
+cudaError_t launch_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm,
+                             const double* spatial_dev, const double* range, uint8_t* out,
+                             const uint32_t* list, const uint32_t* count, cudaStream_t st) {
     // 4 warps per block up to R = 16 (static smem < 48 KB), 2 beyond
     constexpr int WPB = R <= 16 ? 4 : 2;
     k_bilateral_fixup2<R, WPB><<<sm_count() * 32 / WPB, WPB * 32, 0, st>>>(
@@ -848,12 +862,31 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
                            const double* spatial_host, const double* spatial_dev,
                            const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
                            cudaStream_t st, cudaEvent_t after_main) {
-    // the certified kernel for radii 7..24 (sigma_s in (3, 12]); P = 8 outputs per thread,
-    // 16 warps, the dx loop fully unrolled
+    if (!bilateral_fast_available(radius)) {
+        const cudaError_t e = bilateral_tiled(depth, guide, gm, radius, spatial_host, range, out, nullptr, st);
+        if (after_main) record_event_any(after_main, st);
+        return e;
+    }
+    // count and the tile-claim counter (count[1]) start at zero
+    cudaError_t e = cudaMemsetAsync(count, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    e = bilateral_sep_main(depth, guide, gm, radius, spatial_host, range, out, list, count,
+                           count + 1, 0, -1, st);
+    if (e != cudaSuccess) return e;
+    if (after_main) record_event_any(after_main, st);
+    return bilateral_sep_fixup(depth, guide, gm, radius, spatial_dev, range, out, list, count, st);
+}
+
+// the certified kernel for radii 7..24 (sigma_s in (3, 12]); P = 8 outputs per thread,
+// 16 warps, the dx loop fully unrolled
+cudaError_t bilateral_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                               const double* spatial_host, const double* range, uint8_t* out,
+                               uint32_t* list, uint32_t* count, uint32_t* tile_ctr,
+                               int tile_row0, int tile_row1, cudaStream_t st) {
 #define P3S_SEP(RR)                                                                          \
     case RR:                                                                                 \
-        return launch_sep<RR, 8, 16, RR>(depth, guide, gm, spatial_host, spatial_dev, range,  \
-                                         out, list, count, st, after_main);
+        return launch_sep_main<RR, 8, 16, RR>(depth, guide, gm, spatial_host, range, out,    \
+                                              list, count, tile_ctr, tile_row0, tile_row1, st);
     switch (radius) {
         P3S_SEP(7) P3S_SEP(8) P3S_SEP(9) P3S_SEP(10) P3S_SEP(11) P3S_SEP(12) P3S_SEP(13)
         P3S_SEP(14) P3S_SEP(15) P3S_SEP(16) P3S_SEP(17) P3S_SEP(18) P3S_SEP(19) P3S_SEP(20)
@@ -861,10 +894,26 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
         default: break;
     }
 #undef P3S_SEP
-    const cudaError_t e = bilateral_tiled(depth, guide, gm, radius, spatial_host, range, out, nullptr, st);
-    if (after_main) record_event_any(after_main, st);
-    return e;
+    return cudaErrorInvalidValue;
 }
+
+cudaError_t bilateral_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                                const double* spatial_dev, const double* range, uint8_t* out,
+                                const uint32_t* list, const uint32_t* count, cudaStream_t st) {
+#define P3S_FIX(RR)                                                                          \
+    case RR:                                                                                 \
+        return launch_sep_fixup<RR>(depth, guide, gm, spatial_dev, range, out, list, count, st);
+    switch (radius) {
+        P3S_FIX(7) P3S_FIX(8) P3S_FIX(9) P3S_FIX(10) P3S_FIX(11) P3S_FIX(12) P3S_FIX(13)
+        P3S_FIX(14) P3S_FIX(15) P3S_FIX(16) P3S_FIX(17) P3S_FIX(18) P3S_FIX(19) P3S_FIX(20)
+        P3S_FIX(21) P3S_FIX(22) P3S_FIX(23) P3S_FIX(24)
+        default: break;
+    }
+#undef P3S_FIX
+    return cudaErrorInvalidValue;
+}
+
+int bilateral_sep_tile_rows() { return 16 * 8; }
 
 bool bilateral_fast_available(int radius) {
     const char* v = getenv("P3S_BIL_FAST");

@@ -32,12 +32,12 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
                                                      const uint8_t* __restrict__ B, int pitch,
                                                      int w, int h, uint8_t* __restrict__ luma,
                                                      unsigned long long* __restrict__ sums,
-                                                     int block, int bx_total) {
+                                                     int block, int bx_total, int tile_row0) {
     __shared__ uint8_t s_y[kTH + 2][kSW];
     __shared__ unsigned s_sum[kMaxBY][kMaxBX];
 
     const int x0 = blockIdx.x * kTW;
-    const int y0 = blockIdx.y * kTH;
+    const int y0 = (tile_row0 + blockIdx.y) * kTH;
     const int tid = threadIdx.x;
     for (int i = tid; i < kMaxBY * kMaxBX; i += blockDim.x) (&s_sum[0][0])[i] = 0u;
 
@@ -145,9 +145,9 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
 // depth.cpp:55-71: value = (alpha*255.0) * (centre/row_denom) + beta * (sum / count).
 __global__ void k_block_values(const unsigned long long* __restrict__ sums, int w, int h,
                                int block, int bx, int by, double alpha255, double beta,
-                               double row_denom, double* __restrict__ values) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= bx * by) return;
+                               double row_denom, double* __restrict__ values, int i0, int i1) {
+    const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= i1) return;
     const int iy = i / bx, ix = i % bx;
     const int y0 = iy * block, y1 = min(y0 + block, h);
     const int xa = ix * block, xb = min(xa + block, w);
@@ -186,9 +186,9 @@ __global__ void __launch_bounds__(kUpThreads) k_upsample(const double* __restric
                                                          const int* __restrict__ ri1,
                                                          const double* __restrict__ rf, int w,
                                                          int h, int pitch,
-                                                         uint8_t* __restrict__ depth) {
+                                                         uint8_t* __restrict__ depth, int ya, int yb) {
     const int x0 = (blockIdx.x * kUpThreads + threadIdx.x) * kUpCols;
-    const int y0 = blockIdx.y * kUpRows;
+    const int y0 = ya + blockIdx.y * kUpRows;
     if (x0 >= w) return;
     int a[kUpCols], b[kUpCols];
     double fx[kUpCols];
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kUpThreads) k_upsample(const double* __restric
     }
     int cur0 = -1, cur1 = -1;
     double top[kUpCols], bot[kUpCols];
-    const int y1 = min(y0 + kUpRows, h);
+    const int y1 = min(y0 + kUpRows, yb);
     for (int y = y0; y < y1; ++y) {
         const int i0 = __ldg(ri0 + y), i1 = __ldg(ri1 + y);
         if (i0 != cur0 || i1 != cur1) {
@@ -233,28 +233,39 @@ __global__ void __launch_bounds__(kUpThreads) k_upsample(const double* __restric
 
 cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
                         uint8_t* luma, unsigned long long* sums, int block, int bx,
-                        cudaStream_t st) {
-    dim3 grid((gm.w + kTW - 1) / kTW, (gm.h + kTH - 1) / kTH);
-    k_depth_front<<<grid, 256, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, sums, block, bx);
+                        cudaStream_t st, int tile_row0, int tile_row1) {
+    const int rows = (gm.h + kTH - 1) / kTH;
+    if (tile_row1 < 0 || tile_row1 > rows) tile_row1 = rows;
+    if (tile_row1 <= tile_row0) return cudaSuccess;
+    dim3 grid((gm.w + kTW - 1) / kTW, tile_row1 - tile_row0);
+    k_depth_front<<<grid, 256, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, sums, block, bx,
+                                        tile_row0);
     return cudaGetLastError();
 }
 
 cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTables& t,
-                         double* values, cudaStream_t st) {
-    const int n = t.bx * t.by;
-    k_block_values<<<(n + 255) / 256, 256, 0, st>>>(sums, gm.w, gm.h, t.block, t.bx, t.by,
-                                                    t.alpha255, t.beta, t.row_denom, values);
+                         double* values, cudaStream_t st, int brow0, int brow1) {
+    if (brow1 < 0 || brow1 > t.by) brow1 = t.by;
+    const int i0 = brow0 * t.bx, i1 = brow1 * t.bx;
+    if (i1 <= i0) return cudaSuccess;
+    k_block_values<<<(i1 - i0 + 255) / 256, 256, 0, st>>>(sums, gm.w, gm.h, t.block, t.bx, t.by,
+                                                          t.alpha255, t.beta, t.row_denom, values,
+                                                          i0, i1);
     return cudaGetLastError();
 }
 
 cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_t* depth,
-                     cudaStream_t st) {
+                     cudaStream_t st, int ya, int yb) {
+    if (yb < 0 || yb > gm.h) yb = gm.h;
+    if (yb <= ya) return cudaSuccess;
     dim3 grid((gm.w + kUpThreads * kUpCols - 1) / (kUpThreads * kUpCols),
-              (gm.h + kUpRows - 1) / kUpRows);
+              (yb - ya + kUpRows - 1) / kUpRows);
     k_upsample<<<grid, kUpThreads, 0, st>>>(values, t.bx, t.col_i0, t.col_i1, t.col_f, t.row_i0,
-                                            t.row_i1, t.row_f, gm.w, gm.h, gm.pitch, depth);
+                                            t.row_i1, t.row_f, gm.w, gm.h, gm.pitch, depth, ya, yb);
     return cudaGetLastError();
 }
+
+int depth_tile_rows() { return kTH; }
 
 }  // namespace cu
 }  // namespace p3s

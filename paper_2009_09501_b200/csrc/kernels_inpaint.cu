@@ -280,6 +280,112 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
     __syncwarp();
 }
 
+// Round-0 version of process_tile for heavy tiles: the whole CTA (kThreads threads) works
+// on one region (warp 0's shared-memory slot), so the per-pass colour and publish work of a
+// dense hole strip is spread over 8 warps instead of 1. Same simulation, same results; only
+// the thread mapping differs (region rows on threads 0..63, the repair list on all threads).
+__device__ void process_tile_cta(const Eye& E, int tx, int ty, int w, int h, WarpSmem& S,
+                                 uint32_t* counts_slot, bool& remains) {
+    const InpaintEye& io = E.io;
+    const int tid = threadIdx.x;
+    const int x0 = tx * kT - kPasses, y0 = ty * kT - kPasses;
+    const unsigned long long kInner = 0x0000FFFFFFFF0000ull;  // interior columns 16..47
+    // double-buffered pass counters: buffer k & 1 is reset during pass k - 1
+    __shared__ int s_total[2], s_inner[2];
+    const bool rowt = tid < kE;
+    const bool inner_row = tid >= kPasses && tid < kPasses + kT;
+    if (tid == 0) {
+        s_total[1] = 0;
+        s_inner[1] = 0;
+    }
+    unsigned long long d = 0, img = 0;
+    if (rowt) {
+        const int gy = y0 + tid;
+        unsigned long long in = 0, m = 0;
+        if (gy >= 0 && gy < h) m = row_bits(io, x0, gy, w, in);
+        d = m;
+        img = in;
+        S.dmg[tid] = m;
+        S.img[tid] = in;
+    }
+    __syncthreads();
+    if (rowt) {
+        const int r = tid, gy = y0 + r;
+        const unsigned long long near = d | (r > 0 ? S.dmg[r - 1] : 0) | (r + 1 < kE ? S.dmg[r + 1] : 0);
+        if (near && gy >= 0 && gy < h) load_row(io, S, r, gy, x0, w);
+    }
+    __syncthreads();
+    for (int k = 1; k <= kPasses; ++k) {
+        const int b = k & 1;
+        unsigned long long rep = 0;
+        if (rowt) {
+            const int r = tid;
+            const unsigned long long iu = r > 0 ? S.img[r - 1] & ~S.dmg[r - 1] : 0ull;
+            const unsigned long long id = r + 1 < kE ? S.img[r + 1] & ~S.dmg[r + 1] : 0ull;
+            rep = d & two_plus(iu, img & ~d, id);
+            const int cnt = __popcll(rep);
+            if (cnt) {
+                int pos = atomicAdd(&s_total[b], cnt);  // list order is irrelevant (Jacobi pass)
+                for (unsigned long long q = rep; q; q &= q - 1)
+                    S.rep[pos++] = static_cast<uint16_t>((r << 6) | (__ffsll(static_cast<long long>(q)) - 1));
+                if (inner_row && (rep & kInner)) atomicAdd(&s_inner[b], __popcll(rep & kInner));
+            }
+        }
+        if (!__syncthreads_or(rep != 0)) break;  // fixed point of the region
+        const int total = s_total[b];
+        if (tid == 0) {
+            s_total[b ^ 1] = 0;
+            s_inner[b ^ 1] = 0;
+        }
+        for (int i = tid; i < total; i += blockDim.x) {
+            const int e = S.rep[i], r = e >> 6, c = e & 63;
+            const unsigned long long iw[3] = {r > 0 ? S.img[r - 1] & ~S.dmg[r - 1] : 0ull,
+                                              S.img[r] & ~S.dmg[r],
+                                              r + 1 < kE ? S.img[r + 1] & ~S.dmg[r + 1] : 0ull};
+            unsigned cntn = 0, a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (!dx && !dy) continue;
+                    const int cc = c + dx;
+                    if (cc < 0 || cc >= kE || !((iw[dy + 1] >> cc) & 1ull)) continue;
+                    ++cntn;
+                    if (io.plane[0]) a0 += S.col[0][r + dy][cc];
+                    if (io.plane[1]) a1 += S.col[1][r + dy][cc];
+                    if (io.plane[2]) a2 += S.col[2][r + dy][cc];
+                }
+            }
+            if (io.plane[0]) S.col[0][r][c] = static_cast<uint8_t>((2 * a0 + cntn) / (2 * cntn));
+            if (io.plane[1]) S.col[1][r][c] = static_cast<uint8_t>((2 * a1 + cntn) / (2 * cntn));
+            if (io.plane[2]) S.col[2][r][c] = static_cast<uint8_t>((2 * a2 + cntn) / (2 * cntn));
+        }
+        __syncthreads();
+        for (int i = tid; i < total; i += blockDim.x) {
+            const int e = S.rep[i], r = e >> 6, c = e & 63;
+            if (r < kPasses || r >= kPasses + kT || c < kPasses || c >= kPasses + kT) continue;
+            const int gy = y0 + r, gx = x0 + c;
+            const uint8_t c0 = S.col[0][r][c], c1 = S.col[1][r][c], c2 = S.col[2][r][c];
+            const unsigned long long g = static_cast<unsigned long long>(k);  // round 0: pass0 = 0
+            E.state[static_cast<size_t>(gy) * w + gx] =
+                kRepaired | (g << 24) | (static_cast<unsigned long long>(c2) << 16) |
+                (static_cast<unsigned long long>(c1) << 8) | c0;
+            const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
+            if (io.plane[0]) io.plane[0][o] = c0;
+            if (io.plane[1]) io.plane[1][o] = c1;
+            if (io.plane[2]) io.plane[2][o] = c2;
+        }
+        if (tid == 0 && s_inner[b]) atomicAdd(&counts_slot[k], static_cast<uint32_t>(s_inner[b]));
+        if (rowt) {
+            d &= ~rep;
+            S.dmg[tid] = d;
+        }
+        // interior complete: later passes add no interior repairs (see process_tile)
+        if (!__syncthreads_or(inner_row && (d & kInner))) break;
+    }
+    remains = __syncthreads_or(inner_row && (d & kInner)) != 0;
+}
+
 // Debug timeline (P3S_DEBUG_INPAINT): per warp, globaltimer ns at the phase boundaries of
 // round 0 plus tile statistics. nullptr in normal runs.
 __device__ unsigned long long* g_inp_dbg = nullptr;
@@ -347,19 +453,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
         const uint32_t nheavy = round == 0 ? __ldcg(&wk.counters[6]) : 0u;
         const uint32_t* list = wk.lists + static_cast<size_t>(slot) * wk.cap;
         uint32_t* next = wk.lists + static_cast<size_t>(nslot) * wk.cap;
+        if (round == 0) {
+            // heavy tiles first, one whole CTA per tile (counters[7] = CTA claim index)
+            __shared__ uint32_t s_claim;
+            WarpSmem& S0 = reinterpret_cast<WarpSmem*>(smem_raw)[0];
+            for (;;) {
+                if (threadIdx.x == 0) s_claim = atomicAdd(&wk.counters[7], 1u);
+                __syncthreads();
+                const uint32_t i = s_claim;
+                __syncthreads();
+                if (i >= nheavy) break;
+                const uint32_t item = __ldcg(wk.heavy + i);
+                const int e = static_cast<int>(item) / ntiles, t = static_cast<int>(item) - e * ntiles;
+                if (done[e]) continue;
+                bool remains = false;
+                const unsigned long long tt0 = dbg ? gtimer() : 0;
+                process_tile_cta(e ? R : L, t % tiles_x, t / tiles_x, w, h, S0,
+                                 ctl + (e * 3 + slot) * (kPasses + 1), remains);
+                if (dbg && (threadIdx.x & 31) == 0) {
+                    const unsigned long long dd = gtimer() - tt0;
+                    dt[5] += 1;
+                    dt[6] += dd;
+                    dt[7] = dd > dt[7] ? dd : dt[7];
+                }
+                if (remains && threadIdx.x == 0) {
+                    const uint32_t pos = atomicAdd(&wk.counters[2 * nslot], 1u);
+                    next[pos] = item;
+                }
+            }
+        }
         for (;;) {
             // round 0 takes the heavy tiles first (they bound the round), then the rest
             uint32_t i = 0;
             if (lane == 0) i = atomicAdd(&wk.counters[2 * slot + 1], 1u);
             i = __shfl_sync(0xFFFFFFFFu, i, 0);
-            if (i >= nheavy + n) break;
-            uint32_t item;
-            if (i < nheavy) {
-                item = __ldcg(wk.heavy + i);
-            } else {
-                item = __ldcg(list + (i - nheavy));
-                if (round == 0 && __ldcg(wk.init_flags + item) >= kHeavy) continue;  // done above
-            }
+            if (i >= n) break;
+            const uint32_t item = __ldcg(list + i);
+            if (round == 0 && __ldcg(wk.init_flags + item) >= kHeavy) continue;  // done by a CTA
             const int e = static_cast<int>(item) / ntiles, t = static_cast<int>(item) - e * ntiles;
             if (done[e]) continue;
             bool remains = false;

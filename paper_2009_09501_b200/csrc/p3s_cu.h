@@ -35,16 +35,19 @@ struct DepthTables {
 };
 
 // K1: luma plane + per-block Sobel-magnitude sums (image.cpp:13-21, depth.cpp:21-74).
-// sums must be zeroed (bx*by u64) before the call.
+// sums must be zeroed (bx*by u64) before the call. Optional row band: tiles of
+// depth_tile_rows() image rows [tile_row0, tile_row1) (-1: to the end); the block sums of
+// a block row are complete once every tile row covering it has run.
 cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
                         uint8_t* luma, unsigned long long* sums, int block, int bx,
-                        cudaStream_t st);
-// Block values (depth.cpp:55-71) from the sums.
+                        cudaStream_t st, int tile_row0 = 0, int tile_row1 = -1);
+int depth_tile_rows();
+// Block values (depth.cpp:55-71) from the sums, block rows [brow0, brow1).
 cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTables& t,
-                         double* values, cudaStream_t st);
-// Bilinear upsample to the u8 depth map (depth.cpp:104-120).
+                         double* values, cudaStream_t st, int brow0 = 0, int brow1 = -1);
+// Bilinear upsample to the u8 depth map (depth.cpp:104-120), image rows [ya, yb).
 cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_t* depth,
-                     cudaStream_t st);
+                     cudaStream_t st, int ya = 0, int yb = -1);
 
 // K2: exact FP64 cross-bilateral (bilateral.cpp:40-116). spatial: (2r+1) x (r+1) doubles,
 // s[(dy+r)*(r+1) + dx] for dx >= 0; range: 256 doubles. raw (optional, w-strided)
@@ -63,6 +66,19 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
                            const double* spatial_host, const double* spatial_dev,
                            const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
                            cudaStream_t st, cudaEvent_t after_main = nullptr);
+// The certified path in parts, for row-banded schedules: bilateral_sep_main runs the FP32
+// kernel over tile rows [tile_row0, tile_row1) of bilateral_sep_tile_rows() image rows
+// (appending to list/count, which the caller zeroes once per frame; tile_ctr: one zeroed
+// u32 per launch for dynamic tile claims); bilateral_sep_fixup then recomputes every listed
+// pixel. Only for radii where bilateral_fast_available().
+cudaError_t bilateral_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                               const double* spatial_host, const double* range, uint8_t* out,
+                               uint32_t* list, uint32_t* count, uint32_t* tile_ctr,
+                               int tile_row0, int tile_row1, cudaStream_t st);
+cudaError_t bilateral_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
+                                const double* spatial_dev, const double* range, uint8_t* out,
+                                const uint32_t* list, const uint32_t* count, cudaStream_t st);
+int bilateral_sep_tile_rows();
 // cudaEventRecord, or an event-record graph node while `st` is being captured.
 void record_event_any(cudaEvent_t e, cudaStream_t st);
 bool bilateral_fast_available(int radius);

@@ -321,3 +321,17 @@ def test_widest_supported_rows(p3s, checker):
     with pytest.raises(p3s.P3SError) as e:
         p3s.convert(np.zeros((3, 2, wmax + 16), np.uint8), p3s.Config())
     assert e.value.status == 1 and "exceeds the GPU DIBR row limit" in e.value.message
+
+
+@pytest.mark.parametrize("w,h,block,sigma_s", [(500, 700, 4, 8.0), (1283, 389, 37, 3.1),
+                                               (640, 1031, 16, 12.0), (900, 600, 64, 5.5),
+                                               (777, 2100, 23, 8.0)])
+def test_banded_convert_boundaries(p3s, checker, w, h, block, sigma_s):
+    """p3s_convert on pinned planes uploads the frame in two row parts and filters band A
+    while band B is still crossing PCIe (engine.cpp plan_bands). The band edges depend on
+    the depth block size, the radius and the height; every split must give the reference's
+    bytes, and consecutive frames through the same captured graph must too."""
+    over = dict(depth_block=block, sigma_spatial=sigma_s, alpha=0.7, beta=0.3,
+                formats=7 if w % 2 == 0 else 5, base=20)
+    for seed in (3, 4):
+        compare_convert(p3s, checker, checker.synthetic_frame(w, h, seed), over)
