@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <deque>
 #include <cmath>
 #include <cstdio>
@@ -239,6 +240,7 @@ struct Pipeline::Impl {
     unsigned long long* sums = nullptr;
     double* values = nullptr;
     double *range = nullptr, *spatial = nullptr, *shift = nullptr;
+    float* sep_table = nullptr;  // the certified bilateral's replicated FP32 range table
     int4* cols = nullptr;  // integer DIBR column tables (nullptr: FP64 device path)
     uint8_t *ana = nullptr, *hsbs = nullptr, *fsbs = nullptr, *eyes = nullptr;
     uint32_t* mbits = nullptr;
@@ -246,7 +248,8 @@ struct Pipeline::Impl {
     unsigned char* ipa = nullptr;  // inpaint arena (state words + tile flags)
     uint32_t* counts = nullptr;  // 2
     uint32_t* bil_list = nullptr;   // bilateral fast path: uncertified pixels (N)
-    uint32_t* bil_count = nullptr;  // 4: count, tile-claim counters of the bilateral launches
+    static constexpr int kBilSlots = 64;  // counters ahead of the list: 2 per band, K <= 32
+    uint32_t* bil_count = nullptr;  // kBilSlots: counts, tile-claim counters of the bilateral launches
     uint32_t* ctl = nullptr;     // 128
     long long* stats = nullptr;  // 6
     // stage-API extras (allocated on first use)
@@ -266,16 +269,35 @@ struct Pipeline::Impl {
     long long acc_bil_ns = 0, acc_bil_n = 0;  // main bilateral kernel (without the fix-up)
     bool own_stream = false;
 
-    // Row-banded synchronous conversion (convert_image on pinned host planes): the upload is
-    // split at row in_rows_a; band A (depth tile rows [0, dtile_a), block rows [0, brow_a),
-    // depth rows [0, urow_a), bilateral tile rows [0, btile_a)) computes while the rest of the
-    // frame is still crossing PCIe; band B (the remainder) runs on a second stream so its
-    // bilateral CTAs fill the SMs as band A's retire. Same kernels, same bytes.
+    // Row-banded synchronous conversion (convert_image on pinned host planes). The frame is
+    // cut into K bands of bilateral tile rows; Band::* are each band's END boundaries in the
+    // units of every stage (upload rows, depth tiles, block rows, depth rows, bilateral tile
+    // rows). The upload goes out in K row parts; a high-priority stream runs the depth stage
+    // part by part as the rows land; each band's filter (+ fix-up, + DIBR on the fused
+    // routes) runs on its own stream, so band k+1's CTAs fill the SMs as band k's retire.
+    // On the fused routes every band's output rows start back over PCIe while later bands
+    // still filter; after the inpaint, only the 32-pixel words that held damage are patched
+    // into the host planes. Same kernels, same bytes.
+    struct Band {
+        int in_rows, dtile, brow, urow, btile;
+    };
+    std::vector<Band> bands;
     bool band_ok = false;
-    int in_rows_a = 0, dtile_a = 0, brow_a = 0, urow_a = 0, btile_a = 0;
-    cudaStream_t band_stream = nullptr, h2d_stream = nullptr;
-    std::array<cudaEvent_t, 5> band_ev{};  // 0, 1: upload parts done; 2: fork; 3: join; 4: prior work
-    cudaGraphExec_t band_exec = nullptr;
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr, depth_stream = nullptr;
+    std::vector<cudaStream_t> band_streams;
+    // per band: upload part landed, depth part done (fork), band done (join), DIBR rows done
+    std::vector<cudaEvent_t> ev_in, ev_fork, ev_join, ev_rows;
+    cudaEvent_t ev_prior = nullptr, ev_d2h = nullptr, ev_start = nullptr;
+    cudaGraphExec_t band_exec = nullptr, band_exec2 = nullptr;  // head, body
+    cudaStream_t aux_stream = nullptr;  // side copies beside the frame's tail
+    cudaEvent_t aux_done = nullptr;
+    cudaStream_t aux() {
+        if (!aux_stream) {
+            CK(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&aux_done, cudaEventDisableTiming));
+        }
+        return aux_stream;
+    }
 
     std::size_t plane() const { return static_cast<std::size_t>(pitch) * h; }
     std::size_t npix() const { return static_cast<std::size_t>(w) * h; }
@@ -332,6 +354,7 @@ struct Pipeline::Impl {
         const std::size_t o_range = a.take<double>(256), o_shift = a.take<double>(256);
         const std::size_t o_cols = a.take<int4>(256);
         const std::size_t o_spat = a.take<double>(h_spatial.size());
+        const std::size_t o_septab = a.take<float>(cu::bilateral_sep_table_bytes() / 4);
         const std::size_t o_ana = (formats & kFormatAnaglyph) ? a.take<uint8_t>(3 * P) : 0;
         const std::size_t o_hsbs = (formats & kFormatHsbs) ? a.take<uint8_t>(3 * P) : 0;
         const std::size_t o_fsbs =
@@ -341,7 +364,7 @@ struct Pipeline::Impl {
         const std::size_t o_lists = a.take<uint32_t>(backward ? 0 : 2 * N);
         const std::size_t o_ipa = a.take<unsigned char>(backward ? 0 : cu::inpaint_scratch_bytes(w, h));
         const std::size_t o_cnt = a.take<uint32_t>(2);
-        const std::size_t o_bil = a.take<uint32_t>(N + 4);
+        const std::size_t o_bil = a.take<uint32_t>(N + kBilSlots);
         const std::size_t o_ctl = a.take<uint32_t>(128);
         const std::size_t o_stats = a.take<long long>(6);
         arena_bytes = a.off;
@@ -360,6 +383,7 @@ struct Pipeline::Impl {
         shift = reinterpret_cast<double*>(arena + o_shift);
         if (int_cols) cols = reinterpret_cast<int4*>(arena + o_cols);
         spatial = reinterpret_cast<double*>(arena + o_spat);
+        sep_table = reinterpret_cast<float*>(arena + o_septab);
         if (formats & kFormatAnaglyph) ana = arena + o_ana;
         if (formats & kFormatHsbs) hsbs = arena + o_hsbs;
         if (formats & kFormatFsbs) fsbs = arena + o_fsbs;
@@ -371,7 +395,7 @@ struct Pipeline::Impl {
         }
         counts = reinterpret_cast<uint32_t*>(arena + o_cnt);
         bil_count = reinterpret_cast<uint32_t*>(arena + o_bil);
-        bil_list = bil_count + 4;
+        bil_list = bil_count + kBilSlots;
         ctl = reinterpret_cast<uint32_t*>(arena + o_ctl);
         stats = reinterpret_cast<long long*>(arena + o_stats);
 
@@ -389,6 +413,7 @@ struct Pipeline::Impl {
         if (int_cols) up(o_cols, cols_buf, sizeof(cols_buf));
         up(o_spat, h_spatial.data(), h_spatial.size() * sizeof(double));
         CK(cudaMemsetAsync(arena + o_stats, 0, 6 * sizeof(long long), stream));
+        CK(cu::build_sep_table(range, sep_table, stream));
         CK(cudaStreamSynchronize(stream));  // host vectors above go out of scope
 
         dt.col_i0 = reinterpret_cast<int*>(arena + o_ci0);
@@ -407,43 +432,66 @@ struct Pipeline::Impl {
 
     void plan_bands(const std::vector<int>& ri1, int by, int blk) {
         band_ok = false;
+        bands.clear();
         const char* env = std::getenv("P3S_BANDED");
         if (env && std::atoi(env) == 0) return;
         if (!cu::bilateral_fast_available(radius)) return;
         const int TYb = cu::bilateral_sep_tile_rows(), TD = cu::depth_tile_rows();
-        const int tiles_y = (h + TYb - 1) / TYb;
-        // band A's bilateral should last about as long as the rest of the upload
-        // (PCIe ~54 GB/s vs the filter's ~0.17 ns/px at r = 16): ~1/4 of the rows
-        const char* fr = std::getenv("P3S_BAND_FRAC");
-        const double frac = fr ? std::atof(fr) : 0.24;
-        const int a = static_cast<int>(std::lround(tiles_y * frac));
-        if (a < 1 || a >= tiles_y) return;
-        const int need = a * TYb + radius;  // depth / luma rows band A's filter reads
-        if (need >= h) return;
-        // fewest block rows whose upsampled rows (ri1[y] < brow) cover [0, need)
-        int b = 1;
+        const int tiles_y = (h + TYb - 1) / TYb, dtiles = (h + TD - 1) / TD;
+        // band ends: a thin first band (short wait for its upload part), then 4 tile rows
+        // per band (the upload of the next band outruns this band's filter ~3x), then
+        // halving bands at the bottom: a band's download (~1/3 of its filter time) must hide
+        // under the next band's filter, and the last one's under the inpaint
+        std::vector<int> ends = {1};
+        const char* be = std::getenv("P3S_BAND_ENDS");  // e.g. "1,4,8,12,14,16" (tuning)
+        if (be) {
+            ends.clear();
+            for (const char* q = be; *q;) {
+                ends.push_back(std::atoi(q));
+                while (*q && *q != ',') ++q;
+                if (*q) ++q;
+            }
+        } else {
+            const int tail_start = tiles_y - 5;  // the last 5 tile rows: 2, 2, 1
+            for (int t = 4; t < tail_start; t += 4) ends.push_back(t);
+            for (int t : {tiles_y - 5, tiles_y - 3, tiles_y - 1})
+                if (t > ends.back()) ends.push_back(t);
+        }
         auto urows = [&](int bb) {
             return static_cast<int>(std::lower_bound(ri1.begin(), ri1.end(), bb) - ri1.begin());
         };
-        while (b < by && urows(b) < need) ++b;
-        if (b >= by) return;
-        const int dt_a = (b * blk + TD - 1) / TD;  // depth tile rows completing block rows < b
-        if (dt_a * TD >= h) return;
-        btile_a = a;
-        brow_a = b;
-        urow_a = urows(b);
-        dtile_a = dt_a;
-        in_rows_a = std::min(h, dt_a * TD + 1);  // + the Sobel row below
+        for (int T : ends) {
+            if (T >= tiles_y) break;
+            const int need = T * TYb + radius;  // depth / luma rows the band's filter reads
+            if (need >= h) break;
+            int b = bands.empty() ? 1 : bands.back().brow;
+            while (b < by && urows(b) < need) ++b;  // fewest block rows whose rows cover it
+            if (b >= by) break;
+            const int dtl = (b * blk + TD - 1) / TD;  // depth tiles completing block rows < b
+            if (dtl * TD >= h) break;
+            bands.push_back(Band{std::min(h, dtl * TD + 1), dtl, b, urows(b), T});
+        }
+        if (bands.empty()) return;
+        while (bands.size() > kBilSlots / 2 - 1) bands.pop_back();
+        bands.push_back(Band{h, dtiles, by, h, tiles_y});
         band_ok = true;
     }
 
     ~Impl() {
         cudaSetDevice(dev);
         if (band_exec) cudaGraphExecDestroy(band_exec);
-        for (auto& e : band_ev)
+        if (band_exec2) cudaGraphExecDestroy(band_exec2);
+        if (aux_stream) cudaStreamDestroy(aux_stream);
+        if (aux_done) cudaEventDestroy(aux_done);
+        for (auto* v : {&ev_in, &ev_fork, &ev_join, &ev_rows})
+            for (auto e : *v)
+                if (e) cudaEventDestroy(e);
+        for (auto e : {ev_prior, ev_d2h, ev_start})
             if (e) cudaEventDestroy(e);
-        if (band_stream) cudaStreamDestroy(band_stream);
-        if (h2d_stream) cudaStreamDestroy(h2d_stream);
+        for (auto s2 : band_streams)
+            if (s2) cudaStreamDestroy(s2);
+        for (auto s2 : {h2d_stream, d2h_stream, depth_stream})
+            if (s2) cudaStreamDestroy(s2);
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
         for (auto& g : timed_graphs) cudaGraphExecDestroy(g.exec);
         for (auto& e : conv_ev)
@@ -492,7 +540,7 @@ struct Pipeline::Impl {
                        cudaStream_t st, cudaEvent_t after_main = nullptr) {
         if (!raw && cu::bilateral_fast_available(radius)) {
             CK(cu::bilateral_fast(dmap, guide, gm, radius, h_spatial.data(), spatial, range, out,
-                                  bil_list, bil_count, st, after_main));
+                                  bil_list, bil_count, st, after_main, sep_table));
             static const bool dbg = std::getenv("P3S_DEBUG_BIL") != nullptr;
             if (dbg) {
                 uint32_t n = 0;
@@ -533,38 +581,13 @@ struct Pipeline::Impl {
     }
 
     void enq_dibr_inpaint(const uint8_t* s, cudaStream_t st, cudaEvent_t mid) {
-        uint8_t *L[3], *R[3];
-        int lp = pitch;
-        eye_planes(L, R, lp);
         cu::EyeOut eo[2];
-        for (int e = 0; e < 2; ++e) {
-            for (int c = 0; c < 3; ++c) eo[e].plane[c] = e ? R[c] : L[c];
-            eo[e].pitch = lp;
-            eo[e].mask_bytes = nullptr;
-            eo[e].mask_bits = backward ? nullptr : mbits + static_cast<std::size_t>(e) * mwords * h;
-            eo[e].mask_pitch = mwords;
-            eo[e].list = backward ? nullptr : list_ptr(e, 0);
-            eo[e].count = counts + e;
-        }
+        dibr_eyes(eo);
         if (!backward) CK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), st));
         CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols, backward,
                     eo[0], eo[1], st));
         if (mid) record_event(mid, st);
-        if (!backward) {
-            cu::InpaintEye ie[2];
-            for (int e = 0; e < 2; ++e) {
-                for (int c = 0; c < 3; ++c) ie[e].plane[c] = eo[e].plane[c];
-                ie[e].pitch = lp;
-                ie[e].mask_bytes = nullptr;
-                ie[e].mask_bits = eo[e].mask_bits;
-                ie[e].mask_pitch = mwords;
-                ie[e].list = list_ptr(e, 0);
-                ie[e].count = counts + e;
-                ie[e].list2 = nullptr;
-                ie[e].repair = reinterpret_cast<uint32_t*>(ipa);
-            }
-            CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st));
-        }
+        enq_inpaint(st);
     }
 
     void enq_formats(cudaStream_t st) {
@@ -730,101 +753,264 @@ struct Pipeline::Impl {
     }
 
     void ensure_band_resources() {
-        if (band_stream) return;
+        if (h2d_stream) return;
         int lo = 0, hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        CK(cudaStreamCreateWithPriority(&band_stream, cudaStreamNonBlocking, hi));
         CK(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
-        for (auto& e : band_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&depth_stream, cudaStreamNonBlocking, hi));
+        const std::size_t K = bands.size();
+        band_streams.assign(K, nullptr);
+        for (auto& s2 : band_streams) CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        for (auto* v : {&ev_in, &ev_fork, &ev_join, &ev_rows}) {
+            v->assign(K, nullptr);
+            for (auto& e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        for (auto* e : {&ev_prior, &ev_d2h, &ev_start}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         if (!conv_ev[0])
             for (auto& e : conv_ev) CK(cudaEventCreate(&e));
     }
 
-    // Host planes -> src in two row parts on h2d_stream (band_ev[0], band_ev[1]).
-    void upload_banded(const ImageRGB8& img, cudaStream_t st) {
-        CK(cudaEventRecord(band_ev[4], st));  // earlier work on st (reads src) comes first
-        CK(cudaStreamWaitEvent(h2d_stream, band_ev[4], 0));
-        for (int part = 0; part < 2; ++part) {
-            const int r0 = part ? in_rows_a : 0, r1 = part ? h : in_rows_a;
-            for (int c = 0; c < 3; ++c)
-                CK(cudaMemcpy2DAsync(src + c * plane() + static_cast<std::size_t>(r0) * pitch, pitch,
-                                     img.plane(c).data() + static_cast<std::size_t>(r0) * w, w, w,
-                                     r1 - r0, cudaMemcpyHostToDevice, h2d_stream));
-            CK(cudaEventRecord(band_ev[part], h2d_stream));
+    // the fused routes write the final output planes in DIBR (patched in place by the
+    // inpaint), so their rows can leave per band
+    bool band_back() const { return route != kEyes; }
+
+    // Host planes -> src in K row parts on h2d_stream (ev_in[k]): parts [k0, k1). Part 0 goes
+    // before the frame's graph; the others after it, held until band 0's depth stage is done
+    // (conv_ev[1]): while the copy engine streams host reads, every dependent launch of that
+    // chain waits behind them on PCIe (~20 us each), so the first band gets the link first.
+    void upload_banded(const ImageRGB8& img, cudaStream_t st, int k0, int k1) {
+        if (k0 == 0) {
+            CK(cudaEventRecord(ev_prior, st));  // earlier work on st (reads src) comes first
+            CK(cudaStreamWaitEvent(h2d_stream, ev_prior, 0));
+        } else {
+            CK(cudaStreamWaitEvent(h2d_stream, conv_ev[1], 0));
+        }
+        int r0 = k0 == 0 ? 0 : bands[k0 - 1].in_rows;
+        for (int k = k0; k < k1; ++k) {
+            const int r1 = bands[k].in_rows;
+            if (r1 > r0)
+                for (int c = 0; c < 3; ++c)
+                    CK(cudaMemcpy2DAsync(src + c * plane() + static_cast<std::size_t>(r0) * pitch, pitch,
+                                         img.plane(c).data() + static_cast<std::size_t>(r0) * w, w, w,
+                                         r1 - r0, cudaMemcpyHostToDevice, h2d_stream));
+            CK(cudaEventRecord(ev_in[k], h2d_stream));
+            r0 = std::max(r0, r1);
         }
     }
 
-    void enqueue_banded(cudaStream_t st, const std::array<cudaEvent_t, 7>& ev) {
+    void dibr_eyes(cu::EyeOut (&eo)[2]) const {
+        uint8_t *L[3], *R[3];
+        int lp = pitch;
+        eye_planes(L, R, lp);
+        for (int e = 0; e < 2; ++e) {
+            for (int c = 0; c < 3; ++c) eo[e].plane[c] = e ? R[c] : L[c];
+            eo[e].pitch = lp;
+            eo[e].mask_bytes = nullptr;
+            eo[e].mask_bits = backward ? nullptr : mbits + static_cast<std::size_t>(e) * mwords * h;
+            eo[e].mask_pitch = mwords;
+            eo[e].list = backward ? nullptr : list_ptr(e, 0);
+            eo[e].count = counts + e;
+        }
+    }
+
+    void enq_inpaint(cudaStream_t st) {
+        if (backward) return;
+        cu::EyeOut eo[2];
+        dibr_eyes(eo);
+        cu::InpaintEye ie[2];
+        for (int e = 0; e < 2; ++e) {
+            for (int c = 0; c < 3; ++c) ie[e].plane[c] = eo[e].plane[c];
+            ie[e].pitch = eo[e].pitch;
+            ie[e].mask_bytes = nullptr;
+            ie[e].mask_bits = eo[e].mask_bits;
+            ie[e].mask_pitch = mwords;
+            ie[e].list = list_ptr(e, 0);
+            ie[e].count = counts + e;
+            ie[e].list2 = nullptr;
+            ie[e].repair = reinterpret_cast<uint32_t*>(ipa);
+        }
+        CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st));
+    }
+
+    // bil_count layout: [0, K) per-band uncertified counts, [K, 2K) tile-claim counters;
+    // band k lists its pixels from bil_list + (first row of band k) * w.
+    // Head: band 0's depth stage (launched before the upload of the other parts is queued).
+    void enqueue_banded_head(cudaStream_t st, const std::array<cudaEvent_t, 7>& ev) {
         const uint8_t* s = src;
-        cudaStream_t sb = band_stream;
-        wait_event_any(st, band_ev[0]);
+        const int K = static_cast<int>(bands.size());
+        wait_event_any(st, ev_in[0]);
         record_event(ev[0], st);
         CK(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * dt.bx * dt.by, st));
-        CK(cudaMemsetAsync(bil_count, 0, 4 * sizeof(uint32_t), st));
+        CK(cudaMemsetAsync(bil_count, 0, 2 * K * sizeof(uint32_t), st));
+        if (!backward) CK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), st));
+        const Band& b = bands[0];
         CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
-                           dt.block, dt.bx, st, 0, dtile_a));
-        CK(cu::block_values(sums, gm, dt, values, st, 0, brow_a));
-        CK(cu::upsample(values, gm, dt, depth, st, 0, urow_a));
+                           dt.block, dt.bx, st, 0, b.dtile));
+        CK(cu::block_values(sums, gm, dt, values, st, 0, b.brow));
+        CK(cu::upsample(values, gm, dt, depth, st, 0, b.urow));
         record_event(ev[1], st);
-        CK(cudaEventRecord(band_ev[2], st));  // fork
-        CK(cudaStreamWaitEvent(sb, band_ev[2], 0));
-        CK(cu::bilateral_sep_main(depth, luma, gm, radius, h_spatial.data(), range, filt, bil_list,
-                                  bil_count, bil_count + 1, 0, btile_a, st));
-        wait_event_any(sb, band_ev[1]);
-        CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
-                           dt.block, dt.bx, sb, dtile_a, -1));
-        CK(cu::block_values(sums, gm, dt, values, sb, brow_a, -1));
-        CK(cu::upsample(values, gm, dt, depth, sb, urow_a, -1));
-        CK(cu::bilateral_sep_main(depth, luma, gm, radius, h_spatial.data(), range, filt, bil_list,
-                                  bil_count, bil_count + 2, btile_a, -1, sb));
-        CK(cudaEventRecord(band_ev[3], sb));  // join
-        CK(cudaStreamWaitEvent(st, band_ev[3], 0));
+    }
+
+    // Body: the other parts' depth stages (each after its upload part), every band's filter
+    // (+ fix-up + DIBR rows on the fused routes), then the inpaint and formats.
+    void enqueue_banded_body(cudaStream_t st, const std::array<cudaEvent_t, 7>& ev) {
+        const uint8_t* s = src;
+        const int K = static_cast<int>(bands.size());
+        const int TYb = cu::bilateral_sep_tile_rows();
+        const bool back = band_back();
+        cu::EyeOut eo[2];
+        dibr_eyes(eo);
+        CK(cudaEventRecord(ev_start, st));
+        CK(cudaStreamWaitEvent(depth_stream, ev_start, 0));
+        Band prev{0, 0, 0, 0, 0};
+        for (int k = 0; k < K; ++k) {
+            const Band& b = bands[k];
+            cudaStream_t ds = depth_stream, bs = band_streams[k];
+            if (k > 0) {
+                wait_event_any(ds, ev_in[k]);
+                CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
+                                   dt.block, dt.bx, ds, prev.dtile, b.dtile));
+                CK(cu::block_values(sums, gm, dt, values, ds, prev.brow, b.brow));
+                CK(cu::upsample(values, gm, dt, depth, ds, prev.urow, b.urow));
+            }
+            CK(cudaEventRecord(ev_fork[k], ds));
+            CK(cudaStreamWaitEvent(bs, ev_fork[k], 0));
+            const int y0 = prev.btile * TYb, y1 = std::min(h, b.btile * TYb);
+            uint32_t* list = bil_list + static_cast<std::size_t>(y0) * w;
+            CK(cu::bilateral_sep_main(depth, luma, gm, radius, h_spatial.data(), range, filt, list,
+                                      bil_count + k, bil_count + K + k, prev.btile, b.btile,
+                                      sep_table, bs));
+            CK(cu::bilateral_sep_fixup(depth, luma, gm, radius, spatial, range, filt, list,
+                                       bil_count + k, bs));
+            if (back) {
+                CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols,
+                            backward, eo[0], eo[1], bs, y0, y1));
+                record_event(ev_rows[k], bs);
+            }
+            CK(cudaEventRecord(ev_join[k], bs));
+            prev = b;
+        }
+        for (int k = 0; k < K; ++k) CK(cudaStreamWaitEvent(st, ev_join[k], 0));
         record_event(ev[6], st);
-        CK(cu::bilateral_sep_fixup(depth, luma, gm, radius, spatial, range, filt, bil_list, bil_count,
-                                   st));
         record_event(ev[2], st);
-        enq_dibr_inpaint(s, st, ev[3]);
+        if (!back)
+            CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols,
+                        backward, eo[0], eo[1], st));
+        record_event(ev[3], st);
+        enq_inpaint(st);
         record_event(ev[4], st);
         enq_formats(st);
         record_event(ev[5], st);
     }
 
-    // convert_image's frame: upload + run, banded when the plan and the host planes allow.
-    void upload_run_conv(const ImageRGB8& img, cudaStream_t st) {
+    cudaGraphExec_t capture(void (Impl::*fn)(cudaStream_t, const std::array<cudaEvent_t, 7>&)) {
+        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            (this->*fn)(stream, conv_ev);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(stream, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            throw;
+        }
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamEndCapture(stream, &g));
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        return exec;
+    }
+
+    // Output planes of format f on the host (pitch = output width).
+    struct HostOut {
+        uint8_t* plane[3];
+    };
+
+    // After the banded graph: each band's output rows leave as soon as its DIBR finished
+    // (d2h_stream); then the words that held damage are rewritten from the final planes.
+    void download_banded(StereoFormat f, const HostOut& out, cudaStream_t st) {
+        const int K = static_cast<int>(bands.size());
+        const int TYb = cu::bilateral_sep_tile_rows();
+        const int ow = output_width(f), op = output_pitch(f);
+        const std::size_t ps = static_cast<std::size_t>(op) * h;
+        int y0 = 0;
+        for (int k = 0; k < K; ++k) {
+            const int y1 = std::min(h, bands[k].btile * TYb);
+            CK(cudaStreamWaitEvent(d2h_stream, ev_rows[k], 0));
+            for (int c = 0; c < 3; ++c)
+                CK(cudaMemcpy2DAsync(out.plane[c] + static_cast<std::size_t>(y0) * ow, ow,
+                                     output(f) + c * ps + static_cast<std::size_t>(y0) * op, op, ow,
+                                     y1 - y0, cudaMemcpyDeviceToHost, d2h_stream));
+            y0 = y1;
+        }
+        CK(cudaEventRecord(ev_d2h, d2h_stream));
+        CK(cudaStreamWaitEvent(st, ev_d2h, 0));
+        if (backward) return;  // no holes: the early rows are final
+        cu::EyeOut eo[2];
+        dibr_eyes(eo);
+        cu::PatchEye pe[2];
+        for (int e = 0; e < 2; ++e) {
+            for (int c = 0; c < 3; ++c) {
+                pe[e].dev[c] = eo[e].plane[c];
+                pe[e].host[c] = eo[e].plane[c] ? out.plane[c] + (route == kDirectFsbs && e ? w : 0) : nullptr;
+            }
+            pe[e].dpitch = eo[e].pitch;
+            pe[e].hpitch = ow;
+            pe[e].mask = eo[e].mask_bits;
+            pe[e].mpitch = mwords;
+        }
+        CK(cu::patch_host(pe[0], pe[1], gm, st));
+    }
+
+    // convert_image's frame: upload + run (+ the outputs' download when banded). Returns
+    // true when the outputs in `outs` were downloaded here.
+    bool upload_run_conv(const ImageRGB8& img, cudaStream_t st, std::map<StereoFormat, ImageRGB8>* outs) {
         bool pinned = band_ok;
         for (int c = 0; c < 3 && pinned; ++c) pinned = host_pinned(img.plane(c).data());
         if (!pinned) {
             for (int c = 0; c < 3; ++c) h2d_plane(src + c * plane(), img.plane(c).data(), st);
             run_conv(src, st);
-            return;
+            return false;
         }
         if ((formats & kFormatHsbs) && (w % 2 != 0))
             throw std::invalid_argument("side_by_side: half mode requires an even width");
         ensure_band_resources();
-        upload_banded(img, st);
+        const int K = static_cast<int>(bands.size());
+        // part 0 -> head (band 0's depth) -> the other parts (held until the head is done)
+        // -> body. An event-wait node sees the records made before its graph's launch, so
+        // each graph is launched after the uploads it waits for are queued.
+        upload_banded(img, st, 0, 1);
         last_conv = true;
         if (!graphs_enabled()) {
-            enqueue_banded(st, conv_ev);
-            return;
+            enqueue_banded_head(st, conv_ev);
+            upload_banded(img, st, 1, K);
+            enqueue_banded_body(st, conv_ev);
+        } else {
+            if (!band_exec) band_exec = capture(&Impl::enqueue_banded_head);
+            if (!band_exec2) band_exec2 = capture(&Impl::enqueue_banded_body);
+            CK(cudaGraphLaunch(band_exec, st));
+            upload_banded(img, st, 1, K);
+            CK(cudaGraphLaunch(band_exec2, st));
         }
-        if (!band_exec) {
-            CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-            try {
-                enqueue_banded(stream, conv_ev);
-            } catch (...) {
-                cudaGraph_t g = nullptr;
-                cudaStreamEndCapture(stream, &g);
-                if (g) cudaGraphDestroy(g);
-                cudaGetLastError();
-                throw;
+        if (!outs || !band_back()) return false;
+        const StereoFormat f = route == kFusedAnaglyph ? kFormatAnaglyph : kFormatFsbs;
+        ImageRGB8 o(output_width(f), h, false);
+        HostOut ho{{o.plane(0).data(), o.plane(1).data(), o.plane(2).data()}};
+        for (int c = 0; c < 3; ++c)
+            if (!host_pinned(ho.plane[c])) {
+                // unpinned output planes: plain download after the frame
+                for (int c2 = 0; c2 < 3; ++c2)
+                    d2h_plane(ho.plane[c2], output(f) + c2 * static_cast<std::size_t>(output_pitch(f)) * h,
+                              output_pitch(f), output_width(f), st);
+                (*outs)[f] = std::move(o);
+                return true;
             }
-            cudaGraph_t g = nullptr;
-            CK(cudaStreamEndCapture(stream, &g));
-            const cudaError_t e = cudaGraphInstantiate(&band_exec, g, 0);
-            cudaGraphDestroy(g);
-            CK(e);
-        }
-        CK(cudaGraphLaunch(band_exec, st));
+        download_banded(f, ho, st);
+        (*outs)[f] = std::move(o);
+        return true;
     }
 
     StageTimings timings() {
@@ -1404,16 +1590,36 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
     cfg.validate();
     auto p = stage_plan(dev, src.width, src.height, cfg);
     cudaStream_t st = p->stream;
-    p->upload_run_conv(src, st);
+    ConversionResult res;
+    static const bool dbg = std::getenv("P3S_DEBUG_CONV") != nullptr;
+    static thread_local cudaEvent_t dbg_ev[2] = {nullptr, nullptr};
+    if (dbg && !dbg_ev[0]) {
+        CK(cudaEventCreate(&dbg_ev[0]));
+        CK(cudaEventCreate(&dbg_ev[1]));
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    if (dbg) CK(cudaEventRecord(dbg_ev[0], st));
+    const bool have_outputs = p->upload_run_conv(src, st, &res.outputs);
+    const auto t1 = std::chrono::steady_clock::now();
     const std::size_t n = p->npix();
     uint8_t* buf = static_cast<uint8_t*>(map_pool().take(dev.ordinal(), 2 * n));
     try {
-        // device copies of the maps (unpitched), then the outputs to the host
-        CK(cudaMemcpy2DAsync(buf, p->w, p->depth, p->pitch, p->w, p->h, cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemcpy2DAsync(buf + n, p->w, p->filt, p->pitch, p->w, p->h, cudaMemcpyDeviceToDevice, st));
-        ConversionResult res;
+        // device copies of the maps (unpitched), then the outputs to the host. After a
+        // graph frame the copies run on a side stream from the filter's end (conv_ev[2]),
+        // beside the inpaint and the downloads.
+        cudaStream_t ms = st;
+        if (p->last_conv) {
+            ms = p->aux();
+            CK(cudaStreamWaitEvent(ms, p->conv_ev[2], 0));
+        }
+        CK(cudaMemcpy2DAsync(buf, p->w, p->depth, p->pitch, p->w, p->h, cudaMemcpyDeviceToDevice, ms));
+        CK(cudaMemcpy2DAsync(buf + n, p->w, p->filt, p->pitch, p->w, p->h, cudaMemcpyDeviceToDevice, ms));
+        if (ms != st) {
+            CK(cudaEventRecord(p->aux_done, ms));
+            CK(cudaStreamWaitEvent(st, p->aux_done, 0));
+        }
         for (StereoFormat f : {kFormatAnaglyph, kFormatHsbs, kFormatFsbs}) {
-            if (!(p->formats & f)) continue;
+            if (!(p->formats & f) || have_outputs) continue;
             const int ow = p->output_width(f);
             ImageRGB8 img(ow, p->h, false);
             const std::size_t ps = static_cast<std::size_t>(p->output_pitch(f)) * p->h;
@@ -1421,8 +1627,27 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
                 p->d2h_plane(img.plane(c).data(), p->output(f) + c * ps, p->output_pitch(f), ow, st);
             res.outputs[f] = std::move(img);
         }
+        if (dbg) CK(cudaEventRecord(dbg_ev[1], st));
         CK(cudaStreamSynchronize(st));
         res.timings = p->timings();
+        if (dbg) {
+            float a0 = 0, b5 = 0, ab = 0;
+            cudaEventElapsedTime(&a0, dbg_ev[0], p->conv_ev[0]);
+            cudaEventElapsedTime(&b5, p->conv_ev[5], dbg_ev[1]);
+            cudaEventElapsedTime(&ab, dbg_ev[0], dbg_ev[1]);
+            std::fprintf(stderr, "[p3s] gpu: start->ev0 %.1f us, ev5->end %.1f us, start->end %.1f us\n",
+                         a0 * 1e3, b5 * 1e3, ab * 1e3);
+            const auto t2 = std::chrono::steady_clock::now();
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            float e01 = 0, e06 = 0, e64 = 0, e05 = 0;
+            cudaEventElapsedTime(&e01, p->conv_ev[0], p->conv_ev[1]);
+            cudaEventElapsedTime(&e06, p->conv_ev[0], p->conv_ev[6]);
+            cudaEventElapsedTime(&e64, p->conv_ev[6], p->conv_ev[4]);
+            cudaEventElapsedTime(&e05, p->conv_ev[0], p->conv_ev[5]);
+            std::fprintf(stderr, "[p3s] convert: enqueue %.1f us, wait %.1f us, total %.1f us | gpu: depth0 %.1f, "
+                         "filter+dibr end %.1f, inpaint %.1f, all %.1f us\n", us(t0, t1), us(t1, t2), us(t0, t2),
+                         e01 * 1e3, e06 * 1e3, e64 * 1e3, e05 * 1e3);
+        }
         maps = std::make_shared<DeferredMaps>(dev.ordinal(), p->w, p->h, buf);
         return res;
     } catch (...) {
@@ -1435,8 +1660,16 @@ ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg
     cfg.validate();
     auto p = stage_plan(dev, src.width, src.height, cfg);
     cudaStream_t st = p->stream;
-    p->upload_run_conv(src, st);
     ConversionResult res;
+    if (p->upload_run_conv(src, st, &res.outputs)) {
+        res.depth = GrayMap(p->w, p->h, false);
+        res.filtered_depth = GrayMap(p->w, p->h, false);
+        p->d2h_plane(res.depth.data.data(), p->depth, p->pitch, p->w, st);
+        p->d2h_plane(res.filtered_depth.data.data(), p->filt, p->pitch, p->w, st);
+        CK(cudaStreamSynchronize(st));
+        res.timings = p->timings();
+        return res;
+    }
     p->download_overlapped(res, st, dev.impl().copy_stream);
     res.timings = p->timings();
     return res;

@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     const uint8_t* __restrict__ guide, int pitch, int w, int h,
     const double* __restrict__ range_g, uint8_t* __restrict__ out, uint32_t* __restrict__ list,
     uint32_t* __restrict__ count, int tiles_x, int tile_begin, int tile_end,
-    uint32_t* __restrict__ tile_ctr) {
+    uint32_t* __restrict__ tile_ctr, const float* __restrict__ table_g) {
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R;
     constexpr int SH = TY + 2 * R;
@@ -487,9 +487,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     // raw guide / depth bytes of the NEXT tile, fetched with cp.async while this one computes
     uint8_t* s_raw = smem + kSepEntries * kF32Copies * 4 + (SW * SH * 4 + 15) / 16 * 16;  // [2][SH][SWR]
 
-    for (int i = threadIdx.x; i < kSepEntries * kF32Copies; i += blockDim.x) {
-        const int k = i / kF32Copies;
-        reinterpret_cast<float*>(tbl)[i] = k < 511 ? static_cast<float>(range_g[abs(k - 255)]) : 0.0f;
+    if (table_g) {
+        // the plan's prebuilt replicated table: 16-byte async copies, landing with the
+        // first tile's prefetch (same commit group)
+        for (int i = threadIdx.x; i < kSepEntries * kF32Copies / 4; i += blockDim.x)
+            cp_async16(tbl + 16 * i, table_g + 4 * i);
+    } else {
+        for (int i = threadIdx.x; i < kSepEntries * kF32Copies; i += blockDim.x) {
+            const int k = i / kF32Copies;
+            reinterpret_cast<float*>(tbl)[i] = k < 511 ? static_cast<float>(range_g[abs(k - 255)]) : 0.0f;
+        }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // certificate: every numerator / denominator term carries <= R + 5 float roundings
@@ -518,6 +525,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     __shared__ int s_next;
     int tile = tile_begin + static_cast<int>(blockIdx.x);
     if (tile < tile_end) prefetch(tile);
+    else cp_async_commit();
 
     while (tile < tile_end) {
         const int tx0 = (tile % tiles_x) * kTX;
@@ -806,7 +814,7 @@ template <int R, int P, int NW, int U = 4>
 cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
                             const double* spatial_host, const double* range, uint8_t* out,
                             uint32_t* list, uint32_t* count, uint32_t* tile_ctr, int tr0, int tr1,
-                            cudaStream_t st) {
+                            const float* table, cudaStream_t st) {
     SepParam<R, P> sp;
     // sx(d) = exp(-(d*d) * inv_s): the dy = 0 row of the host spatial table (same formula)
     const double* row0 = spatial_host + static_cast<size_t>(R) * (R + 1);
@@ -841,7 +849,8 @@ cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
     const int t0 = tr0 * tiles_x, t1 = tr1 * tiles_x;
     const int grid = min(t1 - t0, per_sm * sm_count());
     k_bilateral_sep<R, P, NW, U><<<grid, NW * 32, smem, st>>>(
-        sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, t0, t1, tile_ctr);
+        sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, t0, t1, tile_ctr,
+        table);
     return cudaGetLastError();
 }
 
@@ -861,7 +870,7 @@ cudaError_t launch_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm
 cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                            const double* spatial_host, const double* spatial_dev,
                            const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
-                           cudaStream_t st, cudaEvent_t after_main) {
+                           cudaStream_t st, cudaEvent_t after_main, const float* table) {
     if (!bilateral_fast_available(radius)) {
         const cudaError_t e = bilateral_tiled(depth, guide, gm, radius, spatial_host, range, out, nullptr, st);
         if (after_main) record_event_any(after_main, st);
@@ -871,7 +880,7 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
     cudaError_t e = cudaMemsetAsync(count, 0, 2 * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
     e = bilateral_sep_main(depth, guide, gm, radius, spatial_host, range, out, list, count,
-                           count + 1, 0, -1, st);
+                           count + 1, 0, -1, table, st);
     if (e != cudaSuccess) return e;
     if (after_main) record_event_any(after_main, st);
     return bilateral_sep_fixup(depth, guide, gm, radius, spatial_dev, range, out, list, count, st);
@@ -882,11 +891,12 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
 cudaError_t bilateral_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                                const double* spatial_host, const double* range, uint8_t* out,
                                uint32_t* list, uint32_t* count, uint32_t* tile_ctr,
-                               int tile_row0, int tile_row1, cudaStream_t st) {
+                               int tile_row0, int tile_row1, const float* table, cudaStream_t st) {
 #define P3S_SEP(RR)                                                                          \
     case RR:                                                                                 \
         return launch_sep_main<RR, 8, 16, RR>(depth, guide, gm, spatial_host, range, out,    \
-                                              list, count, tile_ctr, tile_row0, tile_row1, st);
+                                              list, count, tile_ctr, tile_row0, tile_row1,   \
+                                              table, st);
     switch (radius) {
         P3S_SEP(7) P3S_SEP(8) P3S_SEP(9) P3S_SEP(10) P3S_SEP(11) P3S_SEP(12) P3S_SEP(13)
         P3S_SEP(14) P3S_SEP(15) P3S_SEP(16) P3S_SEP(17) P3S_SEP(18) P3S_SEP(19) P3S_SEP(20)
@@ -914,6 +924,23 @@ cudaError_t bilateral_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom
 }
 
 int bilateral_sep_tile_rows() { return 16 * 8; }
+
+size_t bilateral_sep_table_bytes() { return static_cast<size_t>(kSepEntries) * kF32Copies * 4; }
+
+namespace {
+__global__ void k_build_sep_table(const double* __restrict__ range_g, float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= kSepEntries * kF32Copies) return;
+    const int k = i / kF32Copies;
+    out[i] = k < 511 ? static_cast<float>(range_g[abs(k - 255)]) : 0.0f;
+}
+}  // namespace
+
+cudaError_t build_sep_table(const double* range, float* table, cudaStream_t st) {
+    const int n = kSepEntries * kF32Copies;
+    k_build_sep_table<<<(n + 255) / 256, 256, 0, st>>>(range, table);
+    return cudaGetLastError();
+}
 
 bool bilateral_fast_available(int radius) {
     const char* v = getenv("P3S_BIL_FAST");

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
                                               const uint8_t* __restrict__ D, int pitch, int w, int h,
                                               const double* __restrict__ shift_g,
                                               const int4* __restrict__ cols_g, int backward,
-                                              EyeOut L, EyeOut Rt) {
+                                              EyeOut L, EyeOut Rt, int ya, int yb) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ double s_shift[INT ? 1 : 256];
     __shared__ int4 s_cols[INT ? 256 : 1];
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
         }
     };
 
-    for (int y = blockIdx.x; y < h; y += gridDim.x) {
+    for (int y = ya + static_cast<int>(blockIdx.x); y < yb; y += gridDim.x) {
         __syncthreads();  // previous row's readers are done with shared memory
         const size_t row = static_cast<size_t>(y) * pitch;
         const uint8_t* planes_in[4] = {R + row, G + row, B + row, D + row};
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
                                                   const uint8_t* __restrict__ B,
                                                   const uint8_t* __restrict__ D, int pitch, int w,
                                                   int h, const int4* __restrict__ cols_g, EyeOut L,
-                                                  EyeOut Rt) {
+                                                  EyeOut Rt, int ya, int yb) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int4 s_cols[256];
     const int wpad = (w + 15) & ~15;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
     const int tid = threadIdx.x, lane = tid & 31;
     for (int i = tid; i < 256; i += blockDim.x) s_cols[i] = cols_g[i];
 
-    for (int y = blockIdx.x; y < h; y += gridDim.x) {
+    for (int y = ya + static_cast<int>(blockIdx.x); y < yb; y += gridDim.x) {
         __syncthreads();
         const size_t row = static_cast<size_t>(y) * pitch;
         for (int v = tid; v < nvec; v += blockDim.x) {
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                                                    const uint8_t* __restrict__ B,
                                                    const uint8_t* __restrict__ D, int pitch,
                                                    int w, int h, const int4* __restrict__ cols_g,
-                                                   EyeOut L, EyeOut Rt) {
+                                                   EyeOut L, EyeOut Rt, int ya, int yb) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int4 s_cols[256];
     const int wpad = (w + 15) & ~15;
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
     for (int i = tid; i < 256; i += blockDim.x) s_cols[i] = cols_g[i];
     const int nqr = (nq + 31) & ~31;
 
-    for (int y = blockIdx.x; y < h; y += gridDim.x) {
+    for (int y = ya + static_cast<int>(blockIdx.x); y < yb; y += gridDim.x) {
         __syncthreads();
         const size_t row = static_cast<size_t>(y) * pitch;
         for (int q = tid; q < nq; q += blockDim.x) {
@@ -567,7 +567,10 @@ __global__ void k_hsbs16(const uint8_t* __restrict__ l0, const uint8_t* __restri
 
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
-                 EyeOut right, cudaStream_t st) {
+                 EyeOut right, cudaStream_t st, int ya, int yb) {
+    if (yb < 0 || yb > gm.h) yb = gm.h;
+    if (yb <= ya) return cudaSuccess;
+    const int rows = yb - ya;
     const int wpad = (gm.w + 15) & ~15;
     const size_t smem = static_cast<size_t>(wpad) * (backward ? 4 : 12);
     constexpr size_t kMax = kDibrMaxSmem;
@@ -601,7 +604,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
     if (cols && !backward && left.mask_bits && right.mask_bits && left.list && right.list &&
         vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 <= kMax) {
         void (*qk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
-                   const int4*, EyeOut, EyeOut) = ana ? k_dibr_quad<0> : k_dibr_quad<1>;
+                   const int4*, EyeOut, EyeOut, int, int) = ana ? k_dibr_quad<0> : k_dibr_quad<1>;
         static bool qconf[64] = {false};
         if (dev < 64 && !qconf[dev]) {
             cudaFuncSetAttribute(k_dibr_quad<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
@@ -612,15 +615,15 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         int qper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, qk, 256, qsmem);
         if (qper < 1) qper = 1;
-        qk<<<min(gm.h, qper * sm_count()), 256, qsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
-                                                             cols, left, right);
+        qk<<<min(rows, qper * sm_count()), 256, qsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
+                                                             cols, left, right, ya, yb);
         return cudaGetLastError();
     }
     if (ana && cols && aligned && (backward || (left.mask_bits && right.mask_bits && left.list &&
                                                 right.list)) &&
         vec != 0 && static_cast<size_t>(wpad) * (backward ? 7 : 15) + 16 <= kMax) {
         void (*vk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
-                   const int4*, EyeOut, EyeOut) = backward ? k_dibr_ana<true> : k_dibr_ana<false>;
+                   const int4*, EyeOut, EyeOut, int, int) = backward ? k_dibr_ana<true> : k_dibr_ana<false>;
         static bool vconf[64] = {false};
         if (dev < 64 && !vconf[dev]) {
             cudaFuncSetAttribute(k_dibr_ana<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
@@ -631,19 +634,19 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         int vper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, vk, 256, vsmem);
         if (vper < 1) vper = 1;
-        vk<<<min(gm.h, vper * sm_count()), 256, vsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
-                                                             cols, left, right);
+        vk<<<min(rows, vper * sm_count()), 256, vsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
+                                                             cols, left, right, ya, yb);
         return cudaGetLastError();
     }
     void (*kern)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
-                 const double*, const int4*, int, EyeOut, EyeOut) =
+                 const double*, const int4*, int, EyeOut, EyeOut, int, int) =
         ana ? (cols ? k_dibr<0, true> : k_dibr<0, false>) : (cols ? k_dibr<1, true> : k_dibr<1, false>);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
     if (per_sm < 1) per_sm = 1;
-    const int grid = min(gm.h, per_sm * sm_count());
+    const int grid = min(rows, per_sm * sm_count());
     kern<<<grid, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h, shift, cols,
-                                  backward ? 1 : 0, left, right);
+                                  backward ? 1 : 0, left, right, ya, yb);
     return cudaGetLastError();
 }
 

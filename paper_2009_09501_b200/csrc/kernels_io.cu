@@ -132,5 +132,46 @@ cudaError_t interleave(const uint8_t* r, const uint8_t* g, const uint8_t* b, int
     return cudaGetLastError();
 }
 
+namespace {
+// One warp per (eye, row, group of 32 mask words): lane j tests word j; for every word with
+// damage the warp copies its 32 bytes per plane (lane = pixel), one coalesced store each.
+__global__ void __launch_bounds__(256) k_patch_host(PatchEye a, PatchEye b, int w, int h) {
+    const int lane = threadIdx.x & 31;
+    const int mwords = (w + 31) >> 5, groups = (mwords + 31) >> 5;
+    const long long total = 2LL * h * groups;
+    const long long nwarps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    for (long long it = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < total;
+         it += nwarps) {
+        const int e = static_cast<int>(it / (static_cast<long long>(h) * groups));
+        const int rem = static_cast<int>(it - static_cast<long long>(e) * h * groups);
+        const int y = rem / groups, g = rem - y * groups;
+        const PatchEye& P = e ? b : a;
+        const int j = g * 32 + lane;
+        const uint32_t m = j < mwords ? __ldg(P.mask + static_cast<size_t>(y) * P.mpitch + j) : 0u;
+        unsigned nz = __ballot_sync(0xFFFFFFFFu, m != 0u);
+        while (nz) {
+            const int k = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const int x = (g * 32 + k) * 32 + lane;
+            if (x < w) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    if (P.dev[c])
+                        P.host[c][static_cast<size_t>(y) * P.hpitch + x] =
+                            P.dev[c][static_cast<size_t>(y) * P.dpitch + x];
+            }
+        }
+    }
+}
+}  // namespace
+
+cudaError_t patch_host(PatchEye left, PatchEye right, Geom gm, cudaStream_t st) {
+    const int mwords = (gm.w + 31) >> 5, groups = (mwords + 31) >> 5;
+    const long long warps = 2LL * gm.h * groups;
+    const int blocks = static_cast<int>(std::min<long long>((warps + 7) / 8, sm_count() * 8LL));
+    k_patch_host<<<blocks, 256, 0, st>>>(left, right, gm.w, gm.h);
+    return cudaGetLastError();
+}
+
 }  // namespace cu
 }  // namespace p3s

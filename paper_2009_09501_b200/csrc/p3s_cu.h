@@ -65,7 +65,8 @@ int bilateral_tiled_max_radius();
 cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                            const double* spatial_host, const double* spatial_dev,
                            const double* range, uint8_t* out, uint32_t* list, uint32_t* count,
-                           cudaStream_t st, cudaEvent_t after_main = nullptr);
+                           cudaStream_t st, cudaEvent_t after_main = nullptr,
+                           const float* table = nullptr);
 // The certified path in parts, for row-banded schedules: bilateral_sep_main runs the FP32
 // kernel over tile rows [tile_row0, tile_row1) of bilateral_sep_tile_rows() image rows
 // (appending to list/count, which the caller zeroes once per frame; tile_ctr: one zeroed
@@ -74,11 +75,15 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
 cudaError_t bilateral_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                                const double* spatial_host, const double* range, uint8_t* out,
                                uint32_t* list, uint32_t* count, uint32_t* tile_ctr,
-                               int tile_row0, int tile_row1, cudaStream_t st);
+                               int tile_row0, int tile_row1, const float* table, cudaStream_t st);
 cudaError_t bilateral_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                                 const double* spatial_dev, const double* range, uint8_t* out,
                                 const uint32_t* list, const uint32_t* count, cudaStream_t st);
 int bilateral_sep_tile_rows();
+// The certified kernel's replicated FP32 range table (bilateral_sep_table_bytes(), built once
+// per plan from the FP64 range table); table = nullptr builds it in every CTA instead.
+size_t bilateral_sep_table_bytes();
+cudaError_t build_sep_table(const double* range, float* table, cudaStream_t st);
 // cudaEventRecord, or an event-record graph node while `st` is being captured.
 void record_event_any(cudaEvent_t e, cudaStream_t st);
 bool bilateral_fast_available(int radius);
@@ -106,9 +111,20 @@ struct EyeOut {
 // frames wider than dibr_max_width() are rejected at plan creation.
 constexpr size_t kDibrMaxSmem = 220 * 1024;  // + the kernels' static tables <= 227 KB
 inline int dibr_max_width() { return static_cast<int>(kDibrMaxSmem / 12) & ~15; }
+// Host patch after a banded early download: every 32-pixel word whose mask bit is set
+// (damage the inpaint repaired after the rows left) is copied from the device planes to the
+// host planes (pinned, so device-visible under UVA) with coalesced 32-byte stores.
+struct PatchEye {
+    const uint8_t* dev[3];  // nullptr: plane not produced by this eye
+    uint8_t* host[3];
+    int dpitch, hpitch;
+    const uint32_t* mask;
+    int mpitch;
+};
+cudaError_t patch_host(PatchEye left, PatchEye right, Geom gm, cudaStream_t st);
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
-                 EyeOut right, cudaStream_t st);
+                 EyeOut right, cudaStream_t st, int ya = 0, int yb = -1);  // rows [ya, yb)
 
 // Byte mask -> damaged list (stage-level inpaint entry point).
 cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* list,
