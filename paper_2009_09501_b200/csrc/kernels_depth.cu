@@ -17,14 +17,33 @@ namespace {
 
 constexpr int kTW = 128;  // tile width (pixels)
 constexpr int kTH = 16;   // tile height
-constexpr int kSW = kTW + 2 + 6;  // smem row stride (halo + pad)
+// smem row: left halo at kX0 - 1, pixel c at kX0 + c (8-byte aligned), right halo at kX0 + kTW
+constexpr int kX0 = 8;
+constexpr int kSW = kX0 + kTW + 8;
 constexpr int kMaxBX = kTW / 4 + 2;  // local block columns a tile can touch (block >= 4)
 constexpr int kMaxBY = kTH / 4 + 2;
 
 __device__ __forceinline__ int clampi(int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
 
+// v / block for 0 <= v, v * block < 2^32, with magic = floor(2^32 / block) + 1 (host;
+// magic = 0 when the frame is too large for that bound: plain division)
+#define div_block(v, magic) \
+    ((magic) ? static_cast<int>(__umulhi(static_cast<unsigned>(v), (magic))) : (v) / block)
+
 __device__ __forceinline__ uint8_t luma_px(unsigned r, unsigned g, unsigned b) {
     return static_cast<uint8_t>((77u * r + 150u * g + 29u * b + 128u) >> 8);
+}
+
+// luma of 4 pixels (bytes of r4/g4/b4) -> 4 bytes. Two pixels per 32-bit word in 16-bit
+// lanes: 77r + 150g + 29b + 128 <= 65408 never carries into the next lane.
+__device__ __forceinline__ uint32_t luma4(uint32_t r4, uint32_t g4, uint32_t b4) {
+    const uint32_t rl = __byte_perm(r4, 0, 0x4240), rh = __byte_perm(r4, 0, 0x4341);
+    const uint32_t gl = __byte_perm(g4, 0, 0x4240), gh = __byte_perm(g4, 0, 0x4341);
+    const uint32_t bl = __byte_perm(b4, 0, 0x4240), bh = __byte_perm(b4, 0, 0x4341);
+    const uint32_t sl = 77u * rl + 150u * gl + 29u * bl + 0x00800080u;  // pixels 0, 2
+    const uint32_t sh = 77u * rh + 150u * gh + 29u * bh + 0x00800080u;  // pixels 1, 3
+    // luma bytes sit at bytes 1 and 3 of each word
+    return __byte_perm(sl, sh, 0x7351);
 }
 
 __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__ R,
@@ -32,8 +51,9 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
                                                      const uint8_t* __restrict__ B, int pitch,
                                                      int w, int h, uint8_t* __restrict__ luma,
                                                      unsigned long long* __restrict__ sums,
-                                                     int block, int bx_total, int tile_row0) {
-    __shared__ uint8_t s_y[kTH + 2][kSW];
+                                                     int block, int bx_total, int tile_row0,
+                                                     unsigned magic) {
+    __shared__ __align__(16) uint8_t s_y[kTH + 2][kSW];
     __shared__ unsigned s_sum[kMaxBY][kMaxBX];
 
     const int x0 = blockIdx.x * kTW;
@@ -52,26 +72,18 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
             const uint2 vr = __ldg(reinterpret_cast<const uint2*>(R + off));
             const uint2 vg = __ldg(reinterpret_cast<const uint2*>(G + off));
             const uint2 vb = __ldg(reinterpret_cast<const uint2*>(B + off));
-            const uint8_t* pr = reinterpret_cast<const uint8_t*>(&vr);
-            const uint8_t* pg = reinterpret_cast<const uint8_t*>(&vg);
-            const uint8_t* pb = reinterpret_cast<const uint8_t*>(&vb);
-            uint8_t yv[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                yv[k] = luma_px(pr[k], pg[k], pb[k]);
-                s_y[sr][1 + 8 * c8 + k] = yv[k];
-            }
+            const uint2 yv = make_uint2(luma4(vr.x, vg.x, vb.x), luma4(vr.y, vg.y, vb.y));
+            *reinterpret_cast<uint2*>(&s_y[sr][kX0 + 8 * c8]) = yv;
             const int oy = y0 - 1 + sr;
             if (sr >= 1 && sr <= kTH && oy < h)
-                *reinterpret_cast<uint2*>(luma + static_cast<size_t>(oy) * pitch + x0 + 8 * c8) =
-                    *reinterpret_cast<const uint2*>(yv);
+                *reinterpret_cast<uint2*>(luma + static_cast<size_t>(oy) * pitch + x0 + 8 * c8) = yv;
         }
         for (int item = tid; item < (kTH + 2) * 2; item += blockDim.x) {
             const int sr = item >> 1, side = item & 1;
             const int gy = clampi(y0 - 1 + sr, h - 1);
             const int gx = side ? x0 + kTW : x0 - 1;
             const size_t off = static_cast<size_t>(gy) * pitch + gx;
-            s_y[sr][side ? kTW + 1 : 0] = luma_px(R[off], G[off], B[off]);
+            s_y[sr][side ? kX0 + kTW : kX0 - 1] = luma_px(R[off], G[off], B[off]);
         }
         __syncthreads();
     } else {
@@ -80,40 +92,64 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
             const int gy = clampi(y0 - 1 + sr, h - 1);
             const int gx = clampi(x0 - 1 + sc, w - 1);
             const size_t off = static_cast<size_t>(gy) * pitch + gx;
-            s_y[sr][sc] = luma_px(R[off], G[off], B[off]);
+            s_y[sr][kX0 - 1 + sc] = luma_px(R[off], G[off], B[off]);
         }
         __syncthreads();
         for (int item = tid; item < kTH * kTW; item += blockDim.x) {
             const int r = item / kTW, c = item % kTW;
             const int oy = y0 + r, ox = x0 + c;
-            if (oy < h && ox < w) luma[static_cast<size_t>(oy) * pitch + ox] = s_y[1 + r][1 + c];
+            if (oy < h && ox < w) luma[static_cast<size_t>(oy) * pitch + ox] = s_y[1 + r][kX0 + c];
         }
     }
 
     // ---- Sobel magnitude (depth.cpp:21-41) and block sums (depth.cpp:64-67) ----
-    // thread -> row ty, 8 consecutive pixels starting at column 8*c8. The block column of a
+    // thread -> row ty, 8 consecutive pixels starting at column 8*c8. Per window column j
+    // (pixels x-1 .. x+8) the vertical [1 2 1] sum cs and the difference d = bottom - top are
+    // formed once; then gx = cs[j+1] - cs[j-1] and gy = d[j-1] + 2 d[j] + d[j+1] (the
+    // reference's expressions regrouped in exact integer arithmetic). The block column of a
     // pixel is tracked incrementally (one division per thread, not per pixel).
     {
         const int ty = tid >> 4, c8 = tid & 15;
         const int oy = y0 + ty;
         if (oy < h) {
-            const int bx0 = x0 / block, by0 = y0 / block;
-            const int lby = oy / block - by0;
+            int cs[10], dd[10];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const uint8_t* row = &s_y[ty + r][kX0 + 8 * c8];
+                const uint2 mid = *reinterpret_cast<const uint2*>(row);
+                int p[10];
+                p[0] = row[-1];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    p[1 + k] = (mid.x >> (8 * k)) & 0xFF;
+                    p[5 + k] = (mid.y >> (8 * k)) & 0xFF;
+                }
+                p[9] = row[8];
+#pragma unroll
+                for (int j = 0; j < 10; ++j) {
+                    if (r == 0) {
+                        cs[j] = p[j];
+                        dd[j] = -p[j];
+                    } else if (r == 1) {
+                        cs[j] += 2 * p[j];
+                    } else {
+                        cs[j] += p[j];
+                        dd[j] += p[j];
+                    }
+                }
+            }
+            const int bx0 = div_block(x0, magic), by0 = div_block(y0, magic);
+            const int lby = div_block(oy, magic) - by0;
             const int ox0 = x0 + 8 * c8;
-            int lbx = ox0 / block - bx0;
+            int lbx = div_block(ox0, magic) - bx0;
             int next = (bx0 + lbx + 1) * block;  // first column of the next block
             unsigned run = 0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const int c = 1 + 8 * c8 + k;  // smem column of this pixel
                 const int ox = ox0 + k;
                 if (ox < w) {
-                    const int p00 = s_y[ty][c - 1], p10 = s_y[ty][c], p20 = s_y[ty][c + 1];
-                    const int p01 = s_y[ty + 1][c - 1], p21 = s_y[ty + 1][c + 1];
-                    const int p02 = s_y[ty + 2][c - 1], p12 = s_y[ty + 2][c],
-                              p22 = s_y[ty + 2][c + 1];
-                    const int gx = (p20 + 2 * p21 + p22) - (p00 + 2 * p01 + p02);
-                    const int gy = (p02 + 2 * p12 + p22) - (p00 + 2 * p10 + p20);
+                    const int gx = cs[k + 2] - cs[k];
+                    const int gy = dd[k] + 2 * dd[k + 1] + dd[k + 2];
                     const unsigned mag = min((static_cast<unsigned>(abs(gx)) + static_cast<unsigned>(abs(gy))) >> 2, 255u);
                     if (ox == next) {
                         if (run) atomicAdd(&s_sum[lby][lbx], run);
@@ -129,9 +165,9 @@ __global__ void __launch_bounds__(256) k_depth_front(const uint8_t* __restrict__
     }
     __syncthreads();
     {
-        const int bx0 = x0 / block, by0 = y0 / block;
-        const int nbx = (min(x0 + kTW, w) - 1) / block - bx0 + 1;
-        const int nby = (min(y0 + kTH, h) - 1) / block - by0 + 1;
+        const int bx0 = div_block(x0, magic), by0 = div_block(y0, magic);
+        const int nbx = div_block(min(x0 + kTW, w) - 1, magic) - bx0 + 1;
+        const int nby = div_block(min(y0 + kTH, h) - 1, magic) - by0 + 1;
         for (int i = tid; i < nbx * nby; i += blockDim.x) {
             const int ly = i / nbx, lx = i % nbx;
             const unsigned v = s_sum[ly][lx];
@@ -238,8 +274,12 @@ cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Ge
     if (tile_row1 < 0 || tile_row1 > rows) tile_row1 = rows;
     if (tile_row1 <= tile_row0) return cudaSuccess;
     dim3 grid((gm.w + kTW - 1) / kTW, tile_row1 - tile_row0);
+    const unsigned long long span = static_cast<unsigned long long>(std::max(gm.w, gm.h) + kTW);
+    const unsigned magic = span * static_cast<unsigned>(block) < (1ull << 32)
+                               ? static_cast<unsigned>((1ull << 32) / static_cast<unsigned>(block) + 1ull)
+                               : 0u;
     k_depth_front<<<grid, 256, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, sums, block, bx,
-                                        tile_row0);
+                                        tile_row0, magic);
     return cudaGetLastError();
 }
 
