@@ -12,7 +12,11 @@ p3s.set_device(0)
 chk = oracle.load("port")
 cases = [(67, 33, dict()), (130, 72, dict(base=40, formats=7)), (96, 64, dict(mode=1, formats=1)),
          (161, 90, dict(base=60, formats=4)), (128, 48, dict(formats=2)), (1, 9, dict(base=4, formats=5)),
-         (40, 30, dict(sigma_spatial=3.0, formats=3))]
+         (40, 30, dict(sigma_spatial=3.0, formats=3)),
+         # tall enough for the banded synchronous path (engine.cpp plan_bands): fused
+         # anaglyph, direct FSBS, materialised eyes, backward
+         (200, 300, dict()), (170, 420, dict(formats=4, base=24)), (150, 400, dict(formats=7, base=40)),
+         (130, 300, dict(mode=1, formats=1))]
 for w, h, over in cases:
     img = chk.synthetic_frame(w, h, w + h)
     ref = chk.convert(img, oracle.Cfg(**over))
