@@ -223,8 +223,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the video / 8K config lines")
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=4,
                     help="plans/streams the device-resident frames are pipelined over")
+    ap.add_argument("--inpaint-ctas", type=int, default=-1,
+                    help="inpaint CTAs per lane when --streams > 1 (-1: SMs / 4; 0: one per SM)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--reference-budget", type=float, default=150.0)
     args = ap.parse_args()
@@ -266,21 +268,31 @@ def main():
     # (depth, DIBR, inpaint, their launch tails) overlap another frame's work. Untimed runs
     # replay one CUDA graph per (plan, ring frame), captured during the warm-up; the per-stage
     # breakdown comes from a separate event-timed pass below.
-    lanes = [pipe] + [p3s.Pipeline(W4K, H4K, cfg) for _ in range(max(1, args.streams) - 1)]
+    # With several lanes in flight, each lane's cooperative inpaint runs on a quarter of the
+    # SMs (Pipeline.set_inpaint_ctas): its rounds are latency-bound, so the SMs it leaves go
+    # to the other lanes' filters (more aggregate frames/s). The single-stream leg and the
+    # stage breakdown use `pipe`, which keeps one inpaint CTA per SM (lowest latency).
+    nl = max(1, args.streams)
+    inpaint_ctas = args.inpaint_ctas if args.inpaint_ctas >= 0 else (p3s.sm_count() // 4 if nl > 1 else 0)
+    lanes = [p3s.Pipeline(W4K, H4K, cfg) for _ in range(nl)] if nl > 1 else [pipe]
     for ln in lanes:
+        if ln is not pipe:
+            ln.set_inpaint_ctas(inpaint_ctas)
+    for ln in lanes + ([pipe] if nl > 1 else []):
         for i in range(max(args.warmup, RING)):
             ln.run(ring[i % RING].addr)
     p3s.device_sync()
 
-    def timed_loop(nlanes, steps):
+    def timed_loop(use, steps):
         a, z = p3s.Event(), p3s.Event()
-        ends = [p3s.Event() for _ in range(nlanes)]
+        ends = [p3s.Event() for _ in use]
         a.record(stream)
-        for ln in lanes[1:nlanes]:
-            a.wait(ln.stream)
+        for ln in use:
+            if ln is not pipe:
+                a.wait(ln.stream)
         for i in range(steps):
-            lanes[i % nlanes].run(ring[i % RING].addr)
-        for ln, e in zip(lanes[:nlanes], ends):
+            use[i % len(use)].run(ring[i % RING].addr)
+        for ln, e in zip(use, ends):
             e.record(ln.stream)
             e.wait(stream)
         z.record(stream)
@@ -292,10 +304,10 @@ def main():
     p3s.device_sync()
     clocks.start()
     time.sleep(0.3)  # let nvidia-smi attach before the region
-    elapsed_ms = timed_loop(len(lanes), args.steps)
+    elapsed_ms = timed_loop(lanes, args.steps)
     clk = clocks.stop()
     barrier(world)
-    single_ms = timed_loop(1, min(args.steps, 100))  # one stream: frames back to back
+    single_ms = timed_loop([pipe], min(args.steps, 100))  # one stream: frames back to back
     # stage breakdown (CUDA events between stages, direct launches)
     pipe.timing_sum(reset=True)
     pipe.bilateral_kernel_sum(reset=True)
@@ -548,6 +560,7 @@ def main():
                                    f"over {len(lanes)} streams per GPU"),
         "stages_ms": {k: v / 1e6 for k, v in per.items()},
         "streams": len(lanes),
+        "inpaint_ctas_per_lane": inpaint_ctas,
         "single_stream": {"frames_per_s": min(args.steps, 100) / (single_ms / 1e3),
                           "note": "same frames back to back on one stream (per-frame latency "
                                   "bound, no overlap between frames)"},

@@ -152,6 +152,11 @@ public:
     // Sum of the main bilateral kernel's time (without the exact fix-up) over the same timed
     // runs, for the roofline of the dominant kernel.
     long long bilateral_kernel_ns(long long* count, bool reset = true);
+    // CTAs of the cooperative inpaint kernel (0 = one per SM, the default). With several
+    // pipelines running concurrently, fewer CTAs leave SMs to the other frames (more
+    // aggregate frames/s); a single stream wants every SM (lowest latency). Recaptures the
+    // plan's graphs.
+    void set_inpaint_ctas(int ctas);
     // Device pointers of the results of the last run (pitch(), or fsbs_pitch() for FSBS).
     const std::uint8_t* d_depth() const;
     const std::uint8_t* d_filtered() const;

@@ -41,6 +41,8 @@ P3S_API int p3s_gpu_device_count(void);
 /* Binds the calling thread to a CUDA device (all later calls on this thread use it). */
 P3S_API p3s_status p3s_gpu_set_device(int ordinal);
 P3S_API p3s_status p3s_gpu_device_name(char* buf, size_t cap);
+/* Streaming multiprocessors of the calling thread's device. */
+P3S_API p3s_status p3s_gpu_sm_count(int* out);
 
 /* ---- stage entry points (host planes in/out, row-major w*h, no pitch) ---- */
 /* image.cpp:13-21 */
@@ -98,6 +100,10 @@ P3S_API p3s_status p3s_pipeline_timing_sum(p3s_pipeline* p, p3s_timings* sum, in
 /* Same accumulation for the main bilateral kernel alone (without the exact fix-up). */
 P3S_API p3s_status p3s_pipeline_bilateral_kernel_sum(p3s_pipeline* p, int64_t* sum_ns,
                                                      int64_t* count, int reset);
+/* CTAs of the cooperative inpaint kernel (0 = one per SM, the default). With several
+ * pipelines running concurrently, fewer CTAs leave SMs to the other frames' kernels (more
+ * aggregate frames/s); one stream wants every SM (lowest latency). */
+P3S_API p3s_status p3s_pipeline_set_inpaint_ctas(p3s_pipeline* p, int ctas);
 /* Copies results of the last run to host planes (any pointer may be NULL), then syncs. */
 P3S_API p3s_status p3s_pipeline_download(p3s_pipeline* p, uint8_t* depth, uint8_t* filtered,
                                          p3s_format format, uint8_t* outr, uint8_t* outg,

@@ -121,6 +121,8 @@ _SIGS = {
     "p3s_gpu_device_count": (C.c_int, []),
     "p3s_gpu_set_device": (C.c_int, [C.c_int]),
     "p3s_gpu_device_name": (C.c_int, [C.c_char_p, C.c_size_t]),
+    "p3s_gpu_sm_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "p3s_pipeline_set_inpaint_ctas": (C.c_int, [vp, C.c_int]),
     "p3s_gpu_luma": (C.c_int, [u8p, u8p, u8p, C.c_int, C.c_int, u8p]),
     "p3s_gpu_block_depth": (C.c_int, [u8p, u8p, u8p, C.c_int, C.c_int, vp, f64p]),
     "p3s_gpu_upsample": (C.c_int, [f64p, C.c_int, C.c_int, C.c_int, u8p]),
@@ -210,6 +212,12 @@ def device_count() -> int:
 
 def set_device(ordinal: int) -> None:
     _check(lib().p3s_gpu_set_device(ordinal))
+
+
+def sm_count() -> int:
+    n = C.c_int()
+    _check(lib().p3s_gpu_sm_count(C.byref(n)))
+    return n.value
 
 
 def device_name() -> str:
@@ -470,6 +478,11 @@ class Pipeline:
         _check(lib().p3s_pipeline_download(self.handle, _p(depth), _p(filt), fmt,
                                            *[_p(out[c]) for c in range(3)]))
         return depth, filt, out
+
+    def set_inpaint_ctas(self, ctas: int) -> None:
+        """CTAs of the cooperative inpaint (0 = one per SM). Fewer suit several concurrent
+        pipelines (aggregate throughput); a single stream wants all SMs (latency)."""
+        _check(lib().p3s_pipeline_set_inpaint_ctas(self.handle, int(ctas)))
 
     def bilateral_kernel_sum(self, reset: bool = True):
         """(sum of the main bilateral kernel's ns, runs) over the timed runs (no fix-up)."""

@@ -458,6 +458,17 @@ p3s_status p3s_gpu_device_name(char* buf, size_t cap) {
     });
 }
 
+p3s_status p3s_gpu_sm_count(int* out) {
+    if (!out) return fail(P3S_ERR_INVALID, "null argument");
+    return guarded([&] {
+        p3s::Device& d = p3s::Device::current();
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d.ordinal()) != cudaSuccess)
+            throw p3s::DeviceError("cudaDeviceGetAttribute failed");
+        *out = n;
+    });
+}
+
 #define NEED(...)                                                          \
     do {                                                                   \
         const void* ptrs_[] = {__VA_ARGS__};                               \
@@ -640,6 +651,12 @@ p3s_status p3s_pipeline_bilateral_kernel_sum(p3s_pipeline* p, int64_t* sum_ns, i
         *sum_ns = p->p->bilateral_kernel_ns(&n, reset != 0);
         if (count) *count = n;
     });
+}
+
+p3s_status p3s_pipeline_set_inpaint_ctas(p3s_pipeline* p, int ctas) {
+    NEED(p);
+    if (ctas < 0) return fail(P3S_ERR_INVALID, "inpaint CTAs must be >= 0");
+    return guarded([&] { p->p->set_inpaint_ctas(ctas); });
 }
 
 p3s_status p3s_pipeline_download(p3s_pipeline* p, uint8_t* depth, uint8_t* filtered,

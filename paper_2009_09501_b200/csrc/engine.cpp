@@ -268,6 +268,10 @@ struct Pipeline::Impl {
     long long acc_n = 0;
     long long acc_bil_ns = 0, acc_bil_n = 0;  // main bilateral kernel (without the fix-up)
     bool own_stream = false;
+    // CTAs of the cooperative inpaint (0: one per SM). Fewer leave SMs to other pipelines'
+    // frames: more aggregate throughput with several streams, longer single-frame latency.
+    int inpaint_ctas = 0;
+    void set_inpaint_ctas(int ctas);
 
     // Row-banded synchronous conversion (convert_image on pinned host planes). The frame is
     // cut into K bands of bilateral tile rows; Band::* are each band's END boundaries in the
@@ -830,7 +834,7 @@ struct Pipeline::Impl {
             ie[e].list2 = nullptr;
             ie[e].repair = reinterpret_cast<uint32_t*>(ipa);
         }
-        CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st));
+        CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st, inpaint_ctas));
     }
 
     // bil_count layout: [0, K) per-band uncertified counts, [K, 2K) tile-claim counters;
@@ -1013,6 +1017,17 @@ struct Pipeline::Impl {
         return true;
     }
 
+    void drop_graphs() {
+        CK(cudaStreamSynchronize(stream));
+        for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+        for (auto& g : timed_graphs) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+        timed_graphs.clear();
+        if (band_exec) cudaGraphExecDestroy(band_exec);
+        if (band_exec2) cudaGraphExecDestroy(band_exec2);
+        band_exec = band_exec2 = nullptr;
+    }
+
     StageTimings timings() {
         if (last_conv) return stage_times(conv_ev);
         if (last_slot < 0) return StageTimings{};
@@ -1192,6 +1207,13 @@ std::size_t Pipeline::frame_bytes() const { return 3 * impl_->plane(); }
 void Pipeline::run(const std::uint8_t* d_src, void* stream) {
     impl_->run(d_src, stream ? static_cast<cudaStream_t>(stream) : impl_->stream, false);
 }
+void Pipeline::Impl::set_inpaint_ctas(int ctas) {
+    if (ctas < 0) throw std::invalid_argument("inpaint CTAs must be >= 0");
+    if (ctas == inpaint_ctas) return;
+    drop_graphs();  // the launch configuration is baked into captured graphs
+    inpaint_ctas = ctas;
+}
+void Pipeline::set_inpaint_ctas(int ctas) { impl_->set_inpaint_ctas(ctas); }
 void Pipeline::run_timed(const std::uint8_t* d_src, void* stream) {
     impl_->run(d_src, stream ? static_cast<cudaStream_t>(stream) : impl_->stream, true);
 }

@@ -574,7 +574,7 @@ size_t inpaint_scratch_bytes(int w, int h) {
 }
 
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
-                    uint32_t* scratch, long long* stats, cudaStream_t st) {
+                    uint32_t* scratch, long long* stats, cudaStream_t st, int max_ctas) {
     (void)capacity;
     // scratch: ctl (2*3*(kPasses+1) u32, zeroed here); the per-pixel state words, tile
     // flags and work lists live in the engine-provided inpaint arena (InpaintEye.repair of
@@ -610,7 +610,8 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inpaint_tiles, kThreads, smem);
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-    const int blocks = per_sm * sm_count();
+    int blocks = per_sm * sm_count();
+    if (max_ctas > 0 && max_ctas < blocks) blocks = max_ctas;
     int w = gm.w, h = gm.h, tx = tiles_x, ty = tiles_y;
     void* args[] = {&L, &R, &wk, &w, &h, &tx, &ty, &scratch, &stats};
     static unsigned long long* dbg = nullptr;

@@ -148,7 +148,7 @@ struct InpaintEye {
 size_t inpaint_scratch_bytes(int w, int h);
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
                     uint32_t* scratch /* >= 128 words, zeroed by the call */, long long* stats,
-                    cudaStream_t st);
+                    cudaStream_t st, int max_ctas = 0 /* 0: one CTA per SM */);
 
 // Formats from materialised eyes (stereo_format.cpp:8-73).
 cudaError_t anaglyph(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
