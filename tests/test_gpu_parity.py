@@ -335,3 +335,25 @@ def test_banded_convert_boundaries(p3s, checker, w, h, block, sigma_s):
                 formats=7 if w % 2 == 0 else 5, base=20)
     for seed in (3, 4):
         compare_convert(p3s, checker, checker.synthetic_frame(w, h, seed), over)
+
+
+@pytest.mark.parametrize("ctas", [1, 5, 37])
+def test_inpaint_cta_cap_is_invisible(p3s, checker, ctas):
+    """Pipeline.set_inpaint_ctas (the throughput option) changes only how many CTAs run the
+    cooperative inpaint: multi-round damage (large parallax), graph replay after the change
+    and the timed path all give the oracle's bytes and pass statistics."""
+    w, h = 480, 270
+    cfg = p3s.Config(base=90, formats=1)
+    img = checker.synthetic_frame(w, h, 11)
+    ref = checker.convert(img, __import__("oracle").Cfg(base=90, formats=1), threads=NCPU)
+    pipe = p3s.Pipeline(w, h, cfg)
+    dbuf = p3s.DeviceBuffer(pipe.frame_bytes)
+    pipe.upload(img, dbuf.addr)
+    pipe.run(dbuf.addr)  # graph captured with one CTA per SM
+    pipe.set_inpaint_ctas(ctas)
+    for timed in (False, True, False):
+        pipe.run(dbuf.addr, timed=timed)
+        _, _, out = pipe.download()
+        assert np.array_equal(out, ref["anaglyph"])
+    with pytest.raises(p3s.P3SError):
+        pipe.set_inpaint_ctas(-1)
