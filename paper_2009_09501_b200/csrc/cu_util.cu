@@ -13,6 +13,27 @@ void record_event_any(cudaEvent_t e, cudaStream_t st) {
         cudaEventRecord(e, st);
 }
 
+namespace {
+// Zero up to kZeroRanges ranges of 4-byte words in one launch. cudaMemsetAsync nodes can be
+// queued behind bulk copies on a copy engine (the banded convert keeps PCIe copies in flight
+// while its kernels run); a kernel never is.
+__global__ void k_zero(ZeroRanges z) {
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (int r = 0; r < z.n; ++r) {
+        uint32_t* p = static_cast<uint32_t*>(z.p[r]);
+        for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < z.words[r]; i += stride) p[i] = 0u;
+    }
+}
+}  // namespace
+
+cudaError_t zero(const ZeroRanges& z, cudaStream_t st) {
+    unsigned most = 1;
+    for (int r = 0; r < z.n; ++r) most = z.words[r] > most ? z.words[r] : most;
+    const unsigned blocks = (most + 255) / 256 < 256u ? (most + 255) / 256 : 256u;
+    k_zero<<<blocks, 256, 0, st>>>(z);
+    return cudaGetLastError();
+}
+
 int sm_count() {
     static int cache[64] = {0};
     int dev = 0;

@@ -57,6 +57,28 @@ void wait_event_any(cudaStream_t st, cudaEvent_t e) {
           "cudaStreamWaitEvent");
 }
 
+int sm_count_cached() {
+    static thread_local int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+// cu::ZeroRanges from {pointer, 4-byte words} pairs
+cu::ZeroRanges zr(std::initializer_list<std::pair<void*, unsigned>> ranges) {
+    cu::ZeroRanges z{};
+    for (const auto& r : ranges) {
+        if (z.n == cu::kZeroRanges) throw std::logic_error("too many zero ranges");
+        z.p[z.n] = r.first;
+        z.words[z.n] = r.second;
+        ++z.n;
+    }
+    return z;
+}
+
 bool host_pinned(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -533,7 +555,7 @@ struct Pipeline::Impl {
 
     // ---- stage launchers ----
     void enq_depth(const uint8_t* s, cudaStream_t st) {
-        CK(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * dt.bx * dt.by, st));
+        CK(cu::zero(zr({{sums, 2u * dt.bx * dt.by}}), st));
         CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
                            dt.block, dt.bx, st));
         CK(cu::block_values(sums, gm, dt, values, st));
@@ -587,7 +609,7 @@ struct Pipeline::Impl {
     void enq_dibr_inpaint(const uint8_t* s, cudaStream_t st, cudaEvent_t mid) {
         cu::EyeOut eo[2];
         dibr_eyes(eo);
-        if (!backward) CK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), st));
+        if (!backward) CK(cu::zero(zr({{counts, 2u}}), st));
         CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols, backward,
                     eo[0], eo[1], st));
         if (mid) record_event(mid, st);
@@ -845,9 +867,9 @@ struct Pipeline::Impl {
         const int K = static_cast<int>(bands.size());
         wait_event_any(st, ev_in[0]);
         record_event(ev[0], st);
-        CK(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * dt.bx * dt.by, st));
-        CK(cudaMemsetAsync(bil_count, 0, 2 * K * sizeof(uint32_t), st));
-        if (!backward) CK(cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), st));
+        CK(cu::zero(zr({{sums, 2u * dt.bx * dt.by},
+                        {bil_count, 2u * K},
+                        {counts, backward ? 0u : 2u}}), st));
         const Band& b = bands[0];
         CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
                            dt.block, dt.bx, st, 0, b.dtile));
@@ -885,8 +907,10 @@ struct Pipeline::Impl {
             CK(cu::bilateral_sep_main(depth, luma, gm, radius, h_spatial.data(), range, filt, list,
                                       bil_count + k, bil_count + K + k, prev.btile, b.btile,
                                       sep_table, bs));
+            // a band lists a few hundred pixels: one CTA per SM, so the launch does not
+            // hold the SMs the next band's filter CTAs are waiting for
             CK(cu::bilateral_sep_fixup(depth, luma, gm, radius, spatial, range, filt, list,
-                                       bil_count + k, bs));
+                                       bil_count + k, bs, sm_count_cached()));
             if (back) {
                 CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols,
                             backward, eo[0], eo[1], bs, y0, y1));

@@ -857,10 +857,14 @@ cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
 template <int R>
 cudaError_t launch_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm,
                              const double* spatial_dev, const double* range, uint8_t* out,
-                             const uint32_t* list, const uint32_t* count, cudaStream_t st) {
-    // 4 warps per block up to R = 16 (static smem < 48 KB), 2 beyond
+                             const uint32_t* list, const uint32_t* count, cudaStream_t st,
+                             int max_ctas) {
+    // 4 warps per block up to R = 16 (static smem < 48 KB), 2 beyond; by default enough
+    // warps for every listed pixel of a 4K frame in one wave
     constexpr int WPB = R <= 16 ? 4 : 2;
-    k_bilateral_fixup2<R, WPB><<<sm_count() * 32 / WPB, WPB * 32, 0, st>>>(
+    int ctas = sm_count() * 32 / WPB;
+    if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
+    k_bilateral_fixup2<R, WPB><<<ctas, WPB * 32, 0, st>>>(
         depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
 }
@@ -877,7 +881,11 @@ cudaError_t bilateral_fast(const uint8_t* depth, const uint8_t* guide, Geom gm, 
         return e;
     }
     // count and the tile-claim counter (count[1]) start at zero
-    cudaError_t e = cudaMemsetAsync(count, 0, 2 * sizeof(uint32_t), st);
+    ZeroRanges z{};
+    z.p[0] = count;
+    z.words[0] = 2;
+    z.n = 1;
+    cudaError_t e = zero(z, st);
     if (e != cudaSuccess) return e;
     e = bilateral_sep_main(depth, guide, gm, radius, spatial_host, range, out, list, count,
                            count + 1, 0, -1, table, st);
@@ -909,10 +917,12 @@ cudaError_t bilateral_sep_main(const uint8_t* depth, const uint8_t* guide, Geom 
 
 cudaError_t bilateral_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                                 const double* spatial_dev, const double* range, uint8_t* out,
-                                const uint32_t* list, const uint32_t* count, cudaStream_t st) {
+                                const uint32_t* list, const uint32_t* count, cudaStream_t st,
+                                int max_ctas) {
 #define P3S_FIX(RR)                                                                          \
     case RR:                                                                                 \
-        return launch_sep_fixup<RR>(depth, guide, gm, spatial_dev, range, out, list, count, st);
+        return launch_sep_fixup<RR>(depth, guide, gm, spatial_dev, range, out, list, count, st, \
+                                    max_ctas);
     switch (radius) {
         P3S_FIX(7) P3S_FIX(8) P3S_FIX(9) P3S_FIX(10) P3S_FIX(11) P3S_FIX(12) P3S_FIX(13)
         P3S_FIX(14) P3S_FIX(15) P3S_FIX(16) P3S_FIX(17) P3S_FIX(18) P3S_FIX(19) P3S_FIX(20)

@@ -592,11 +592,15 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     wk.counters = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4);
     wk.heavy = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 64);
     wk.cap = static_cast<int>(2 * tiles);
-    cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * 3 * (kPasses + 1) * sizeof(uint32_t), st);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(flags, 0, 2 * tiles * 4, st);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(wk.counters, 0, 8 * sizeof(uint32_t), st);
+    ZeroRanges z{};
+    z.p[0] = scratch;
+    z.words[0] = 2 * 3 * (kPasses + 1);
+    z.p[1] = flags;
+    z.words[1] = static_cast<unsigned>(2 * tiles);
+    z.p[2] = wk.counters;
+    z.words[2] = 8;
+    z.n = 3;
+    cudaError_t e = zero(z, st);
     if (e != cudaSuccess) return e;
     const size_t smem = kWarps * sizeof(WarpSmem);
     static bool configured[64] = {false};

@@ -78,7 +78,8 @@ cudaError_t bilateral_sep_main(const uint8_t* depth, const uint8_t* guide, Geom 
                                int tile_row0, int tile_row1, const float* table, cudaStream_t st);
 cudaError_t bilateral_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                                 const double* spatial_dev, const double* range, uint8_t* out,
-                                const uint32_t* list, const uint32_t* count, cudaStream_t st);
+                                const uint32_t* list, const uint32_t* count, cudaStream_t st,
+                                int max_ctas = 0 /* 0: one warp per listed pixel of a 4K frame */);
 int bilateral_sep_tile_rows();
 // The certified kernel's replicated FP32 range table (bilateral_sep_table_bytes(), built once
 // per plan from the FP64 range table); table = nullptr builds it in every CTA instead.
@@ -86,6 +87,14 @@ size_t bilateral_sep_table_bytes();
 cudaError_t build_sep_table(const double* range, float* table, cudaStream_t st);
 // cudaEventRecord, or an event-record graph node while `st` is being captured.
 void record_event_any(cudaEvent_t e, cudaStream_t st);
+// Zero several ranges of whole 4-byte words (4-byte aligned) with one kernel launch.
+constexpr int kZeroRanges = 4;
+struct ZeroRanges {
+    void* p[kZeroRanges];
+    unsigned words[kZeroRanges];
+    int n;
+};
+cudaError_t zero(const ZeroRanges& z, cudaStream_t st);
 bool bilateral_fast_available(int radius);
 cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                       const double* spatial, const double* range, uint8_t* out, double* raw,
