@@ -314,6 +314,7 @@ struct Pipeline::Impl {
     // per band: upload part landed, depth part done (fork), band done (join), DIBR rows done
     std::vector<cudaEvent_t> ev_in, ev_fork, ev_join, ev_rows;
     cudaEvent_t ev_prior = nullptr, ev_d2h = nullptr, ev_start = nullptr;
+    std::vector<cudaEvent_t> ev_dbg;  // P3S_DEBUG_CONV: per band, filter start / end (timing)
     cudaGraphExec_t band_exec = nullptr, band_exec2 = nullptr;  // head, body
     cudaStream_t aux_stream = nullptr;  // side copies beside the frame's tail
     cudaEvent_t aux_done = nullptr;
@@ -793,6 +794,10 @@ struct Pipeline::Impl {
             for (auto& e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         for (auto* e : {&ev_prior, &ev_d2h, &ev_start}) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        if (std::getenv("P3S_DEBUG_CONV")) {
+            ev_dbg.assign(3 * K, nullptr);
+            for (auto& e : ev_dbg) CK(cudaEventCreate(&e));
+        }
         if (!conv_ev[0])
             for (auto& e : conv_ev) CK(cudaEventCreate(&e));
     }
@@ -902,13 +907,14 @@ struct Pipeline::Impl {
             }
             CK(cudaEventRecord(ev_fork[k], ds));
             CK(cudaStreamWaitEvent(bs, ev_fork[k], 0));
+            if (!ev_dbg.empty()) record_event(ev_dbg[3 * k], bs);
             const int y0 = prev.btile * TYb, y1 = std::min(h, b.btile * TYb);
             uint32_t* list = bil_list + static_cast<std::size_t>(y0) * w;
             CK(cu::bilateral_sep_main(depth, luma, gm, radius, h_spatial.data(), range, filt, list,
                                       bil_count + k, bil_count + K + k, prev.btile, b.btile,
                                       sep_table, bs));
-            // a band lists a few hundred pixels: one CTA per SM, so the launch does not
-            // hold the SMs the next band's filter CTAs are waiting for
+            if (!ev_dbg.empty()) record_event(ev_dbg[3 * k + 1], bs);
+            // a band lists a few hundred pixels: one CTA per SM is plenty
             CK(cu::bilateral_sep_fixup(depth, luma, gm, radius, spatial, range, filt, list,
                                        bil_count + k, bs, sm_count_cached()));
             if (back) {
@@ -916,6 +922,7 @@ struct Pipeline::Impl {
                             backward, eo[0], eo[1], bs, y0, y1));
                 record_event(ev_rows[k], bs);
             }
+            if (!ev_dbg.empty()) record_event(ev_dbg[3 * k + 2], bs);
             CK(cudaEventRecord(ev_join[k], bs));
             prev = b;
         }
@@ -1683,6 +1690,15 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
             cudaEventElapsedTime(&ab, dbg_ev[0], dbg_ev[1]);
             std::fprintf(stderr, "[p3s] gpu: start->ev0 %.1f us, ev5->end %.1f us, start->end %.1f us\n",
                          a0 * 1e3, b5 * 1e3, ab * 1e3);
+            for (std::size_t k = 0; 3 * k + 2 < p->ev_dbg.size(); ++k) {
+                float t0 = 0, t1 = 0, t2 = 0;
+                cudaEventElapsedTime(&t0, p->conv_ev[0], p->ev_dbg[3 * k]);
+                cudaEventElapsedTime(&t1, p->conv_ev[0], p->ev_dbg[3 * k + 1]);
+                cudaEventElapsedTime(&t2, p->conv_ev[0], p->ev_dbg[3 * k + 2]);
+                cudaGetLastError();
+                std::fprintf(stderr, "[p3s]   band %zu (tile rows to %d): start %.1f, filter end %.1f, end %.1f us\n",
+                             k, p->bands[k].btile, t0 * 1e3, t1 * 1e3, t2 * 1e3);
+            }
             const auto t2 = std::chrono::steady_clock::now();
             auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
             float e01 = 0, e06 = 0, e64 = 0, e05 = 0;

@@ -31,6 +31,6 @@ cfg = p3s.Config()
 for rep in range(3):
     t0 = time.perf_counter()
     for i in range(20):
-        L.p3s_convert(imgh.h, cfg.h, C.byref(res)); L.p3s_result_free(res)
+        p3s._check(L.p3s_convert(imgh.h, cfg.h, C.byref(res))); L.p3s_result_free(res)
     dt = (time.perf_counter() - t0) / 20
     print("p3s_convert: %.3f ms" % (dt * 1e3))
