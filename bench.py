@@ -42,10 +42,10 @@ W4K, H4K = 3840, 2160
 RING = 8
 SWEEP = [0, 2, 16, 30, 60, 120, 254, 510]
 L2_BYTES = 126 * 2**20
-# kernels per step on the default route (ncu launch list in profiles/): k_zero +
-# k_depth_front, k_block_values, k_upsample; k_zero + k_bilateral_sep, k_bilateral_fixup2;
-# k_zero + k_dibr_quad<0>; k_zero + k_inpaint_tiles (k_zero clears the per-frame counters)
-LAUNCHES_PER_STEP = 11
+# kernels per step on the default route (ncu launch list in profiles/): k_depth_front,
+# k_block_values, k_upsample, k_bilateral_sep, k_bilateral_fixup2, k_dibr_quad<0>,
+# k_inpaint_tiles (the per-frame counters are cleared by memsets on this path)
+LAUNCHES_PER_STEP = 7
 
 # The workload both arms measure (BASELINE.json metric on configs[1]); the arms add how
 # they ran it under "parallelism".

@@ -716,8 +716,16 @@ p3s_status video_create(int w, int h, const p3s_config* cfg, const int* devices,
                 p3s::Device& dev = p3s::Device::current();
                 p3s_video::Shard shard;
                 shard.device = d;
-                for (int i = 0; i < streams; ++i)
+                // several frames in flight: each cooperative inpaint takes a quarter of the
+                // SMs, leaving the rest to the other streams' filters (Pipeline::set_inpaint_ctas)
+                int sms = 0;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+                const char* env = std::getenv("P3S_VIDEO_INPAINT_CTAS");
+                const int ctas = env ? std::atoi(env) : (streams > 1 ? sms / 4 : 0);
+                for (int i = 0; i < streams; ++i) {
                     shard.pipes.push_back(std::make_unique<p3s::Pipeline>(w, h, cfg->cfg, dev));
+                    shard.pipes.back()->set_inpaint_ctas(ctas);
+                }
                 v->shards.push_back(std::move(shard));
             }
         } catch (...) {

@@ -16,7 +16,9 @@ void record_event_any(cudaEvent_t e, cudaStream_t st) {
 namespace {
 // Zero up to kZeroRanges ranges of 4-byte words in one launch. cudaMemsetAsync nodes can be
 // queued behind bulk copies on a copy engine (the banded convert keeps PCIe copies in flight
-// while its kernels run); a kernel never is.
+// while its kernels run); a kernel is not. The other way round, a kernel needs an SM slot,
+// which other streams' persistent kernels may hold for milliseconds, so multi-stream paths
+// keep the memsets.
 __global__ void k_zero(ZeroRanges z) {
     const unsigned stride = gridDim.x * blockDim.x;
     for (int r = 0; r < z.n; ++r) {
@@ -26,7 +28,15 @@ __global__ void k_zero(ZeroRanges z) {
 }
 }  // namespace
 
-cudaError_t zero(const ZeroRanges& z, cudaStream_t st) {
+cudaError_t zero(const ZeroRanges& z, cudaStream_t st, bool by_kernel) {
+    if (!by_kernel) {
+        for (int r = 0; r < z.n; ++r) {
+            if (!z.words[r]) continue;
+            const cudaError_t e = cudaMemsetAsync(z.p[r], 0, static_cast<size_t>(z.words[r]) * 4, st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     unsigned most = 1;
     for (int r = 0; r < z.n; ++r) most = z.words[r] > most ? z.words[r] : most;
     const unsigned blocks = (most + 255) / 256 < 256u ? (most + 255) / 256 : 256u;

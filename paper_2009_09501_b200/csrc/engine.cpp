@@ -845,7 +845,7 @@ struct Pipeline::Impl {
         }
     }
 
-    void enq_inpaint(cudaStream_t st) {
+    void enq_inpaint(cudaStream_t st, bool zero_by_kernel = false) {
         if (backward) return;
         cu::EyeOut eo[2];
         dibr_eyes(eo);
@@ -861,7 +861,8 @@ struct Pipeline::Impl {
             ie[e].list2 = nullptr;
             ie[e].repair = reinterpret_cast<uint32_t*>(ipa);
         }
-        CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st, inpaint_ctas));
+        CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st, inpaint_ctas,
+                       zero_by_kernel));
     }
 
     // bil_count layout: [0, K) per-band uncertified counts, [K, 2K) tile-claim counters;
@@ -874,7 +875,7 @@ struct Pipeline::Impl {
         record_event(ev[0], st);
         CK(cu::zero(zr({{sums, 2u * dt.bx * dt.by},
                         {bil_count, 2u * K},
-                        {counts, backward ? 0u : 2u}}), st));
+                        {counts, backward ? 0u : 2u}}), st, true));
         const Band& b = bands[0];
         CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
                            dt.block, dt.bx, st, 0, b.dtile));
@@ -933,7 +934,7 @@ struct Pipeline::Impl {
             CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols,
                         backward, eo[0], eo[1], st));
         record_event(ev[3], st);
-        enq_inpaint(st);
+        enq_inpaint(st, true);  // the copy engines are busy with the bands' downloads
         record_event(ev[4], st);
         enq_formats(st);
         record_event(ev[5], st);

@@ -574,7 +574,8 @@ size_t inpaint_scratch_bytes(int w, int h) {
 }
 
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
-                    uint32_t* scratch, long long* stats, cudaStream_t st, int max_ctas) {
+                    uint32_t* scratch, long long* stats, cudaStream_t st, int max_ctas,
+                    bool zero_by_kernel) {
     (void)capacity;
     // scratch: ctl (2*3*(kPasses+1) u32, zeroed here); the per-pixel state words, tile
     // flags and work lists live in the engine-provided inpaint arena (InpaintEye.repair of
@@ -600,7 +601,7 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     z.p[2] = wk.counters;
     z.words[2] = 8;
     z.n = 3;
-    cudaError_t e = zero(z, st);
+    cudaError_t e = zero(z, st, zero_by_kernel);
     if (e != cudaSuccess) return e;
     const size_t smem = kWarps * sizeof(WarpSmem);
     static bool configured[64] = {false};

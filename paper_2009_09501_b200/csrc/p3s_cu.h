@@ -87,14 +87,16 @@ size_t bilateral_sep_table_bytes();
 cudaError_t build_sep_table(const double* range, float* table, cudaStream_t st);
 // cudaEventRecord, or an event-record graph node while `st` is being captured.
 void record_event_any(cudaEvent_t e, cudaStream_t st);
-// Zero several ranges of whole 4-byte words (4-byte aligned) with one kernel launch.
+// Zero several ranges of whole 4-byte words (4-byte aligned): one kernel launch when
+// by_kernel (copy engines busy with PCIe traffic), else one memset per range (SMs busy
+// with other streams' kernels).
 constexpr int kZeroRanges = 4;
 struct ZeroRanges {
     void* p[kZeroRanges];
     unsigned words[kZeroRanges];
     int n;
 };
-cudaError_t zero(const ZeroRanges& z, cudaStream_t st);
+cudaError_t zero(const ZeroRanges& z, cudaStream_t st, bool by_kernel = false);
 bool bilateral_fast_available(int radius);
 cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int radius,
                       const double* spatial, const double* range, uint8_t* out, double* raw,
@@ -157,7 +159,8 @@ struct InpaintEye {
 size_t inpaint_scratch_bytes(int w, int h);
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
                     uint32_t* scratch /* >= 128 words, zeroed by the call */, long long* stats,
-                    cudaStream_t st, int max_ctas = 0 /* 0: one CTA per SM */);
+                    cudaStream_t st, int max_ctas = 0 /* 0: one CTA per SM */,
+                    bool zero_by_kernel = false);
 
 // Formats from materialised eyes (stereo_format.cpp:8-73).
 cudaError_t anaglyph(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
