@@ -1,5 +1,6 @@
 """compute-sanitizer over a small-frame workload covering every kernel route
-(tools/sanitize.py): no memory errors, no shared-memory races. SURVEY.md §4.2 item 5."""
+(tools/sanitize.py): no memory errors, no shared-memory races, no barrier misuse, no reads of
+uninitialised device memory. SURVEY.md §4.2 item 5."""
 import os
 import shutil
 import subprocess
@@ -13,7 +14,7 @@ pytestmark = pytest.mark.gpu
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_sanitizer_clean(tool):
     if not os.path.exists(SAN):
         pytest.fail("compute-sanitizer not found")
