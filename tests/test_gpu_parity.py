@@ -357,3 +357,21 @@ def test_inpaint_cta_cap_is_invisible(p3s, checker, ctas):
         assert np.array_equal(out, ref["anaglyph"])
     with pytest.raises(p3s.P3SError):
         pipe.set_inpaint_ctas(-1)
+
+
+def test_banded_convert_random_configs(p3s, checker):
+    """Random configurations through the row-banded p3s_convert (frames tall enough for
+    several bands): every route, both DIBR modes, random parallax, depth blocks, radii and
+    depth weights, against the oracle."""
+    rng = np.random.default_rng(2024)
+    for i in range(8):
+        w = int(rng.integers(200, 641)) & ~1
+        h = int(rng.integers(300, 721))
+        over = dict(base=int(rng.choice([-1, 0, 8, 30, 64, 120])),
+                    pop_threshold=int(rng.integers(0, 256)),
+                    sigma_spatial=float(rng.choice([3.2, 5.0, 8.0, 11.5])),
+                    sigma_range=float(rng.choice([6.0, 16.0, 40.0])),
+                    depth_block=int(rng.integers(4, 48)), alpha=float(rng.choice([0.0, 0.5, 0.7])),
+                    beta=0.3, mode=int(rng.integers(0, 2)), formats=int(rng.choice([1, 2, 4, 7])))
+        img = checker.synthetic_frame(w, h, 100 + i)
+        compare_convert(p3s, checker, img, over)
