@@ -428,8 +428,10 @@ void oracle_inpaint(const uint8_t* r, const uint8_t* g, const uint8_t* b, const 
     if (cnt == 0) return;
     uint8_t* dmg = (uint8_t*)malloc(n);
     for (size_t i = 0; i < n; ++i) dmg[i] = mask[i] != 0;
-    size_t* list = (size_t*)malloc(sizeof(size_t) * cnt);
-    size_t* keep = (size_t*)malloc(sizeof(size_t) * cnt);
+    /* two damaged-pixel lists, swapped each pass (current / still damaged) */
+    size_t* bufs[2] = {(size_t*)malloc(sizeof(size_t) * cnt), (size_t*)malloc(sizeof(size_t) * cnt)};
+    int cur = 0;
+    size_t* list = bufs[0];
     uint8_t* rep = (uint8_t*)malloc(4 * cnt);
     size_t m = 0;
     for (size_t i = 0; i < n; ++i)
@@ -437,6 +439,7 @@ void oracle_inpaint(const uint8_t* r, const uint8_t* g, const uint8_t* b, const 
     size_t remaining = m;
     while (remaining > 0) {
         size_t nrep = 0, nkeep = 0;
+        size_t* keep = bufs[cur ^ 1];
         for (size_t k = 0; k < remaining; ++k) {
             const size_t idx = list[k];
             const int x = (int)(idx % (size_t)w), y = (int)(idx / (size_t)w);
@@ -471,7 +474,8 @@ void oracle_inpaint(const uint8_t* r, const uint8_t* g, const uint8_t* b, const 
         }
         stats[0] += 1;
         stats[1] += (int64_t)nrep;
-        size_t* t = list; list = keep; keep = t;
+        cur ^= 1;
+        list = bufs[cur];
         remaining = nkeep;
         if (nrep == 0 && remaining > 0) {
             for (size_t k = 0; k < remaining; ++k) {
@@ -482,7 +486,7 @@ void oracle_inpaint(const uint8_t* r, const uint8_t* g, const uint8_t* b, const 
             remaining = 0;
         }
     }
-    free(dmg); free(list); free(keep); free(rep);
+    free(dmg); free(bufs[0]); free(bufs[1]); free(rep);
 }
 
 /* stereo_format.cpp:8-21. */
