@@ -7,7 +7,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import load_case
+from conftest import ROOT, load_case
 
 pytestmark = pytest.mark.gpu
 
@@ -375,3 +375,14 @@ def test_banded_convert_random_configs(p3s, checker):
                     beta=0.3, mode=int(rng.integers(0, 2)), formats=int(rng.choice([1, 2, 4, 7])))
         img = checker.synthetic_frame(w, h, 100 + i)
         compare_convert(p3s, checker, img, over)
+
+
+def test_convert_is_deterministic_across_calls():
+    """tools/stress_convert.py: back-to-back p3s_convert calls over alternating frames, sizes
+    and routes (plan switches, graph replays, the banded early downloads and host patch)
+    return the same bytes every time."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "stress_convert.py"), "--calls", "80"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "stress ok" in r.stdout, r.stdout + r.stderr
