@@ -386,3 +386,33 @@ def test_convert_is_deterministic_across_calls():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "stress_convert.py"), "--calls", "80"],
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "stress ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_concurrent_convert_threads(p3s, checker):
+    """p3s_convert from several host threads at once (reference capi.cpp: thread-safe on
+    distinct handles): each thread gets its own plans and streams on the device, the banded
+    schedules of different threads overlap on the GPU, and every result equals the
+    single-threaded one."""
+    import threading
+    frames = [checker.synthetic_frame(640 + 32 * i, 480 + 16 * i, 40 + i) for i in range(4)]
+    cfgs = [p3s.Config(), p3s.Config(formats=7, base=24), p3s.Config(mode=1), p3s.Config(formats=4)]
+    expect = [p3s.convert(f, c) for f, c in zip(frames, cfgs)]
+    errors = []
+
+    def work(k):
+        try:
+            for rep in range(6):
+                i = (k + rep) % 4
+                out = p3s.convert(frames[i], cfgs[i])
+                for key in ("anaglyph", "hsbs", "fsbs", "depth", "filtered"):
+                    if key in expect[i] and not np.array_equal(out[key], expect[i][key]):
+                        errors.append((k, rep, key))
+        except Exception as e:  # noqa: BLE001 - surfaced by the assert below
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:5]
