@@ -35,6 +35,19 @@ struct StageTimings {
     }
 };
 
+// Row-band plan of the synchronous convert: where
+// each band ends, in the units of every stage. Host-only arithmetic (no device needed);
+// empty when the frame is too short for two bands.
+struct BandEnd {
+    int in_rows;  // upload rows [0, in_rows) are needed
+    int dtile;    // depth-front tile rows (16 image rows each) [0, dtile)
+    int brow;     // block rows [0, brow)
+    int urow;     // depth rows [0, urow)
+    int btile;    // filter tile rows (128 image rows each) [0, btile)
+};
+std::vector<BandEnd> band_plan(int width, int height, int radius, int depth_block,
+                               const char* ends_override = nullptr);
+
 // Reference pipeline.hpp:29-35.
 struct ConversionResult {
     std::map<StereoFormat, ImageRGB8> outputs;  // exactly the requested formats

@@ -41,6 +41,11 @@ P3S_API int p3s_gpu_device_count(void);
 /* Binds the calling thread to a CUDA device (all later calls on this thread use it). */
 P3S_API p3s_status p3s_gpu_set_device(int ordinal);
 P3S_API p3s_status p3s_gpu_device_name(char* buf, size_t cap);
+/* Row-band plan of the synchronous p3s_convert schedule (host arithmetic, no device
+ * needed): writes up to cap bands as 5 ints each (upload rows, depth-front tile rows,
+ * block rows, depth rows, filter tile rows: where the band ENDS) and returns the band count
+ * (0: the frame is converted in one piece), or -1 with p3s_last_error set. */
+P3S_API int p3s_gpu_band_plan(int w, int h, const p3s_config* cfg, int* out, int cap);
 /* Streaming multiprocessors of the calling thread's device. */
 P3S_API p3s_status p3s_gpu_sm_count(int* out);
 

@@ -122,6 +122,7 @@ _SIGS = {
     "p3s_gpu_set_device": (C.c_int, [C.c_int]),
     "p3s_gpu_device_name": (C.c_int, [C.c_char_p, C.c_size_t]),
     "p3s_gpu_sm_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "p3s_gpu_band_plan": (C.c_int, [C.c_int, C.c_int, vp, C.POINTER(C.c_int), C.c_int]),
     "p3s_pipeline_set_inpaint_ctas": (C.c_int, [vp, C.c_int]),
     "p3s_gpu_luma": (C.c_int, [u8p, u8p, u8p, C.c_int, C.c_int, u8p]),
     "p3s_gpu_block_depth": (C.c_int, [u8p, u8p, u8p, C.c_int, C.c_int, vp, f64p]),
@@ -212,6 +213,16 @@ def device_count() -> int:
 
 def set_device(ordinal: int) -> None:
     _check(lib().p3s_gpu_set_device(ordinal))
+
+
+def band_plan(w: int, h: int, cfg: "Config"):
+    """Row bands of the synchronous p3s_convert schedule: a list of (upload rows, depth
+    tile rows, block rows, depth rows, filter tile rows) band ends; [] = one piece."""
+    buf = (C.c_int * (5 * 64))()
+    n = lib().p3s_gpu_band_plan(w, h, cfg.h, buf, 64)
+    if n < 0:
+        raise P3SError(1, lib().p3s_last_error().decode())
+    return [tuple(buf[5 * i:5 * i + 5]) for i in range(n)]
 
 
 def sm_count() -> int:

@@ -458,6 +458,25 @@ p3s_status p3s_gpu_device_name(char* buf, size_t cap) {
     });
 }
 
+int p3s_gpu_band_plan(int w, int h, const p3s_config* cfg, int* out, int cap) {
+    if (!cfg || (cap > 0 && !out) || w <= 0 || h <= 0) {
+        fail(P3S_ERR_INVALID, "invalid argument");
+        return -1;
+    }
+    int n = -1;
+    const p3s_status st = guarded([&] {
+        cfg->cfg.validate();
+        const int radius = static_cast<int>(std::ceil(2.0 * cfg->cfg.sigma_spatial));
+        const std::vector<p3s::BandEnd> b = p3s::band_plan(w, h, radius, cfg->cfg.depth_block);
+        for (std::size_t i = 0; i < b.size() && static_cast<int>(i) < cap; ++i) {
+            const int v[5] = {b[i].in_rows, b[i].dtile, b[i].brow, b[i].urow, b[i].btile};
+            for (int j = 0; j < 5; ++j) out[5 * i + j] = v[j];
+        }
+        n = static_cast<int>(b.size());
+    });
+    return st == P3S_OK ? n : -1;
+}
+
 p3s_status p3s_gpu_sm_count(int* out) {
     if (!out) return fail(P3S_ERR_INVALID, "null argument");
     return guarded([&] {

@@ -238,6 +238,58 @@ std::int64_t ms_to_ns(float ms) { return static_cast<std::int64_t>(std::llround(
 
 }  // namespace
 
+// Row bands of the synchronous convert (Pipeline::Impl::plan_bands, DESIGN.md "Banded
+// synchronous convert"): each entry is where a band ENDS in the units of every stage.
+// Empty when the frame is too short for two bands.
+std::vector<BandEnd> band_plan(int w, int h, int radius, int blk, const char* ends_env) {
+    (void)w;
+    std::vector<BandEnd> bands;
+    if (!cu::bilateral_fast_available(radius)) return bands;  // the band kernels are the certified ones
+    const int TYb = cu::bilateral_sep_tile_rows(), TD = cu::depth_tile_rows();
+    const int tiles_y = (h + TYb - 1) / TYb, dtiles = (h + TD - 1) / TD;
+    const int by = (h + blk - 1) / blk;
+    std::vector<int> ri0, ri1;
+    std::vector<double> rf;
+    locate_axis(h, by, blk, ri0, ri1, rf);
+    // band ends: a thin first band (short wait for its upload part), then 4 tile rows
+    // per band (the upload of the next band outruns this band's filter ~3x), then
+    // halving bands at the bottom: a band's download (~1/3 of its filter time) must hide
+    // under the next band's filter, and the last one's under the inpaint
+    std::vector<int> ends = {1};
+    if (ends_env) {  // e.g. "1,4,8,12,14,16" (tuning)
+        ends.clear();
+        for (const char* q = ends_env; *q;) {
+            ends.push_back(std::atoi(q));
+            while (*q && *q != ',') ++q;
+            if (*q) ++q;
+        }
+    } else {
+        const int tail_start = tiles_y - 5;  // the last 5 tile rows: 2, 2, 1
+        for (int t = 4; t < tail_start; t += 4) ends.push_back(t);
+        for (int t : {tiles_y - 5, tiles_y - 3, tiles_y - 1})
+            if (t > ends.back()) ends.push_back(t);
+    }
+    auto urows = [&](int bb) {
+        return static_cast<int>(std::lower_bound(ri1.begin(), ri1.end(), bb) - ri1.begin());
+    };
+    for (int T : ends) {
+        if (T >= tiles_y || (!bands.empty() && T <= bands.back().btile)) break;
+        const int need = T * TYb + radius;  // depth / luma rows the band's filter reads
+        if (need >= h) break;
+        int b = bands.empty() ? 1 : bands.back().brow;
+        while (b < by && urows(b) < need) ++b;  // fewest block rows whose rows cover it
+        if (b >= by) break;
+        const int dtl = (b * blk + TD - 1) / TD;  // depth tiles completing block rows < b
+        if (dtl * TD >= h) break;
+        bands.push_back(BandEnd{std::min(h, dtl * TD + 1), dtl, b, urows(b), T});
+    }
+    if (bands.empty()) return bands;
+    constexpr std::size_t kMaxBands = 31;  // Pipeline::Impl::kBilSlots / 2 - 1
+    while (bands.size() > kMaxBands) bands.pop_back();
+    bands.push_back(BandEnd{h, dtiles, by, h, tiles_y});
+    return bands;
+}
+
 // ==========================================================================================
 // Pipeline::Impl — one plan
 // ==========================================================================================
@@ -356,7 +408,7 @@ struct Pipeline::Impl {
         std::vector<double> cf, rf;
         locate_axis(w, bx, blk, ci0, ci1, cf);
         locate_axis(h, by, blk, ri0, ri1, rf);
-        plan_bands(ri1, by, blk);
+        plan_bands(blk);
         h_spatial = spatial_table(cfg, radius);
         double h_range[256], h_shift[256];
         range_table(cfg, h_range);
@@ -457,51 +509,14 @@ struct Pipeline::Impl {
         dt.row_denom = h > 1 ? h - 1 : 1;
     }
 
-    void plan_bands(const std::vector<int>& ri1, int by, int blk) {
+    void plan_bands(int blk) {
         band_ok = false;
         bands.clear();
         const char* env = std::getenv("P3S_BANDED");
         if (env && std::atoi(env) == 0) return;
-        if (!cu::bilateral_fast_available(radius)) return;
-        const int TYb = cu::bilateral_sep_tile_rows(), TD = cu::depth_tile_rows();
-        const int tiles_y = (h + TYb - 1) / TYb, dtiles = (h + TD - 1) / TD;
-        // band ends: a thin first band (short wait for its upload part), then 4 tile rows
-        // per band (the upload of the next band outruns this band's filter ~3x), then
-        // halving bands at the bottom: a band's download (~1/3 of its filter time) must hide
-        // under the next band's filter, and the last one's under the inpaint
-        std::vector<int> ends = {1};
-        const char* be = std::getenv("P3S_BAND_ENDS");  // e.g. "1,4,8,12,14,16" (tuning)
-        if (be) {
-            ends.clear();
-            for (const char* q = be; *q;) {
-                ends.push_back(std::atoi(q));
-                while (*q && *q != ',') ++q;
-                if (*q) ++q;
-            }
-        } else {
-            const int tail_start = tiles_y - 5;  // the last 5 tile rows: 2, 2, 1
-            for (int t = 4; t < tail_start; t += 4) ends.push_back(t);
-            for (int t : {tiles_y - 5, tiles_y - 3, tiles_y - 1})
-                if (t > ends.back()) ends.push_back(t);
-        }
-        auto urows = [&](int bb) {
-            return static_cast<int>(std::lower_bound(ri1.begin(), ri1.end(), bb) - ri1.begin());
-        };
-        for (int T : ends) {
-            if (T >= tiles_y) break;
-            const int need = T * TYb + radius;  // depth / luma rows the band's filter reads
-            if (need >= h) break;
-            int b = bands.empty() ? 1 : bands.back().brow;
-            while (b < by && urows(b) < need) ++b;  // fewest block rows whose rows cover it
-            if (b >= by) break;
-            const int dtl = (b * blk + TD - 1) / TD;  // depth tiles completing block rows < b
-            if (dtl * TD >= h) break;
-            bands.push_back(Band{std::min(h, dtl * TD + 1), dtl, b, urows(b), T});
-        }
-        if (bands.empty()) return;
-        while (bands.size() > kBilSlots / 2 - 1) bands.pop_back();
-        bands.push_back(Band{h, dtiles, by, h, tiles_y});
-        band_ok = true;
+        for (const BandEnd& e : band_plan(w, h, radius, blk, std::getenv("P3S_BAND_ENDS")))
+            bands.push_back(Band{e.in_rows, e.dtile, e.brow, e.urow, e.btile});
+        band_ok = !bands.empty();
     }
 
     ~Impl() {
