@@ -47,6 +47,9 @@ struct BandEnd {
 };
 std::vector<BandEnd> band_plan(int width, int height, int radius, int depth_block,
                                const char* ends_override = nullptr);
+// Whether plans of this width/config use the host-verified integer DIBR column tables
+// (dibr.cpp:33-41 as x + off + (x >= X)); false keeps the FP64 device path. Host only.
+bool dibr_integer_columns(int width, const ConversionConfig& cfg);
 
 // Reference pipeline.hpp:29-35.
 struct ConversionResult {

@@ -46,6 +46,9 @@ P3S_API p3s_status p3s_gpu_device_name(char* buf, size_t cap);
  * block rows, depth rows, filter tile rows: where the band ENDS) and returns the band count
  * (0: the frame is converted in one piece), or -1 with p3s_last_error set. */
 P3S_API int p3s_gpu_band_plan(int w, int h, const p3s_config* cfg, int* out, int cap);
+/* 1 if conversions of width w with cfg use the host-verified integer DIBR column tables,
+ * 0 if they keep the FP64 device path, -1 on invalid arguments (host only). */
+P3S_API int p3s_gpu_dibr_integer_columns(int w, const p3s_config* cfg);
 /* Streaming multiprocessors of the calling thread's device. */
 P3S_API p3s_status p3s_gpu_sm_count(int* out);
 

@@ -123,6 +123,7 @@ _SIGS = {
     "p3s_gpu_device_name": (C.c_int, [C.c_char_p, C.c_size_t]),
     "p3s_gpu_sm_count": (C.c_int, [C.POINTER(C.c_int)]),
     "p3s_gpu_band_plan": (C.c_int, [C.c_int, C.c_int, vp, C.POINTER(C.c_int), C.c_int]),
+    "p3s_gpu_dibr_integer_columns": (C.c_int, [C.c_int, vp]),
     "p3s_pipeline_set_inpaint_ctas": (C.c_int, [vp, C.c_int]),
     "p3s_gpu_luma": (C.c_int, [u8p, u8p, u8p, C.c_int, C.c_int, u8p]),
     "p3s_gpu_block_depth": (C.c_int, [u8p, u8p, u8p, C.c_int, C.c_int, vp, f64p]),
@@ -223,6 +224,14 @@ def band_plan(w: int, h: int, cfg: "Config"):
     if n < 0:
         raise P3SError(1, lib().p3s_last_error().decode())
     return [tuple(buf[5 * i:5 * i + 5]) for i in range(n)]
+
+
+def dibr_integer_columns(w: int, cfg: "Config") -> bool:
+    """True when plans of width w use the host-verified integer DIBR column tables."""
+    r = lib().p3s_gpu_dibr_integer_columns(w, cfg.h)
+    if r < 0:
+        raise P3SError(1, lib().p3s_last_error().decode())
+    return bool(r)
 
 
 def sm_count() -> int:

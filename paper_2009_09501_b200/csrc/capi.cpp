@@ -477,6 +477,19 @@ int p3s_gpu_band_plan(int w, int h, const p3s_config* cfg, int* out, int cap) {
     return st == P3S_OK ? n : -1;
 }
 
+int p3s_gpu_dibr_integer_columns(int w, const p3s_config* cfg) {
+    if (!cfg || w <= 0) {
+        fail(P3S_ERR_INVALID, "invalid argument");
+        return -1;
+    }
+    int r = -1;
+    const p3s_status st = guarded([&] {
+        cfg->cfg.validate();
+        r = p3s::dibr_integer_columns(w, cfg->cfg) ? 1 : 0;
+    });
+    return st == P3S_OK ? r : -1;
+}
+
 p3s_status p3s_gpu_sm_count(int* out) {
     if (!out) return fail(P3S_ERR_INVALID, "null argument");
     return guarded([&] {

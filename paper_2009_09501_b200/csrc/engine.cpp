@@ -290,6 +290,15 @@ std::vector<BandEnd> band_plan(int w, int h, int radius, int blk, const char* en
     return bands;
 }
 
+// Whether a plan of this width and config uses the integer DIBR column tables (true) or
+// the FP64 device path (false): dibr_col_table's derivation + verification, host only.
+bool dibr_integer_columns(int w, const ConversionConfig& cfg) {
+    double sh[256];
+    shift_table(cfg.effective_base(w), cfg.pop_threshold, sh);
+    int cols[256][4];
+    return dibr_col_table(sh, w, cols);
+}
+
 // ==========================================================================================
 // Pipeline::Impl — one plan
 // ==========================================================================================

@@ -1,4 +1,4 @@
-"""CPU: the row-band plan of the synchronous p3s_convert schedule (engine.cpp band_plan,
+"""CPU: host-side plan logic. The row-band plan of the synchronous p3s_convert schedule (engine.cpp band_plan,
 DESIGN.md "Banded synchronous convert") respects the reference's dependency cones for every
 band it cuts: the band's filter rows +-r are covered by the depth rows computed so far, those
 depth rows only use block rows already valued (depth.cpp:76-121 locate()), those block rows
@@ -80,3 +80,18 @@ def test_random_plans(p3s):
 def test_short_frames_are_one_piece(p3s):
     assert p3s.band_plan(640, 64, p3s.Config()) == []
     assert p3s.band_plan(640, 128 + 16, p3s.Config()) == []
+
+
+def test_dibr_integer_column_tables_verify(p3s):
+    """engine.cpp dibr_col_table: for every depth and direction, the reference's truncated
+    destination column trunc(fl(x +- sigma_d)) (dibr.cpp:33-41) is x + off + (x >= X), except
+    0 at one x; the host derives (off, X, z) from the exact double evaluation of every x and
+    verifies it. A sample of widths, bases and thresholds must verify (a failure would only
+    route the plan to the FP64 device path, but it would be a regression)."""
+    rng = np.random.default_rng(3)
+    cases = [(3840, -1, 150), (1920, -1, 150), (7680, -1, 150), (15360, 120, 150)]
+    cases += [(int(rng.integers(1, 20000)), int(rng.choice([0, 2, 30, 60, 254, 510, 1000])),
+               int(rng.integers(0, 256))) for _ in range(200)]
+    for w, base, t in cases:
+        cfg = p3s.Config(base=base, pop_threshold=t)
+        assert p3s.dibr_integer_columns(w, cfg), (w, base, t)
