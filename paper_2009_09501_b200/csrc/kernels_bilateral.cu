@@ -759,14 +759,11 @@ cudaError_t launch_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm, in
     for (int i = n; i < N; ++i) sp.s[i] = 0.0;
     const int SW = kTX + 2 * R, SH = kTY + 2 * R;
     const size_t smem = kRangeEntries * kRangeCopies * 8 + static_cast<size_t>(SW) * SH * 2;
-    static int configured_dev[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !configured_dev[dev]) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [] {
         cudaFuncSetAttribute(k_bilateral_tiled<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
-        configured_dev[dev] = 1;
-    }
+    });
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_tiled<N>, kNW * 32, smem);
     if (per_sm < 1) per_sm = 1;
@@ -789,14 +786,11 @@ cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
     const size_t smem = kSignedEntries * kRangeCopies * 8 + static_cast<size_t>(SW) * SH * 4;
-    static int configured_dev[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !configured_dev[dev]) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [] {
         cudaFuncSetAttribute(k_bilateral_r<R, P, NW, MINB, N>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured_dev[dev] = 1;
-    }
+    });
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_r<R, P, NW, MINB, N>,
                                                   NW * 32, smem);
@@ -831,14 +825,11 @@ cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
     constexpr int SWR = (RO + SW + 15) / 16 * 16;
     const size_t smem = kSepEntries * kF32Copies * 4 + (static_cast<size_t>(SW) * SH * 4 + 15) / 16 * 16 +
                         2 * static_cast<size_t>(SWR) * SH;
-    static int configured_dev[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !configured_dev[dev]) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [smem] {
         cudaFuncSetAttribute(k_bilateral_sep<R, P, NW, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        configured_dev[dev] = 1;
-    }
+    });
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_sep<R, P, NW, U>, NW * 32, smem);
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;

@@ -574,16 +574,13 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
     const int wpad = (gm.w + 15) & ~15;
     const size_t smem = static_cast<size_t>(wpad) * (backward ? 4 : 12);
     constexpr size_t kMax = kDibrMaxSmem;
-    static bool configured[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !configured[dev]) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [] {
         cudaFuncSetAttribute(k_dibr<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         cudaFuncSetAttribute(k_dibr<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         cudaFuncSetAttribute(k_dibr<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         cudaFuncSetAttribute(k_dibr<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
-        configured[dev] = true;
-    }
+    });
     if (smem > kMax) return cudaErrorInvalidValue;
     // the fused anaglyph route: left R and right G/B only, bit masks, lists
     const bool ana = left.plane[0] && !left.plane[1] && !left.plane[2] && !right.plane[0] &&
@@ -605,12 +602,11 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 <= kMax) {
         void (*qk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
                    const int4*, EyeOut, EyeOut, int, int) = ana ? k_dibr_quad<0> : k_dibr_quad<1>;
-        static bool qconf[64] = {false};
-        if (dev < 64 && !qconf[dev]) {
+        static std::atomic<unsigned long long> qconf{0};
+        once_per_device(qconf, [] {
             cudaFuncSetAttribute(k_dibr_quad<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
             cudaFuncSetAttribute(k_dibr_quad<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
-            qconf[dev] = true;
-        }
+        });
         const size_t qsmem = static_cast<size_t>(wpad) * 13;
         int qper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, qk, 256, qsmem);
@@ -624,12 +620,11 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         vec != 0 && static_cast<size_t>(wpad) * (backward ? 7 : 15) + 16 <= kMax) {
         void (*vk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
                    const int4*, EyeOut, EyeOut, int, int) = backward ? k_dibr_ana<true> : k_dibr_ana<false>;
-        static bool vconf[64] = {false};
-        if (dev < 64 && !vconf[dev]) {
+        static std::atomic<unsigned long long> vconf{0};
+        once_per_device(vconf, [] {
             cudaFuncSetAttribute(k_dibr_ana<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
             cudaFuncSetAttribute(k_dibr_ana<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
-            vconf[dev] = true;
-        }
+        });
         const size_t vsmem = static_cast<size_t>(wpad) * (backward ? 7 : 15) + 16;
         int vper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, vk, 256, vsmem);

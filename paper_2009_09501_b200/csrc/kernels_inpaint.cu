@@ -604,14 +604,11 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     cudaError_t e = zero(z, st, zero_by_kernel);
     if (e != cudaSuccess) return e;
     const size_t smem = kWarps * sizeof(WarpSmem);
-    static bool configured[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !configured[dev]) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [smem] {
         cudaFuncSetAttribute(k_inpaint_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        configured[dev] = true;
-    }
+    });
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inpaint_tiles, kThreads, smem);
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;

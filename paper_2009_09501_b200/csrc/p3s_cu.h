@@ -7,6 +7,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 namespace p3s {
@@ -87,6 +89,18 @@ size_t bilateral_sep_table_bytes();
 cudaError_t build_sep_table(const double* range, float* table, cudaStream_t st);
 // cudaEventRecord, or an event-record graph node while `st` is being captured.
 void record_event_any(cudaEvent_t e, cudaStream_t st);
+// Per-device one-time launch setup (cudaFuncSetAttribute): runs `setup` until it has
+// completed once on the current device. Host threads may race into it; the setup is
+// idempotent and the device is marked only after it ran, so no launch can see it missing.
+template <class F>
+inline void once_per_device(std::atomic<unsigned long long>& done, F&& setup) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = dev >= 0 && dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return;
+    setup();
+    if (bit) done.fetch_or(bit, std::memory_order_release);
+}
 // Zero several ranges of whole 4-byte words (4-byte aligned): one kernel launch when
 // by_kernel (copy engines busy with PCIe traffic), else one memset per range (SMs busy
 // with other streams' kernels).
