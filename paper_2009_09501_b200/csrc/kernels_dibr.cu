@@ -411,9 +411,10 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                 const uint4 kr = reinterpret_cast<const uint4*>(keyR)[q];
                 const uint32_t kla[4] = {kl.x, kl.y, kl.z, kl.w}, kra[4] = {kr.x, kr.y, kr.z, kr.w};
                 uint32_t oR = 0, oG = 0, oB = 0, lG = 0, lB = 0, rR = 0;
+                // pixels x >= w have zero keys (never splatted); their mask bits are dropped
+                // below instead of testing x per pixel
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    if (x0 + k >= w) continue;
                     if (kla[k]) {
                         const uint32_t v = s_rgb[kXMask - (kla[k] & kXMask)];
                         oR |= (v & 0xFFu) << (8 * k);
@@ -432,6 +433,11 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                     } else {
                         mR |= 1u << k;
                     }
+                }
+                if (x0 + 4 > w) {
+                    const unsigned valid = x0 >= w ? 0u : (1u << (w - x0)) - 1u;
+                    mL &= valid;
+                    mR &= valid;
                 }
                 // never write past w: in the direct-FSBS route the left eye's row continues
                 // with the right eye's pixels
