@@ -425,41 +425,24 @@ def main():
             d = p3s.DeviceBuffer(p8.frame_bytes)
             p8.upload(o8.synthetic_frame(W8, H8, frame_seed(1000 + 4 * rank + i)), d.addr)
             ring8.append(d)
-        # the 8 frames are pipelined over 2 plans (graph replay; inpaint on a quarter of the
-        # SMs, as in the 4K throughput lanes); a separate timed pass gives the stage times
-        lanes8 = [p3s.Pipeline(W8, H8, c8) for _ in range(2)]
-        for ln in lanes8:
-            ln.set_inpaint_ctas(p3s.sm_count() // 4)
-            for i in range(4):
-                ln.run(ring8[i].addr)
-        p3s.device_sync()
-        a8, z8 = p3s.Event(), p3s.Event()
-        ends8 = [p3s.Event() for _ in lanes8]
-        barrier(world)
-        a8.record(lanes8[0].stream)
-        a8.wait(lanes8[1].stream)
-        for i in range(8):
-            lanes8[i % 2].run(ring8[i % 4].addr)
-        for ln, e in zip(lanes8, ends8):
-            e.record(ln.stream)
-            e.wait(lanes8[0].stream)
-        z8.record(lanes8[0].stream)
-        p3s.stream_sync(lanes8[0].stream)
-        (ms8,) = allreduce_max([a8.elapsed_ms(z8)], world, use_dist)
         for i in range(2):
             p8.run(ring8[i].addr, timed=True)
         p3s.stream_sync(p8.stream)
         p8.timing_sum(reset=True)
-        for i in range(4):
-            p8.run(ring8[i].addr, timed=True)
+        a8, z8 = p3s.Event(), p3s.Event()
+        barrier(world)
+        a8.record(p8.stream)
+        for i in range(8):
+            p8.run(ring8[i % 4].addr, timed=True)
+        z8.record(p8.stream)
+        p3s.stream_sync(p8.stream)
+        (ms8,) = allreduce_max([a8.elapsed_ms(z8)], world, use_dist)
         st8, n8 = p8.timing_sum(reset=True)
         extra["hsbs_8k_batch8"] = {"frames_per_s": 8 * world / (ms8 / 1e3), "frames": 8 * world,
                                    "mpix_per_s": 8 * world * W8 * H8 / (ms8 / 1e3) / 1e6,
                                    "stages_ms": {k: v / n8 / 1e6 for k, v in st8.items()},
-                                   "path": "device-resident, 7680x4320, HSBS output, 4 distinct "
-                                           "frames (398 MB > L2), 8 frames over 2 plans/streams; "
-                                           "stages_ms from one stream"}
-        del lanes8
+                                   "path": "device-resident Pipeline, 7680x4320, HSBS output, "
+                                           "4 distinct frames (398 MB > L2)"}
         del p8, ring8
         # the exact-FP64 bilateral (no FP32 certificate) on the same 4K frames, for the FP64
         # roofline of that kernel: 4 separately rounded DMUL/DADD per tap
