@@ -2,10 +2,11 @@
 """Benchmark of the B200 pseudo-stereo hot path (BASELINE.json metric: 4K stereo frames/s).
 
 Workload (BASELINE.json configs[1]): synthetic 3840x2160 RGB frames -> depth map ->
-exact FP64 cross-bilateral -> forward DIBR -> inpaint -> red-cyan anaglyph, default
-config (auto base 30, T=150, sigma_s=8, sigma_r=16). One step = one frame through the
-whole pipeline. Inputs cycle through a device-resident ring of distinct frames larger
-than L2 (8 x 24.9 MB = 199 MB > 126 MB), so every step reads its input from HBM.
+cross-bilateral (certified FP32 + exact FP64 fix-up: the reference's bytes) -> forward
+DIBR -> inpaint -> red-cyan anaglyph, default config (auto base 30, T=150, sigma_s=8,
+sigma_r=16). One step = one frame through the whole pipeline. Inputs cycle through a
+device-resident ring of distinct frames larger than L2 (8 x 24.9 MB = 199 MB > 126 MB), so
+every step reads its input from HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -13,13 +14,19 @@ Multi-GPU (torchrun, one process per GPU): frames are independent, so every rank
 its own frames with no data-path collective (weak scaling); torch.distributed is used
 only for the start/stop barriers and the max-over-ranks of the device time.
 
-Printed: one JSON line (rank 0). `value` = kernel path with inputs resident in HBM
-(CUDA events on the pipeline stream); `e2e` = the same through the drop-in C ABI
-p3s_convert with host (pinned) frames, H2D + D2H of outputs, depth and filtered depth
-inside the timed region; `roofline` = the dominant kernel (the exact FP64 bilateral)
-against the measured FP64 issue rate; `roofline_hbm` = the fused DIBR+anaglyph kernel
-against measured HBM bandwidth; `cpu_baseline` = the reference's own CPU implementation
-(oracle/_ref, compiled from the reference sources) on this host's cores.
+Printed: one JSON line (rank 0).
+  value        device-resident frames/s: frames pipelined over --streams plans (CUDA-graph
+               replay), CUDA events on the first stream; single_stream: one plan.
+  e2e          the drop-in C ABI: p3s_convert + p3s_result_output per frame from pinned
+               host frames, the frame's H2D and the anaglyph's D2H inside the timed region
+               (banded schedule; depth maps stay on the GPU until asked for).
+  e2e_stream   the streamed video API (p3s_video_convert, 4 streams).
+  roofline     the dominant kernel (k_bilateral_sep): range-table lookup bytes per second
+               against the measured shared-memory gather peak; roofline_hbm: the DIBR and
+               depth kernels against the measured HBM bandwidth.
+  cpu_baseline the reference's own CPU implementation (oracle/_ref, compiled from the
+               reference sources) on this host's cores, on a bounded sample.
+`--impl reference` prints the reference arm's line (rank 0 only).
 """
 from __future__ import annotations
 
