@@ -1,6 +1,9 @@
 // Host orchestrator of the B200 pseudo-stereo pipeline: per-thread device contexts, plans
 // (host-computed exact tables + one device arena per (size, config)), the stage API of
-// include/p3s/pipeline.hpp and the full convert_image (reference pipeline.cpp:29-78).
+// include/p3s/pipeline.hpp and the full convert_image (reference pipeline.cpp:29-78),
+// whose synchronous frames run as a row-banded schedule that overlaps the PCIe copies with
+// the filter (band_plan, Pipeline::Impl::upload_run_conv; DESIGN.md "Banded synchronous
+// convert").
 //
 // Built with -ffp-contract=off: the tables below must reproduce the reference's double
 // expressions bit for bit (SURVEY.md §7 rules 1, 2, 4, 5).
