@@ -325,7 +325,7 @@ def test_widest_supported_rows(p3s, checker):
 
 @pytest.mark.parametrize("w,h,block,sigma_s", [(500, 700, 4, 8.0), (1283, 389, 37, 3.1),
                                                (640, 1031, 16, 12.0), (900, 600, 64, 5.5),
-                                               (777, 2100, 23, 8.0)])
+                                               (777, 2100, 23, 8.0), (18768, 300, 16, 8.0)])
 def test_banded_convert_boundaries(p3s, checker, w, h, block, sigma_s):
     """p3s_convert on pinned planes uploads the frame in two row parts and filters band A
     while band B is still crossing PCIe (engine.cpp plan_bands). The band edges depend on
