@@ -519,9 +519,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
         for (int e = 0; e < 2; ++e) {
             if (done[e]) continue;
             const uint32_t* c = ctl + (e * 3 + slot) * (kPasses + 1);
+            // all of the round's pass counts in one go (one L2 round trip, not one per pass)
+            uint32_t cts[kPasses + 1];
+#pragma unroll
+            for (int k = 1; k <= kPasses; ++k) cts[k] = __ldcg(c + k);
             bool stalled = false;
             for (int k = 1; k <= kPasses; ++k) {
-                const long long rep = __ldcg(c + k);
+                const long long rep = cts[k];
                 if (rep == 0) {  // first pass with no repair while damage remains
                     passes[e] += k;
                     stalled = true;
