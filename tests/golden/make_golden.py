@@ -40,6 +40,9 @@ CASES = [
 
 DIGEST_CASES = [
     ("default_1920x1080", 1920, 1080, 1, {}),
+    # the bench workload (BASELINE configs[1]) and a large-parallax 4K frame, all formats
+    ("default_3840x2160", 3840, 2160, 1, {}),
+    ("b120_all_3840x2160", 3840, 2160, 2, dict(base=120, formats=7)),
 ]
 
 

@@ -69,6 +69,20 @@ def test_1080p_matches_reference_digest(p3s, manifest):
     assert sha(out["anaglyph"]) == d["anaglyph"]
 
 
+@pytest.mark.parametrize("name", ["default_3840x2160", "b120_all_3840x2160"])
+def test_4k_matches_reference_digest(p3s, manifest, name):
+    """The bench workload (and a large-parallax, all-formats 4K frame) against SHA-256
+    digests of the REFERENCE's own output (tests/golden/make_golden.py, oracle/_ref)."""
+    d = manifest["digests"][name]
+    import oracle
+    img = oracle.load("port").synthetic_frame(d["w"], d["h"], d["seed"])
+    assert sha(img) == d["input"]
+    out = p3s.convert(img, pcfg(p3s, d["cfg"]))
+    for k in ("depth", "filtered", "anaglyph", "hsbs", "fsbs"):
+        if k in d:
+            assert sha(out[k]) == d[k], k
+
+
 def compare_convert(p3s, checker, img, over):
     import oracle
     ref = checker.convert(img, oracle.Cfg(**over), threads=NCPU)
