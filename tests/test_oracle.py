@@ -62,6 +62,18 @@ def test_port_matches_reference_digest_1080p(port, manifest):
     assert sha(conv["anaglyph"]) == d["anaglyph"]
 
 
+@pytest.mark.parametrize("name", ["default_3840x2160", "b120_all_3840x2160"])
+def test_port_matches_reference_digest_4k(port, manifest, name):
+    d = manifest["digests"][name]
+    img = port.synthetic_frame(d["w"], d["h"], d["seed"])
+    assert sha(img) == d["input"]
+    import os
+    conv = port.convert(img, cfg_of(d), threads=os.cpu_count() or 1)
+    for k in ("depth", "filtered", "anaglyph", "hsbs", "fsbs"):
+        if k in d:
+            assert sha(conv[k]) == d[k], k
+
+
 def test_spec_kats(port, manifest):
     # SPEC.md:88 says luma(255,0,0)=76; the reference computes 77
     for r, g, b, y in manifest["kat"]["luma"]:
