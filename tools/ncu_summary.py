@@ -62,6 +62,9 @@ def main():
                                               ("k_bilateral_fixup2" if k == "k_bilateral_fixup" else k))
         traffic[key] = rw
         print(f"| {short} | " + " | ".join(d.get(x, "") for x in WANT) + f" | {rw / 1e6:.2f} MB |")
+    stage = ["k_depth_front", "k_block_values", "k_upsample"]
+    if all(k in traffic for k in stage):  # the depth stage as bench.py's roofline_hbm names it
+        traffic["+".join(stage)] = sum(traffic[k] for k in stage)
     with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
 
