@@ -170,6 +170,11 @@ P3S_API p3s_status p3s_gpu_smem_peak(double* bytes_per_s, int gather);
  * FP32 + exact FP64 fix-up (radius 16), 0 = exact FP64 kernels. */
 P3S_API p3s_status p3s_gpu_bilateral_path(const p3s_config* cfg, int* certified_fp32);
 P3S_API void p3s_host_free(void* p);
+/* The reference's seeded synthetic frame (bench.cpp:23-46: mt19937_64 seeded with
+ * seed ^ (w << 32) ^ h, one draw per pixel in raster order) written into three caller
+ * planes of w*h bytes. Host code, no GPU needed; the bench's and the tests' input source. */
+P3S_API p3s_status p3s_synthetic_frame(int w, int h, uint64_t seed, uint8_t* r, uint8_t* g,
+                                       uint8_t* b);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,8 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpseudo3d_b200.so")
+# P3S_LIB_PATH: an in-tree experiment build (make VARIANT=...); default the product library
+LIB_PATH = os.environ.get("P3S_LIB_PATH") or os.path.join(HERE, "libpseudo3d_b200.so")
 
 P3S_OK, P3S_ERR_INVALID, P3S_ERR_IO, P3S_ERR_DECODE, P3S_ERR_INTERNAL = range(5)
 MODE_FORWARD, MODE_BACKWARD = 0, 1
@@ -170,6 +171,7 @@ _SIGS = {
     "p3s_gpu_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "p3s_gpu_smem_peak": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
     "p3s_gpu_bilateral_path": (C.c_int, [vp, C.POINTER(C.c_int)]),
+    "p3s_synthetic_frame": (C.c_int, [C.c_int, C.c_int, C.c_uint64, u8p, u8p, u8p]),
 }
 
 _lib = None
@@ -611,6 +613,14 @@ def fp64_peak() -> float:
     v = C.c_double()
     _check(lib().p3s_gpu_fp64_peak(C.byref(v)))
     return v.value
+
+
+def synthetic_frame(w: int, h: int, seed: int = 1) -> np.ndarray:
+    """The reference's seeded synthetic frame (bench.cpp:23-46) as (3, h, w) u8 planes,
+    generated by the product library (host code)."""
+    out = np.empty((3, h, w), np.uint8)
+    _check(lib().p3s_synthetic_frame(w, h, seed, _p(out[0]), _p(out[1]), _p(out[2])))
+    return out
 
 
 def bilateral_fast_path(cfg) -> bool:

@@ -964,6 +964,18 @@ p3s_status p3s_gpu_bilateral_path(const p3s_config* cfg, int* certified_fp32) {
     });
 }
 
+p3s_status p3s_synthetic_frame(int w, int h, uint64_t seed, uint8_t* r, uint8_t* g, uint8_t* b) {
+    NEED(r, g, b);
+    return guarded([&] {
+        if (w <= 0 || h <= 0) throw std::invalid_argument("synthetic_frame: dimensions must be positive");
+        const p3s::ImageRGB8 img = p3s::synthetic_frame(w, h, seed);
+        const std::size_t n = static_cast<std::size_t>(w) * h;
+        std::memcpy(r, img.r.data(), n);
+        std::memcpy(g, img.g.data(), n);
+        std::memcpy(b, img.b.data(), n);
+    });
+}
+
 p3s_status p3s_gpu_smem_peak(double* bytes_per_s, int gather) {
     NEED(bytes_per_s);
     return guarded([&] {

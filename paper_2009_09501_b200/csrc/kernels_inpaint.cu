@@ -19,12 +19,15 @@
 // computed for the pixels a pass repairs (each damaged pixel exactly once), from the
 // pass-start colours of its intact neighbours in shared memory.
 //
-// Cross-tile state is one 64-bit word per initially damaged pixel: 0 = damaged, else
-// (1 << 63) | global pass of repair << 24 | colour bytes, written once by the owning tile.
-// A tile starting round r takes a neighbour pixel as intact only if its word records a
-// repair at a pass <= the round's first pass; words written during the current round are
-// ignored (the region simulation re-derives them), so the racy reads are harmless and ONE
-// grid barrier per round suffices. Per-pass global repair counts (interior pixels only)
+// Cross-tile state is the damage of each 32-pixel row word of a tile interior as it stands
+// at the end of a round: a 64-bit word (tag << 32 | damage bits), tag = round + 1, kept in
+// two slots per word. Round r writes slot r & 1 (round 0 writes both, so no word of a
+// damaged tile keeps another frame's content); a tile starting round r takes, per word, the
+// slot with the largest tag <= r, i.e. the state at the end of round r - 1. Slot (r - 1) & 1
+// is stable during round r, and slot r & 1 only ever goes from an older tag to r + 1, so the
+// racy reads are harmless and ONE grid barrier per round suffices. A region row needs three
+// of these words (6 independent loads), where per-pixel state words needed a serial chain
+// of up to 64 L2 round trips per row in a dense strip. Per-pass global repair counts (interior pixels only)
 // reproduce the reference's global stall rule and pass statistics exactly. Tiles are taken
 // from a per-round work list with one atomic per claim (dynamic load balance).
 #include <cooperative_groups.h>
@@ -47,13 +50,37 @@ constexpr int kPasses = 16;            // passes per round = halo width
 constexpr int kE = kT + 2 * kPasses;   // region side (64: one u64 per row)
 constexpr int kWarps = 8;              // one tile per warp
 constexpr int kThreads = 32 * kWarps;
-constexpr unsigned long long kRepaired = 1ull << 63;
 constexpr uint32_t kHeavy = 128;       // damaged pixels that make a tile "heavy"
 
 struct Eye {
     InpaintEye io;
-    unsigned long long* state;  // per pixel (only initially damaged entries used)
+    unsigned long long* slot[2];  // [h][mwords] tagged damage words of tile interiors
+    int mwords;                   // (w + 31) / 32
 };
+
+// Damage bits of word wi of row gy as of the end of round r - 1 (largest tag <= r); all ones
+// when neither slot holds such a word (a word without initial damage: the caller ANDs it with
+// the initial mask, which is 0 there).
+__device__ __forceinline__ unsigned word_state(const Eye& E, int gy, int wi, int r) {
+    if (wi < 0 || wi >= E.mwords) return 0u;
+    const size_t o = static_cast<size_t>(gy) * E.mwords + wi;
+    const unsigned long long a = __ldcg(E.slot[0] + o), b = __ldcg(E.slot[1] + o);
+    const unsigned ta = static_cast<unsigned>(a >> 32), tb = static_cast<unsigned>(b >> 32);
+    const bool va = ta - 1u < static_cast<unsigned>(r), vb = tb - 1u < static_cast<unsigned>(r);
+    if (va && (!vb || ta >= tb)) return static_cast<unsigned>(a);
+    if (vb) return static_cast<unsigned>(b);
+    return 0xFFFFFFFFu;
+}
+
+// Publishes the interior word of region row r (image row gy) at the end of round `round`.
+__device__ __forceinline__ void publish_word(const Eye& E, int gy, int tx, int round,
+                                             unsigned long long dregion) {
+    const unsigned long long v = (static_cast<unsigned long long>(round + 1) << 32) |
+                                 ((dregion >> kPasses) & 0xFFFFFFFFull);
+    const size_t o = static_cast<size_t>(gy) * E.mwords + tx;
+    __stcg(E.slot[round & 1] + o, v);
+    if (round == 0) __stcg(E.slot[1] + o, v);
+}
 
 struct Work {
     uint32_t* init_flags;  // [2][tiles] damaged-pixel count per tile (initial work list)
@@ -140,30 +167,56 @@ __device__ __forceinline__ unsigned long long two_plus(unsigned long long up, un
     return two;
 }
 
+#ifdef P3S_INPAINT_PHASES
+// experiment build only (make VARIANT=phases EXTRA=-DP3S_INPAINT_PHASES): per-phase ns of
+// the warp tiles of rounds >= 1, summed: [0] words, [1] colour rows, [2] pass decide,
+// [3] compaction, [4] colours, [5] publish/update, [6] tail, [7] tiles, [8] passes
+__device__ unsigned long long g_phase[16];
+__device__ __forceinline__ unsigned long long ptimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PH_MARK(i)                                                            \
+    do {                                                                      \
+        __syncwarp();                                                         \
+        const unsigned long long _n = ptimer();                               \
+        if (round > 0 && (threadIdx.x & 31) == 0) atomicAdd(&g_phase[i], _n - _pt); \
+        _pt = _n;                                                             \
+    } while (0)
+#else
+#define PH_MARK(i) \
+    do {           \
+    } while (0)
+#endif
+
 // One warp simulates up to kPasses Jacobi passes of one tile (+ halo) in shared memory.
 __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int round, WarpSmem& S,
                              uint32_t* counts_slot, bool& remains) {
     const InpaintEye& io = E.io;
     const int lane = threadIdx.x & 31;
     const int x0 = tx * kT - kPasses, y0 = ty * kT - kPasses;
-    const long long pass0 = static_cast<long long>(round) * kPasses;
     const unsigned long long kInner = 0x0000FFFFFFFF0000ull;  // interior columns 16..47
+#ifdef P3S_INPAINT_PHASES
+    unsigned long long _pt = ptimer();
+    if (round > 0 && lane == 0) atomicAdd(&g_phase[7], 1ull);
+#endif
 
-    // 1. damage / in-image words; in later rounds, pixels repaired in earlier rounds
-    //    (state word with pass <= pass0) are intact
+    // 1. damage / in-image words; in later rounds, pixels repaired in earlier rounds (the
+    //    tagged interior words of the end of round - 1) are intact
     unsigned long long d[2], img[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int r = lane + 32 * j, gy = y0 + r;
         unsigned long long in = 0, m = 0;
         if (gy >= 0 && gy < h) m = row_bits(io, x0, gy, w, in);
-        if (round > 0) {
-            for (unsigned long long b = m; b; b &= b - 1) {
-                const int c = __ffsll(static_cast<long long>(b)) - 1;
-                const unsigned long long v = __ldcg(E.state + static_cast<size_t>(gy) * w + (x0 + c));
-                if ((v & kRepaired) && static_cast<long long>((v >> 24) & 0xFFFFFFFFull) <= pass0)
-                    m &= ~(1ull << c);
-            }
+        if (round > 0 && m) {
+            // region columns 0..15 = bits 16..31 of word tx - 1, 16..47 = word tx,
+            // 48..63 = bits 0..15 of word tx + 1
+            const unsigned a = word_state(E, gy, tx - 1, round), b = word_state(E, gy, tx, round),
+                           c = word_state(E, gy, tx + 1, round);
+            m &= static_cast<unsigned long long>(a >> 16) | (static_cast<unsigned long long>(b) << 16) |
+                 (static_cast<unsigned long long>(c & 0xFFFFu) << 48);
         }
         d[j] = m;
         img[j] = in;
@@ -171,6 +224,7 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
         S.img[r] = in;
     }
     __syncwarp();
+    PH_MARK(0);
     // 2. colours of every row next to damage (intact pixels there feed the means)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -179,6 +233,7 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
         if (near && gy >= 0 && gy < h) load_row(io, S, r, gy, x0, w);
     }
     __syncwarp();
+    PH_MARK(1);
     // 3. passes
     for (int k = 1; k <= kPasses; ++k) {
         unsigned long long rep[2], iu[2], im[2], id[2];
@@ -194,6 +249,10 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
             if (r >= kPasses && r < kPasses + kT) inner += __popcll(rep[j] & kInner);
         }
         if (!__any_sync(0xFFFFFFFFu, any)) break;  // fixed point of the region
+#ifdef P3S_INPAINT_PHASES
+        if (round > 0 && lane == 0) atomicAdd(&g_phase[8], 1ull);
+#endif
+        PH_MARK(2);
         // compact the pass's repairs into one list so the colour work spreads over the lanes
         const int cnt = __popcll(rep[0]) + __popcll(rep[1]);
         int incl = cnt;
@@ -211,6 +270,7 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
                     S.rep[pos++] = static_cast<uint16_t>(((lane + 32 * j) << 6) | (__ffsll(static_cast<long long>(b)) - 1));
         }
         __syncwarp();
+        PH_MARK(3);
         // colours from the pass-start intact neighbours (S.dmg is still the pass-start
         // state; a repaired pixel is never an intact neighbour in its own pass, so the
         // in-place writes cannot be read by another lane in this pass)
@@ -238,16 +298,13 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
             if (io.plane[2]) S.col[2][r][c] = static_cast<uint8_t>((2 * a2 + cntn) / (2 * cntn));
         }
         __syncwarp();
+        PH_MARK(4);
         // interior repairs: publish colour + state word
         for (int i = lane; i < total; i += 32) {
             const int e = S.rep[i], r = e >> 6, c = e & 63;
             if (r < kPasses || r >= kPasses + kT || c < kPasses || c >= kPasses + kT) continue;
             const int gy = y0 + r, gx = x0 + c;
             const uint8_t c0 = S.col[0][r][c], c1 = S.col[1][r][c], c2 = S.col[2][r][c];
-            const unsigned long long g = static_cast<unsigned long long>(pass0 + k);
-            E.state[static_cast<size_t>(gy) * w + gx] =
-                kRepaired | (g << 24) | (static_cast<unsigned long long>(c2) << 16) |
-                (static_cast<unsigned long long>(c1) << 8) | c0;
             const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
             if (io.plane[0]) io.plane[0][o] = c0;
             if (io.plane[1]) io.plane[1][o] = c1;
@@ -265,19 +322,25 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
             if (r >= kPasses && r < kPasses + kT) inner_left |= (d[j] & kInner) != 0;
         }
         __syncwarp();
+        PH_MARK(5);
         // interior complete: its pixels never change again (repairs are final), so later
         // passes add no interior repairs; the halo's evolution is discarded anyway
         if (!__any_sync(0xFFFFFFFFu, inner_left)) break;
     }
-    // 4. interior damage left -> the tile runs again next round
+    PH_MARK(2);
+    // 4. publish the interior's damage words; interior damage left -> the tile runs again
     int left = 0;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        const int r = lane + 32 * j;
-        if (r >= kPasses && r < kPasses + kT) left |= (d[j] & kInner) != 0;
+        const int r = lane + 32 * j, gy = y0 + r;
+        if (r >= kPasses && r < kPasses + kT) {
+            left |= (d[j] & kInner) != 0;
+            if (gy < h) publish_word(E, gy, tx, round, d[j]);
+        }
     }
     remains = __any_sync(0xFFFFFFFFu, left);
     __syncwarp();
+    PH_MARK(6);
 }
 
 // Round-0 version of process_tile for heavy tiles: the whole CTA (kThreads threads) works
@@ -366,10 +429,6 @@ __device__ void process_tile_cta(const Eye& E, int tx, int ty, int w, int h, War
             if (r < kPasses || r >= kPasses + kT || c < kPasses || c >= kPasses + kT) continue;
             const int gy = y0 + r, gx = x0 + c;
             const uint8_t c0 = S.col[0][r][c], c1 = S.col[1][r][c], c2 = S.col[2][r][c];
-            const unsigned long long g = static_cast<unsigned long long>(k);  // round 0: pass0 = 0
-            E.state[static_cast<size_t>(gy) * w + gx] =
-                kRepaired | (g << 24) | (static_cast<unsigned long long>(c2) << 16) |
-                (static_cast<unsigned long long>(c1) << 8) | c0;
             const size_t o = static_cast<size_t>(gy) * io.pitch + gx;
             if (io.plane[0]) io.plane[0][o] = c0;
             if (io.plane[1]) io.plane[1][o] = c1;
@@ -383,12 +442,17 @@ __device__ void process_tile_cta(const Eye& E, int tx, int ty, int w, int h, War
         // interior complete: later passes add no interior repairs (see process_tile)
         if (!__syncthreads_or(inner_row && (d & kInner))) break;
     }
+    if (inner_row && y0 + tid < h) publish_word(E, y0 + tid, tx, 0, d);
     remains = __syncthreads_or(inner_row && (d & kInner)) != 0;
 }
 
 // Debug timeline (P3S_DEBUG_INPAINT): per warp, globaltimer ns at the phase boundaries of
 // round 0 plus tile statistics. nullptr in normal runs.
 __device__ unsigned long long* g_inp_dbg = nullptr;
+// per-round debug (P3S_DEBUG_INPAINT): [kDbgRounds][4] = round start (block 0, after the
+// barrier), latest warp finish of the round's tiles, max tile ns, tiles processed
+constexpr int kDbgRounds = 64;
+__device__ unsigned long long* g_inp_rdbg = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -416,7 +480,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
         cnt[e] = __ldcg(eyes[e].io.count);
         for (uint32_t k = gtid; k < cnt[e]; k += gsize) {
             const uint32_t idx = eyes[e].io.list[k];
-            eyes[e].state[idx] = 0ull;
             const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
             const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
             const int t = (y / kT) * tiles_x + x / kT;
@@ -439,8 +502,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
     if (dbg) dt[2] = gtimer();
 
     // ctl layout: [eye][slot 0..2][kPasses + 1] pass counts
+    unsigned long long* rdbg = g_inp_rdbg;
     for (int round = 0; !(done[0] && done[1]); ++round) {
         const int slot = round % 3, nslot = (round + 1) % 3, rslot = (round + 2) % 3;
+        if (rdbg && round < kDbgRounds && blockIdx.x == 0 && threadIdx.x == 0) rdbg[4 * round] = gtimer();
         if (gtid < 2 * (kPasses + 1)) {
             const int e = gtid / (kPasses + 1), k = gtid % (kPasses + 1);
             ctl[(e * 3 + nslot) * (kPasses + 1) + k] = 0;
@@ -467,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
                 const int e = static_cast<int>(item) / ntiles, t = static_cast<int>(item) - e * ntiles;
                 if (done[e]) continue;
                 bool remains = false;
-                const unsigned long long tt0 = dbg ? gtimer() : 0;
+                const unsigned long long tt0 = (dbg || rdbg) ? gtimer() : 0;
                 process_tile_cta(e ? R : L, t % tiles_x, t / tiles_x, w, h, S0,
                                  ctl + (e * 3 + slot) * (kPasses + 1), remains);
                 if (dbg && (threadIdx.x & 31) == 0) {
@@ -475,6 +540,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
                     dt[5] += 1;
                     dt[6] += dd;
                     dt[7] = dd > dt[7] ? dd : dt[7];
+                }
+                if (rdbg && threadIdx.x == 0) {
+                    const unsigned long long now = gtimer();
+                    atomicMax(rdbg + 1, now);
+                    atomicMax(rdbg + 2, now - tt0);
+                    atomicAdd(rdbg + 3, 1ull);
                 }
                 if (remains && threadIdx.x == 0) {
                     const uint32_t pos = atomicAdd(&wk.counters[2 * nslot], 1u);
@@ -493,9 +564,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
             const int e = static_cast<int>(item) / ntiles, t = static_cast<int>(item) - e * ntiles;
             if (done[e]) continue;
             bool remains = false;
-            const unsigned long long tt0 = dbg ? gtimer() : 0;
+            const unsigned long long tt0 = (dbg || rdbg) ? gtimer() : 0;
             process_tile(e ? R : L, t % tiles_x, t / tiles_x, w, h, round, S,
                          ctl + (e * 3 + slot) * (kPasses + 1), remains);
+            if (rdbg && round < kDbgRounds && lane == 0) {
+                const unsigned long long now = gtimer();
+                atomicMax(rdbg + 4 * round + 1, now);
+                atomicMax(rdbg + 4 * round + 2, now - tt0);
+                atomicAdd(rdbg + 4 * round + 3, 1ull);
+            }
             if (dbg && round == 0) {
                 const unsigned long long d = gtimer() - tt0;
                 dt[5] += 1;
@@ -544,9 +621,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
                 const InpaintEye& io = eyes[e].io;
                 for (uint32_t k = gtid; k < cnt[e]; k += gsize) {
                     const uint32_t idx = io.list[k];
-                    if (__ldcg(eyes[e].state + idx) & kRepaired) continue;
                     const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
                     const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
+                    // damage as of the end of this round (tags <= round + 1)
+                    if (!((word_state(eyes[e], y, x >> 5, round + 1) >> (x & 31)) & 1u)) continue;
                     const size_t o = static_cast<size_t>(y) * io.pitch + x;
                     for (int ch = 0; ch < 3; ++ch)
                         if (io.plane[ch]) io.plane[ch][o] = 128;
@@ -557,6 +635,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
                 passes[e] += kPasses;
             }
         }
+    }
+    if (rdbg) {  // debug only (uniform across the grid): the end time of the last round
+        grid.sync();
+        if (gtid == 0) rdbg[4 * kDbgRounds] = gtimer();
     }
     if (gtid == 0 && stats) {
         for (int e = 0; e < 2; ++e) {
@@ -569,12 +651,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(Eye L, Eye R, Wor
 
 }  // namespace
 
+// Damage words of one eye's two slots: 2 * h * mwords u64.
+static size_t slot_bytes(int w, int h) {
+    return 2 * static_cast<size_t>(h) * ((w + 31) / 32) * 8;
+}
+
 size_t inpaint_scratch_bytes(int w, int h) {
-    const size_t n = static_cast<size_t>(w) * h;
     const size_t tiles = static_cast<size_t>((w + kT - 1) / kT) * ((h + kT - 1) / kT);
-    // state words [2][n] | tile counts [2][tiles] | lists [3][2 * tiles] | counters [4][2] |
+    // damage slots [2 eyes] | tile counts [2][tiles] | lists [3][2 * tiles] | counters [4][2] |
     // heavy list [2 * tiles]
-    return 2 * n * 8 + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 64 + 2 * tiles * 4 + 256;
+    return 2 * slot_bytes(w, h) + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 64 + 2 * tiles * 4 + 256;
 }
 
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
@@ -585,12 +671,13 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     // flags and work lists live in the engine-provided inpaint arena (InpaintEye.repair of
     // the left eye points at it; see engine.cpp).
     const int tiles_x = (gm.w + kT - 1) / kT, tiles_y = (gm.h + kT - 1) / kT;
-    const size_t n = static_cast<size_t>(gm.w) * gm.h;
     const size_t tiles = static_cast<size_t>(tiles_x) * tiles_y;
     unsigned char* arena = reinterpret_cast<unsigned char*>(left.repair);
-    Eye L{left, reinterpret_cast<unsigned long long*>(arena)};
-    Eye R{right, reinterpret_cast<unsigned long long*>(arena + n * 8)};
-    unsigned char* flags = arena + 2 * n * 8;
+    const size_t sb = slot_bytes(gm.w, gm.h), half = sb / 2;
+    const int mw = (gm.w + 31) / 32;
+    Eye L{left, {reinterpret_cast<unsigned long long*>(arena), reinterpret_cast<unsigned long long*>(arena + half)}, mw};
+    Eye R{right, {reinterpret_cast<unsigned long long*>(arena + sb), reinterpret_cast<unsigned long long*>(arena + sb + half)}, mw};
+    unsigned char* flags = arena + 2 * sb;
     Work wk;
     wk.init_flags = reinterpret_cast<uint32_t*>(flags);
     wk.lists = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4);
@@ -626,8 +713,41 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
         cudaMalloc(&dbg, static_cast<size_t>(blocks) * kWarps * 8 * sizeof(unsigned long long));
         cudaMemcpyToSymbol(g_inp_dbg, &dbg, sizeof(dbg));
     }
+    static unsigned long long* rdbg = nullptr;
+    if (want && !rdbg) {
+        cudaMalloc(&rdbg, (4 * kDbgRounds + 4) * sizeof(unsigned long long));
+        cudaMemcpyToSymbol(g_inp_rdbg, &rdbg, sizeof(rdbg));
+    }
+    if (want) cudaMemsetAsync(rdbg, 0, (4 * kDbgRounds + 4) * sizeof(unsigned long long), st);
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_inpaint_tiles), dim3(blocks),
                                     dim3(kThreads), args, smem, st);
+#ifdef P3S_INPAINT_PHASES
+    if (e == cudaSuccess) {
+        unsigned long long ph[16];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
+        const double tl = ph[7] ? static_cast<double>(ph[7]) : 1.0, ps = ph[8] ? static_cast<double>(ph[8]) : 1.0;
+        fprintf(stderr, "[p3s] inpaint phases (rounds >= 1, %llu warp tiles, %.2f passes/tile): per tile words %.2f us, "
+                        "colour rows %.2f us, tail %.2f us; per pass decide %.3f us, compact %.3f us, colours %.3f us, "
+                        "publish %.3f us\n",
+                ph[7], ps / tl, ph[0] / tl / 1e3, ph[1] / tl / 1e3, ph[6] / tl / 1e3, ph[2] / ps / 1e3, ph[3] / ps / 1e3,
+                ph[4] / ps / 1e3, ph[5] / ps / 1e3);
+        const unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    }
+#endif
+    if (want && e == cudaSuccess) {
+        cudaStreamSynchronize(st);
+        std::vector<unsigned long long> rb(4 * kDbgRounds + 4);
+        cudaMemcpy(rb.data(), rdbg, rb.size() * 8, cudaMemcpyDeviceToHost);
+        for (int r = 0; r < kDbgRounds && rb[4 * r]; ++r) {
+            const unsigned long long t0 = rb[4 * r];
+            const unsigned long long t1 = (r + 1 < kDbgRounds && rb[4 * (r + 1)]) ? rb[4 * (r + 1)] : rb[4 * kDbgRounds];
+            fprintf(stderr, "[p3s] inpaint round %2d: %6.1f us (tiles done at %6.1f us, max tile %6.1f us, %llu tiles)\n",
+                    r, (t1 - t0) / 1e3, rb[4 * r + 1] > t0 ? (rb[4 * r + 1] - t0) / 1e3 : 0.0, rb[4 * r + 2] / 1e3,
+                    rb[4 * r + 3]);
+        }
+    }
     if (want && e == cudaSuccess) {
         cudaStreamSynchronize(st);
         const int nw = blocks * kWarps;

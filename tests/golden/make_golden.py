@@ -43,6 +43,11 @@ DIGEST_CASES = [
     # the bench workload (BASELINE configs[1]) and a large-parallax 4K frame, all formats
     ("default_3840x2160", 3840, 2160, 1, {}),
     ("b120_all_3840x2160", 3840, 2160, 2, dict(base=120, formats=7)),
+    # the rest of configs[1]'s parallax sweep on the bench frame (B = 30 is the default
+    # case above): B = 510 is a 249-pass, 16-round inpaint that no smaller frame reproduces
+    *[(f"b{b}_3840x2160", 3840, 2160, 1, dict(base=b)) for b in (0, 2, 16, 60, 254, 510)],
+    # configs[4]: 8K anamorph (HSBS) output
+    ("hsbs_7680x4320", 7680, 4320, 1, dict(formats=2)),
 ]
 
 
@@ -84,13 +89,23 @@ def run_case(R, w, h, seed, over):
 def main():
     R = oracle.load("reference")
     assert R.kind == "reference", "golden vectors must come from the compiled reference"
-    manifest = {"source": "oracle/_ref/libp3s_ref.so (reference proj/src compiled with "
-                          "-O2 -ffp-contract=off)", "cases": {}, "digests": {}}
-    for name, w, h, seed, over in CASES:
+    path = os.path.join(OUT, "manifest.json")
+    # --digests-only: keep the .npz cases and add the digest cases missing from the manifest
+    only = "--digests-only" in sys.argv
+    if only:
+        with open(path) as f:
+            manifest = json.load(f)
+    else:
+        manifest = {"source": "oracle/_ref/libp3s_ref.so (reference proj/src compiled with "
+                              "-O2 -ffp-contract=off)", "cases": {}, "digests": {}}
+    for name, w, h, seed, over in ([] if only else CASES):
         cfg, out = run_case(R, w, h, seed, over)
         np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
         manifest["cases"][name] = {"w": w, "h": h, "seed": seed, "cfg": cfg.__dict__}
     for name, w, h, seed, over in DIGEST_CASES:
+        if only and name in manifest["digests"]:
+            continue
+        print("digest", name, flush=True)
         cfg = oracle.Cfg(**over)
         img = R.synthetic_frame(w, h, seed)
         conv = R.convert(img, cfg, threads=os.cpu_count() or 1)
@@ -109,7 +124,7 @@ def main():
                                             (100, 0, 30, 150), (0, 200, 8, 150),
                                             (10, 17, 30, 150), (5, 51, 30, 0), (7, 0, 0, 150)]]
     manifest["kat"] = kat
-    with open(os.path.join(OUT, "manifest.json"), "w") as f:
+    with open(path, "w") as f:
         json.dump(manifest, f, indent=1, sort_keys=True)
     print("wrote", len(CASES), "cases +", len(DIGEST_CASES), "digests")
 
