@@ -1512,14 +1512,15 @@ ImageRGB8 inpaint(const ImageRGB8& frame, const DamageMask& mask, const Conversi
     for (int ch = 0; ch < 3; ++ch) p->h2d_plane(p->eyes + ch * p->plane(), frame.plane(ch).data(), st);
     p->h2d_plane(p->stage_masks, mask.damaged.data(), st);
     CK(cudaMemsetAsync(p->counts, 0, 2 * sizeof(uint32_t), st));
-    CK(cu::mask_to_list(p->stage_masks, p->pitch, p->gm, p->list_ptr(0, 0), p->counts, st));
+    CK(cu::mask_to_list(p->stage_masks, p->pitch, p->gm, p->list_ptr(0, 0), p->counts, st, p->mbits,
+                        p->mwords));
     cu::InpaintEye ie[2];
     for (int e = 0; e < 2; ++e) {
         for (int ch = 0; ch < 3; ++ch) ie[e].plane[ch] = p->eyes + (3 * e + ch) * p->plane();
         ie[e].pitch = p->pitch;
-        ie[e].mask_bytes = p->stage_masks + e * p->plane();
-        ie[e].mask_bits = nullptr;
-        ie[e].mask_pitch = p->pitch;
+        ie[e].mask_bytes = nullptr;
+        ie[e].mask_bits = p->mbits + static_cast<std::size_t>(e) * p->mwords * p->h;  // eye 1: no damage listed
+        ie[e].mask_pitch = p->mwords;
         ie[e].list = p->list_ptr(e, 0);
         ie[e].count = p->counts + e;
         ie[e].list2 = nullptr;

@@ -501,13 +501,16 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
 
 // Byte mask -> damaged list (stage-level inpaint entry point).
 __global__ void k_mask_to_list(const uint8_t* __restrict__ mask, int mpitch, int w, int h,
-                               uint32_t* list, uint32_t* count) {
+                               uint32_t* list, uint32_t* count, uint32_t* bits, int mwords) {
     const int lane = threadIdx.x & 31;
     const int y = blockIdx.y;
     const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
     unsigned m = 0;
     for (int k = 0; k < 16; ++k)
         if (x0 + k < w && mask[static_cast<size_t>(y) * mpitch + x0 + k]) m |= 1u << k;
+    // the same damage as 32-pixel bit words (two threads per word), the inpaint's input
+    const unsigned hi = __shfl_down_sync(0xFFFFFFFFu, m, 1);
+    if (bits && !(lane & 1) && x0 < w) bits[static_cast<size_t>(y) * mwords + (x0 >> 5)] = m | (hi << 16);
     append_list(list, count, m, static_cast<uint32_t>(y) * w + x0, lane);
 }
 
@@ -652,10 +655,10 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
 }
 
 cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* list,
-                         uint32_t* count, cudaStream_t st) {
+                         uint32_t* count, cudaStream_t st, uint32_t* bits, int mwords) {
     const int chunks = (gm.w + 15) / 16;
     dim3 grid((chunks + 127) / 128, gm.h);
-    k_mask_to_list<<<grid, 128, 0, st>>>(mask, mpitch, gm.w, gm.h, list, count);
+    k_mask_to_list<<<grid, 128, 0, st>>>(mask, mpitch, gm.w, gm.h, list, count, bits, mwords);
     return cudaGetLastError();
 }
 

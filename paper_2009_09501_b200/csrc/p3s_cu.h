@@ -151,14 +151,16 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
                  EyeOut right, cudaStream_t st, int ya = 0, int yb = -1);  // rows [ya, yb)
 
-// Byte mask -> damaged list (stage-level inpaint entry point).
+// Byte mask -> damaged list and (bits != nullptr) 32-pixel damage words of mwords per row
+// (stage-level inpaint entry point).
 cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* list,
-                         uint32_t* count, cudaStream_t st);
+                         uint32_t* count, cudaStream_t st, uint32_t* bits = nullptr, int mwords = 0);
 
 // Inpaint (inpaint.cpp:29-130) on both eyes at once, in place on the EyeOut planes.
 // Work lists come from dibr(). stats (device, 6 x i64): passes/repaired/fallback per eye.
-// The masks are the INITIAL damage (read-only). `repair` of the left eye points at a
-// device arena of inpaint_scratch_bytes(w, h) (per-pixel state words + tile flags).
+// The damage is read from mask_bits (the INITIAL damage, 32-pixel words, read-only; the
+// byte mask is not read). `repair` of the left eye points at a device arena of
+// inpaint_scratch_bytes(w, h) (tagged damage words, tile counts, work lists; persistent).
 struct InpaintEye {
     uint8_t* plane[3];
     int pitch;

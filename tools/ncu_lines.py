@@ -1,6 +1,6 @@
 """Aggregate an ncu --set full capture's warp-stall samples by CUDA source line (cuda,sass
 view). usage: python tools/ncu_lines.py REP.ncu-rep [top]"""
-import csv, io, subprocess, sys
+import csv, io, os, subprocess, sys
 from collections import defaultdict
 
 rep = sys.argv[1]
@@ -12,8 +12,12 @@ hdr = None
 agg = defaultdict(lambda: defaultdict(float))
 src = {}
 cur_line = None
+cur_file = ""
 for r in rows:
     if not r:
+        continue
+    if r[0] == "File Path":
+        cur_file = os.path.basename(r[1])
         continue
     if r[0] == "Line No":
         hdr = r
@@ -21,12 +25,12 @@ for r in rows:
     if hdr is None or len(r) < len(hdr):
         continue
     if r[0]:
-        cur_line = int(r[0]) if r[0].isdigit() else r[0]
+        cur_line = f"{cur_file}:{r[0]}"
         src[cur_line] = r[1].strip()
     d = dict(zip(hdr[2:], r[2:]))
     for k in ("Warp Stall Sampling (All Samples)", "Instructions Executed", "stall_long_sb",
               "stall_barrier", "stall_short_sb", "stall_lg", "stall_membar", "stall_branch_resolving",
-              "stall_wait", "stall_mio", "stall_no_inst"):
+              "stall_wait", "stall_mio", "stall_no_inst", "stall_math", "stall_dispatch", "stall_lg_throttle", "stall_drain"):
         try:
             agg[cur_line][k] += float(d.get(k, "0") or 0)
         except ValueError:
@@ -40,5 +44,6 @@ for ln, v in items[:top]:
         break
     det = " ".join(f"{k.replace('stall_', '')}={v[k]:.0f}" for k in
                    ("stall_long_sb", "stall_barrier", "stall_short_sb", "stall_lg", "stall_membar",
-                    "stall_branch_resolving", "stall_wait", "stall_mio", "stall_no_inst") if v[k] > 0.05 * s)
-    print(f"{100 * s / tot:5.1f}% L{ln} inst={v['Instructions Executed']:.0f} [{det}] {src.get(ln, '')[:90]}")
+                    "stall_branch_resolving", "stall_wait", "stall_mio", "stall_no_inst", "stall_math",
+                    "stall_dispatch", "stall_lg_throttle", "stall_drain") if v[k] > 0.05 * s)
+    print(f"{100 * s / tot:5.1f}% {ln} inst={v['Instructions Executed']:.0f} [{det}] {src.get(ln, '')[:90]}")
