@@ -6,32 +6,39 @@ cross-bilateral (certified FP32 + exact FP64 fix-up: the reference's bytes) -> f
 DIBR -> inpaint -> red-cyan anaglyph, default config (auto base 30, T=150, sigma_s=8,
 sigma_r=16). One step = one frame through the whole pipeline. Inputs cycle through a
 device-resident ring of distinct frames larger than L2 (8 x 24.9 MB = 199 MB > 126 MB), so
-every step reads its input from HBM.
+every step reads its input from HBM. Frames come from the product's synthetic_frame
+(p3s_synthetic_frame, byte-identical to the reference's bench.cpp:23-46).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one process per GPU): frames are independent, so every rank runs
-its own frames with no data-path collective (weak scaling); torch.distributed is used
-only for the start/stop barriers and the max-over-ranks of the device time.
+Multi-GPU: one process per GPU. The driver launches N > 1 under torchrun; run directly with
+--gpus N > 1, bench.py re-launches itself that way. Frames are independent, so every rank
+converts its own frames (frame i on rank i mod N) with no data-path collective (weak
+scaling); torch.distributed is only the start/stop barriers and the max-over-ranks of the
+times. Each rank binds to its GPU's NUMA node before allocating its pinned frame rings.
 
 Printed: one JSON line (rank 0).
-  value        device-resident frames/s: frames pipelined over --streams plans (CUDA-graph
-               replay), CUDA events on the first stream; single_stream: one plan.
+  value        device-resident frames/s (all ranks): frames pipelined over --streams plans
+               (CUDA-graph replay), CUDA events on the first stream; single_stream: one plan.
   e2e          the drop-in C ABI: p3s_convert + p3s_result_output per frame from pinned
-               host frames, the frame's H2D and the anaglyph's D2H inside the timed region
-               (banded schedule; depth maps stay on the GPU until asked for).
-  e2e_stream   the streamed video API (p3s_video_convert, 4 streams).
+               host frames, the frame's H2D and the anaglyph's D2H inside the timed region.
+  e2e_stream   the streamed video API (p3s_video_convert, 4 streams), median of 3 runs.
+  configs_extra  configs[3] (2400 4K frames sharded over the ranks, e2e), configs[2] (300
+               frames), configs[4] (8 x 8K HSBS per GPU), configs[0] (1080p, HBM-resident ring).
+  parity       the timed paths' bytes against the reference's digests (tests/golden): a
+               mismatch aborts the run before any number is printed.
   roofline     the dominant kernel (k_bilateral_sep): range-table lookup bytes per second
                against the measured shared-memory gather peak; roofline_hbm: the DIBR and
                depth kernels against the measured HBM bandwidth.
   cpu_baseline the reference's own CPU implementation (oracle/_ref, compiled from the
-               reference sources) on this host's cores, on a bounded sample.
+               reference sources) on this host's cores, per SURVEY.md 8(d).
 `--impl reference` prints the reference arm's line (rank 0 only).
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
 import statistics
@@ -49,10 +56,7 @@ W4K, H4K = 3840, 2160
 RING = 8
 SWEEP = [0, 2, 16, 30, 60, 120, 254, 510]
 L2_BYTES = 126 * 2**20
-# kernels per step on the default route (ncu launch list in profiles/): k_depth_front,
-# k_block_values, k_upsample, k_bilateral_sep, k_bilateral_fixup2, k_dibr_quad<0>,
-# k_inpaint_tiles (the per-frame counters are cleared by memsets on this path)
-LAUNCHES_PER_STEP = 7
+VIDEO_FRAMES = 2400  # configs[3]
 
 # The workload both arms measure (BASELINE.json metric on configs[1]); the arms add how
 # they ran it under "parallelism".
@@ -73,6 +77,49 @@ def measured_peaks():
         with open(path) as f:
             return json.load(f), "measured (MEASURED_PEAKS.json)"
     return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def manifest_digests():
+    with open(os.path.join(ROOT, "tests", "golden", "manifest.json")) as f:
+        return json.load(f)["digests"]
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def digest_for_seed(digests, w, h, seed, cfg_over=None):
+    """The reference digest of synthetic frame (w, h, seed) under the default config."""
+    for d in digests.values():
+        if d["w"] == w and d["h"] == h and d["seed"] == seed and d["cfg"].get("base", -1) == -1 \
+                and d["cfg"].get("formats", 1) == 1 and not cfg_over:
+            return d
+    return None
+
+
+def cpu_info():
+    model, cores = None, set()
+    phys = core = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name" and model is None:
+                    model = v
+                elif k == "physical id":
+                    phys = v
+                elif k == "core id":
+                    core = v
+                elif not k and phys is not None and core is not None:
+                    cores.add((phys, core))
+                    phys = core = None
+    except OSError:
+        pass
+    if phys is not None and core is not None:
+        cores.add((phys, core))
+    return {"model": model, "physical_cores": len(cores) or None, "logical_cpus": os.cpu_count(),
+            "usable_cpus": len(os.sched_getaffinity(0))}
 
 
 class ClockSampler:
@@ -142,52 +189,92 @@ def bilateral_flops(w: int, h: int, sigma_s: float = 8.0) -> float:
     return 4.0 * taps_1d(w, r) * taps_1d(h, r)
 
 
-def make_frames(w, h, n, seed0, checker=None):
-    import oracle
-    o = checker or oracle.load("port")
-    return [o.synthetic_frame(w, h, seed0 + i) for i in range(n)]
+class Dist:
+    """torch.distributed plumbing: barriers and max-over-ranks (identity at world 1)."""
 
+    def __init__(self, world: int, local: int):
+        self.world = world
+        self.on = world > 1
+        if self.on:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-def allreduce_max(vals, world, use_dist):
-    if world == 1 or not use_dist:
-        return vals
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return t.tolist()
+    def barrier(self):
+        if self.on:
+            import torch.distributed as dist
+            dist.barrier()
 
-
-def barrier(world):
-    if world > 1:
+    def max(self, *vals):
+        if not self.on:
+            return list(vals)
+        import torch
         import torch.distributed as dist
-        dist.barrier()
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def close(self):
+        if self.on:
+            import torch.distributed as dist
+            dist.destroy_process_group()
 
 
-def cpu_reference_rate(budget_s: float, max_reps: int, frame, kind="best"):
-    """Reference CPU path on all host cores, bounded sample of whole 4K frames."""
+# ---- reference arm / CPU baseline --------------------------------------------------------
+def reference_timings(frame, threads: int, reps: int, budget_s: float):
+    """The reference convert_image with Executor(threads) on one frame: per-rep wall s and
+    the reference's own StageTimings (depth_gen_ns, pure_ns, ...)."""
     import oracle
-    o = oracle.load(kind)
-    threads = os.cpu_count() or 1
+    o = oracle.load("best")
     cfg = oracle.Cfg()
-    times = []
+    walls, depth_ns, pure_ns = [], [], []
     t_all = time.perf_counter()
-    while len(times) < max_reps:
+    while len(walls) < reps:
         t0 = time.perf_counter()
-        o.convert(frame, cfg, threads=threads)
-        times.append(time.perf_counter() - t0)
+        out = o.convert(frame, cfg, threads=threads)
+        walls.append(time.perf_counter() - t0)
+        t = out["timings"]
+        depth_ns.append(int(t[0]))
+        pure_ns.append(int(t[6]))
         if time.perf_counter() - t_all > budget_s:
             break
-    return o.kind, threads, times
+    return o.kind, walls, depth_ns, pure_ns
+
+
+def cpu_baseline_rows(budget_s: float):
+    """Executor(nproc) and Executor(1), median of >= 3 reps where the budget
+    allows (one labelled rep otherwise), depth_ns / pure_ns (reference pipeline.hpp:24-26) and
+    wall e2e, at 1080p, 4K and 8K."""
+    import paper_2009_09501_b200 as p3s
+    nproc = len(os.sched_getaffinity(0))
+    rows = []
+    kind = None
+    for (w, h, name) in ((1920, 1080, "1080p"), (W4K, H4K, "4K"), (7680, 4320, "8K")):
+        frame = p3s.synthetic_frame(w, h, 1)
+        for threads in (nproc, 1):
+            if name == "8K" and threads == 1:
+                continue  # ~100 s for one rep: not run
+            reps = 3 if (threads == nproc or name == "1080p") else 1
+            kind, walls, dns, pns = reference_timings(frame, threads, reps, budget_s)
+            rows.append({"size": name, "threads": threads, "reps": len(walls),
+                         "frames_per_s": 1.0 / statistics.median(walls),
+                         "wall_ms_median": 1e3 * statistics.median(walls),
+                         "depth_gen_ms_median": statistics.median(dns) / 1e6,
+                         "pure_ms_median": statistics.median(pns) / 1e6,
+                         "note": "median of reps" if len(walls) >= 3 else
+                                 f"{len(walls)} rep(s) only (time budget)"})
+    return kind, nproc, rows
 
 
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    frame = make_frames(W4K, H4K, 1, 1)[0]
+    import paper_2009_09501_b200 as p3s
     import oracle
+    frame = p3s.synthetic_frame(W4K, H4K, 1)
     o = oracle.load("best")
-    threads = os.cpu_count() or 1
+    threads = len(os.sched_getaffinity(0))
     cfg = oracle.Cfg()
     # warm-up frames (page-in, thread-pool start); each is a whole 4K frame on the CPU, so
     # the count is capped at 5 to keep the run bounded
@@ -195,16 +282,19 @@ def run_reference_arm(args, rank, world):
     for _ in range(nwarm):
         o.convert(frame, cfg, threads=threads)
     budget = args.reference_budget
-    times = []
+    times, depth_ns, pure_ns = [], [], []
     t_all = time.perf_counter()
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        o.convert(frame, cfg, threads=threads)
+        out = o.convert(frame, cfg, threads=threads)
         times.append(time.perf_counter() - t0)
+        depth_ns.append(int(out["timings"][0]))
+        pure_ns.append(int(out["timings"][6]))
         if time.perf_counter() - t_all > budget:
             break
     total = sum(times)
     fps = len(times) / total
+    info = cpu_info()
     line = {
         "impl": "reference", "metric": "4K stereo frames/sec", "value": fps, "unit": "frames/s",
         "n_gpus": args.gpus, "steps": len(times), "steps_requested": args.steps,
@@ -215,13 +305,22 @@ def run_reference_arm(args, rank, world):
                                                 f"from the reference sources), {threads} host "
                                                 f"threads, synthetic_frame seed 1"),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads,
-                         "kind": o.kind,
+                         "kind": o.kind, "cpu": info,
+                         "depth_gen_ms_median": statistics.median(depth_ns) / 1e6,
+                         "pure_ms_median": statistics.median(pure_ns) / 1e6,
                          "sample": f"{len(times)} whole UHD frames (time budget {budget:.0f}s), "
                                    f"convert_image with Executor({threads})"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ---- our arm --------------------------------------------------------------------------
+def relaunch_under_torchrun(args) -> int:
+    from paper_2009_09501_b200.sharding import torchrun_argv
+    argv = torchrun_argv(args.gpus, os.path.abspath(__file__), sys.argv[1:])
+    return subprocess.call(argv, env=dict(os.environ, P3S_BENCH_RELAUNCHED="1"))
 
 
 def main():
@@ -232,56 +331,64 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the video / 8K config lines")
+    ap.add_argument("--no-extra", action="store_true", help="skip the video / 8K / 1080p lines")
     ap.add_argument("--streams", type=int, default=4,
                     help="plans/streams the device-resident frames are pipelined over")
     ap.add_argument("--inpaint-ctas", type=int, default=-1,
                     help="inpaint CTAs per lane when --streams > 1 (-1: SMs / 4; 0: one per SM)")
+    ap.add_argument("--video-frames", type=int, default=VIDEO_FRAMES)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--reference-budget", type=float, default=150.0)
+    ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     rank, world, local = dist_env()
+    if world == 1 and args.gpus > 1 and not os.environ.get("P3S_BENCH_RELAUNCHED"):
+        sys.exit(relaunch_under_torchrun(args))
+    if args.launch_selftest:  # CPU test of the launch path (tests/test_bench_launch.py)
+        print(json.dumps({"rank": rank, "world": world, "local": local}), flush=True)
+        return
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but {world} process(es) were launched")
 
     import paper_2009_09501_b200 as p3s
+    from paper_2009_09501_b200.sharding import bind_to_node, frame_seed, shard_frames
     if not os.path.exists(p3s.LIB_PATH):
         p3s.build()
-    use_dist = world > 1
-    if use_dist:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    host_affinity = os.sched_getaffinity(0)
+    dist = Dist(world, local)
     p3s.set_device(local)
+    numa = p3s.numa_node(local)
+    numa_bound = bind_to_node(numa)  # the rank's pinned rings below are node-local
+    digests = manifest_digests()
+    N = W4K * H4K
 
     cfg = p3s.Config()
     pipe = p3s.Pipeline(W4K, H4K, cfg)
-    # frames: distinct per rank (frame-sharded video); seeds follow the reference's
-    # video convention seed = 1 + global frame index
-    from paper_2009_09501_b200.sharding import frame_seed, shard_frames
+    # frames: distinct per rank (frame-sharded video); seeds follow the reference's video
+    # convention seed = 1 + global frame index
     mine = shard_frames(RING * world, rank, world)  # frame i -> rank i mod world
-    o = __import__("oracle").load("port")
-    frames = [o.synthetic_frame(W4K, H4K, frame_seed(i)) for i in mine]
+    seeds = [frame_seed(i) for i in mine]
+    frames = [p3s.synthetic_frame(W4K, H4K, s) for s in seeds]
     ring = [p3s.DeviceBuffer(pipe.frame_bytes) for _ in range(RING)]
     for f, d in zip(frames, ring):
         pipe.upload(f, d.addr)
     p3s.stream_sync(pipe.stream)
     stream = pipe.stream
+    gate = digest_for_seed(digests, W4K, H4K, seeds[0])  # reference bytes of ring frame 0
+    parity = {}
 
     # ---- kernel path: inputs resident in HBM ----
     # Frames are independent (a video), so the device-resident loop pipelines them over
     # `--streams` plans, frame i on plan i % streams: one frame's latency-bound kernels
     # (depth, DIBR, inpaint, their launch tails) overlap another frame's work. Untimed runs
     # replay one CUDA graph per (plan, ring frame), captured during the warm-up; the per-stage
-    # breakdown comes from a separate event-timed pass below.
-    # With several lanes in flight, each lane's cooperative inpaint runs on a quarter of the
-    # SMs (Pipeline.set_inpaint_ctas): its rounds are latency-bound, so the SMs it leaves go
-    # to the other lanes' filters (more aggregate frames/s). The single-stream leg and the
-    # stage breakdown use `pipe`, which keeps one inpaint CTA per SM (lowest latency).
+    # breakdown comes from a separate event-timed pass below. With several lanes in flight,
+    # each lane's cooperative inpaint runs on a quarter of the SMs (Pipeline.set_inpaint_ctas).
     nl = max(1, args.streams)
     inpaint_ctas = args.inpaint_ctas if args.inpaint_ctas >= 0 else (p3s.sm_count() // 4 if nl > 1 else 0)
     lanes = [p3s.Pipeline(W4K, H4K, cfg) for _ in range(nl)] if nl > 1 else [pipe]
@@ -310,13 +417,27 @@ def main():
         return a.elapsed_ms(z)
 
     clocks = ClockSampler(local)
-    barrier(world)
+    dist.barrier()
     p3s.device_sync()
     clocks.start()
     time.sleep(0.3)  # let nvidia-smi attach before the region
+    launches0 = p3s.launch_count()
     elapsed_ms = timed_loop(lanes, args.steps)
+    launches = p3s.launch_count() - launches0
     clk = clocks.stop()
-    barrier(world)
+    dist.barrier()
+
+    # parity gate: every lane's graph replay of ring frame 0 (the timed path exactly)
+    # against the reference's digest of that frame
+    if gate is not None:
+        for k, ln in enumerate(lanes):
+            ln.run(ring[0].addr)
+            _, filt, ana = ln.download()
+            if sha(ana) != gate["anaglyph"] or sha(filt) != gate["filtered"]:
+                raise SystemExit(f"bench: parity gate failed: lane {k} (value loop) output of seed "
+                                 f"{seeds[0]} differs from the reference digest")
+        parity["value_loop"] = f"{len(lanes)} lanes, graph replay, seed {seeds[0]}: = reference digest"
+
     single_ms = timed_loop([pipe], min(args.steps, 100))  # one stream: frames back to back
     # stage breakdown (CUDA events between stages, direct launches)
     pipe.timing_sum(reset=True)
@@ -325,64 +446,75 @@ def main():
         pipe.run(ring[i % RING].addr, timed=True)
     stage_sum, nruns = pipe.timing_sum(reset=True)
     bil_kernel_sum, bil_kernel_n = pipe.bilateral_kernel_sum(reset=True)
-    (elapsed_max,) = allreduce_max([elapsed_ms], world, use_dist)
+    (elapsed_max,) = dist.max(elapsed_ms)
     total_frames = args.steps * world
     fps = total_frames / (elapsed_max / 1e3)
-
-    # correctness spot check of the last frame against the CPU oracle is done by the
-    # parity tests; here only assert the device produced a plausible output
-    depth, filt, out = pipe.download()
-    assert out.any() and filt.any()
 
     # ---- e2e through the drop-in C ABI (host pinned frames, H2D + D2H per step) ----
     L = p3s.lib()
     images = [p3s.Image(f) for f in frames]
     res = C.c_void_p()
+    ana_ptr = C.c_void_p()
     for i in range(max(2, args.warmup // 2)):
         p3s._check(L.p3s_convert(images[i % RING].h, cfg.h, C.byref(res)))
         L.p3s_result_free(res)
+    if gate is not None:  # the e2e path's bytes of ring frame 0
+        p3s._check(L.p3s_convert(images[0].h, cfg.h, C.byref(res)))
+        p3s._check(L.p3s_result_output(res, 1, C.byref(ana_ptr)))
+        ana = np.stack([np.ctypeslib.as_array(C.cast(L.p3s_image_plane(ana_ptr, c), C.POINTER(C.c_uint8)),
+                                              shape=(N,)) for c in range(3)])
+        ok = sha(ana) == gate["anaglyph"]
+        L.p3s_result_free(res)
+        if not ok:
+            raise SystemExit("bench: parity gate failed: p3s_convert output differs from the reference digest")
+        parity["e2e"] = f"p3s_convert seed {seeds[0]}: = reference digest"
     e2e_steps = max(10, min(args.steps, 100))
-    barrier(world)
+    dist.barrier()
     t0 = time.perf_counter()
-    ana_ptr = C.c_void_p()
     checksum = 0
     for i in range(e2e_steps):
         p3s._check(L.p3s_convert(images[i % RING].h, cfg.h, C.byref(res)))
         p3s._check(L.p3s_result_output(res, 1, C.byref(ana_ptr)))
         plane = C.cast(L.p3s_image_plane(ana_ptr, 0), C.POINTER(C.c_uint8))
-        checksum += plane[(i * 7919) % (W4K * H4K)]  # touch the host result
+        checksum += plane[(i * 7919) % N]  # touch the host result
         L.p3s_result_free(res)
     e2e_s = time.perf_counter() - t0
-    barrier(world)
-    (e2e_max,) = allreduce_max([e2e_s], world, use_dist)
+    dist.barrier()
+    (e2e_max,) = dist.max(e2e_s)
     e2e_fps = e2e_steps * world / e2e_max
-    N = W4K * H4K
 
     # ---- e2e through the streaming video API (pinned host frames, 4 streams) ----
     vid = p3s.Video(W4K, H4K, cfg, streams=4)
-    src = [p3s.PinnedBuffer(3 * N) for _ in range(RING)]
-    dst = [p3s.PinnedBuffer(3 * N) for _ in range(RING)]
+    src = [p3s.PinnedBuffer(3 * N, near_device=local) for _ in range(RING)]
+    dst = [p3s.PinnedBuffer(3 * N, near_device=local) for _ in range(RING)]
     for b, f in zip(src, frames):
         b.array[:] = f.reshape(-1)
     vid.convert_ptrs([b.ptr for b in src[:4]], [b.ptr for b in dst[:4]])  # warm-up
+    if gate is not None:
+        if sha(dst[0].array) != gate["anaglyph"]:
+            raise SystemExit("bench: parity gate failed: p3s_video_convert output differs")
+        parity["e2e_stream"] = f"p3s_video_convert seed {seeds[0]}: = reference digest"
     nvid = max(RING, (min(args.steps, 96) // RING) * RING)
     fptrs = [src[i % RING].ptr for i in range(nvid)]
     optrs = [dst[i % RING].ptr for i in range(nvid)]
-    barrier(world)
-    t0 = time.perf_counter()
-    vid.convert_ptrs(fptrs, optrs)
-    vs = time.perf_counter() - t0
-    barrier(world)
-    (vs_max,) = allreduce_max([vs], world, use_dist)
-    e2e_stream = {"value": nvid * world / vs_max, "unit": "frames/s",
+    vs_runs = []
+    for _ in range(3):
+        dist.barrier()
+        t0 = time.perf_counter()
+        vid.convert_ptrs(fptrs, optrs)
+        vs = time.perf_counter() - t0
+        dist.barrier()
+        (vs_max,) = dist.max(vs)
+        vs_runs.append(nvid * world / vs_max)
+    e2e_stream = {"value": statistics.median(vs_runs), "unit": "frames/s", "runs": vs_runs,
                   "h2d_bytes_per_step": 3 * N, "d2h_bytes_per_step": 3 * N, "steps": nvid,
-                  "path": "p3s_video_convert (C ABI), 4 streams, pinned host frames in and "
-                          "anaglyph out; H2D/compute/D2H of neighbouring frames overlap"}
-    del vid
+                  "path": "p3s_video_convert (C ABI), 4 streams, pinned NUMA-local host frames in "
+                          "and anaglyph out; H2D/compute/D2H of neighbouring frames overlap; "
+                          "median of 3 runs"}
 
-    # ---- parallax sweep (configs[1]: "max parallax sweep") ----
+    # ---- parallax sweep (configs[1]: "max parallax sweep"; one GPU) ----
     sweep = {}
-    if not args.no_sweep:
+    if not args.no_sweep and world == 1:
         for b in SWEEP:
             pb = p3s.Pipeline(W4K, H4K, p3s.Config(base=b))
             for i in range(3):
@@ -399,57 +531,91 @@ def main():
             st, n = pb.timing_sum(reset=True)
             passes = pb.inpaint_stats()
             sweep[str(b)] = {"frames_per_s": ns / (a.elapsed_ms(z) / 1e3),
-                             "inpaint_ms": (st["inpaint_left_ns"]) / n / 1e6,
+                             "inpaint_ms": (st["inpaint_left_ns"] + st["inpaint_right_ns"]) / n / 1e6,
                              "dibr_ms": st["dibr_ns"] / n / 1e6,
                              "inpaint_passes": [int(passes[0]), int(passes[3])]}
+            d = next((v for v in digests.values() if v["w"] == W4K and v["seed"] == seeds[0]
+                      and v["cfg"].get("base") == b and v["cfg"].get("formats", 1) == 1), None)
+            if d is not None and seeds[0] == 1:
+                pb.run(ring[0].addr)
+                _, _, ana = pb.download()
+                if sha(ana) != d["anaglyph"]:
+                    raise SystemExit(f"bench: parity gate failed: sweep B={b}")
+                sweep[str(b)]["parity"] = "= reference digest"
             del pb
 
     # ---- the other BASELINE configs, measured alongside (not the headline) ----
     extra = {}
     if not args.no_extra:
-        # configs[2]: 4K video, 300 frames streamed H2D/compute/D2H on this GPU
+        # configs[3]: 4K video, --video-frames frames sharded over the ranks (frame i on rank
+        # i mod N), e2e from each rank's NUMA-local pinned ring through p3s_video_convert
         vid = p3s.Video(W4K, H4K, cfg, streams=4)
-        fp = [src[i % RING].ptr for i in range(300)]
-        op = [dst[i % RING].ptr for i in range(300)]
-        vid.convert_ptrs(fp[:6], op[:6])
-        barrier(world)
+        nmine = len(shard_frames(args.video_frames, rank, world))
+        fp = [src[i % RING].ptr for i in range(nmine)]
+        op = [dst[i % RING].ptr for i in range(nmine)]
+        vid.convert_ptrs(fp[:8], op[:8])
+        dist.barrier()
         t0 = time.perf_counter()
         vid.convert_ptrs(fp, op)
         vt = time.perf_counter() - t0
-        barrier(world)
-        (vt,) = allreduce_max([vt], world, use_dist)
-        extra["video_4k_300"] = {"frames_per_s": 300 * world / vt, "frames": 300 * world,
-                                 "path": "p3s_video_convert, 4 streams, pinned ring of 8 "
-                                         "distinct frames per GPU, anaglyph out (e2e)"}
+        dist.barrier()
+        (vt_max,) = dist.max(vt)
+        extra["video_4k_sharded"] = {
+            "config": "BASELINE configs[3]", "frames": args.video_frames, "n_gpus": world,
+            "frames_per_s": args.video_frames / vt_max,
+            "frames_per_s_per_gpu": args.video_frames / vt_max / world,
+            "mpix_per_s": args.video_frames * N / vt_max / 1e6,
+            "numa_node": numa, "numa_bound": numa_bound,
+            "path": "p3s_video_convert per rank (4 streams), frame i on rank i mod N, pinned "
+                    "NUMA-local ring of 8 distinct frames per rank, anaglyph out (e2e, H2D + D2H "
+                    "inside); time = max over ranks"}
+        # configs[2]: 4K video, 300 frames streamed on one GPU (rank 0's device alone)
+        if world == 1:
+            fp = [src[i % RING].ptr for i in range(300)]
+            op = [dst[i % RING].ptr for i in range(300)]
+            t0 = time.perf_counter()
+            vid.convert_ptrs(fp, op)
+            vt = time.perf_counter() - t0
+            extra["video_4k_300"] = {"config": "BASELINE configs[2]", "frames_per_s": 300 / vt,
+                                     "frames": 300,
+                                     "path": "p3s_video_convert, 4 streams, pinned ring of 8 "
+                                             "distinct frames, anaglyph out (e2e)"}
         del vid
-        # configs[4]: 8K anamorph (HSBS), 8 frames per GPU (64 over 8 GPUs)
+        # configs[4]: 8K anamorph (HSBS), 8 frames per GPU (64 over 8 GPUs), device-resident
         W8, H8 = 7680, 4320
         c8 = p3s.Config(formats=p3s.HSBS)
         p8 = p3s.Pipeline(W8, H8, c8)
-        o8 = __import__("oracle").load("port")
         ring8 = []
-        for i in range(4):
+        seeds8 = [frame_seed(i) for i in shard_frames(8 * world, rank, world)]
+        for s8 in seeds8:
             d = p3s.DeviceBuffer(p8.frame_bytes)
-            p8.upload(o8.synthetic_frame(W8, H8, frame_seed(1000 + 4 * rank + i)), d.addr)
+            p8.upload(p3s.synthetic_frame(W8, H8, s8), d.addr)
             ring8.append(d)
         for i in range(2):
             p8.run(ring8[i].addr, timed=True)
         p3s.stream_sync(p8.stream)
+        if seeds8[0] == 1:
+            p8.run(ring8[0].addr)
+            _, _, hs = p8.download(p3s.HSBS)
+            if sha(hs) != digests["hsbs_7680x4320"]["hsbs"]:
+                raise SystemExit("bench: parity gate failed: 8K HSBS")
+            parity["hsbs_8k"] = "seed 1: = reference digest"
         p8.timing_sum(reset=True)
         a8, z8 = p3s.Event(), p3s.Event()
-        barrier(world)
+        dist.barrier()
         a8.record(p8.stream)
-        for i in range(8):
-            p8.run(ring8[i % 4].addr, timed=True)
+        for d in ring8:
+            p8.run(d.addr, timed=True)
         z8.record(p8.stream)
         p3s.stream_sync(p8.stream)
-        (ms8,) = allreduce_max([a8.elapsed_ms(z8)], world, use_dist)
+        (ms8,) = dist.max(a8.elapsed_ms(z8))
         st8, n8 = p8.timing_sum(reset=True)
-        extra["hsbs_8k_batch8"] = {"frames_per_s": 8 * world / (ms8 / 1e3), "frames": 8 * world,
-                                   "mpix_per_s": 8 * world * W8 * H8 / (ms8 / 1e3) / 1e6,
-                                   "stages_ms": {k: v / n8 / 1e6 for k, v in st8.items()},
-                                   "path": "device-resident Pipeline, 7680x4320, HSBS output, "
-                                           "4 distinct frames (398 MB > L2)"}
+        extra["hsbs_8k"] = {"config": "BASELINE configs[4]", "frames": 8 * world, "n_gpus": world,
+                            "frames_per_s": 8 * world / (ms8 / 1e3),
+                            "mpix_per_s": 8 * world * W8 * H8 / (ms8 / 1e3) / 1e6,
+                            "stages_ms": {k: v / n8 / 1e6 for k, v in st8.items()},
+                            "path": "device-resident Pipeline, 7680x4320, HSBS output, 8 distinct "
+                                    "frames per GPU (796 MB > L2), CUDA events, max over ranks"}
         del p8, ring8
         # the exact-FP64 bilateral (no FP32 certificate) on the same 4K frames, for the FP64
         # roofline of that kernel: 4 separately rounded DMUL/DADD per tap
@@ -465,7 +631,7 @@ def main():
             stx, nx = px.timing_sum(reset=True)
             fil = stx["filter_ns"] / nx
             fp64 = p3s.fp64_peak()
-            ops = 4.0 * bilateral_flops(W4K, H4K) / 4.0
+            ops = bilateral_flops(W4K, H4K)
             extra["bilateral_exact_fp64"] = {
                 "filter_ms": fil / 1e6, "frames_per_s_pipeline": nx / (sum(stx[k] for k in (
                     "depth_gen_ns", "filter_ns", "dibr_ns", "inpaint_left_ns", "inpaint_right_ns",
@@ -477,55 +643,61 @@ def main():
             del px
         finally:
             del os.environ["P3S_BIL_FAST"]
-        # configs[0]: 1920x1080 -> depth + views + anaglyph (device-resident frames/s)
+        # configs[0]: 1920x1080 -> depth + views + anaglyph, device-resident, HBM-resident
+        # ring (64 distinct frames, 398 MB = 3.2 x L2)
         W1, H1 = 1920, 1080
         p1 = p3s.Pipeline(W1, H1, cfg)
+        n1 = 64
         ring1 = []
-        for i in range(8):
+        for i in range(n1):
             d = p3s.DeviceBuffer(p1.frame_bytes)
-            p1.upload(o8.synthetic_frame(W1, H1, frame_seed(2000 + 8 * rank + i)), d.addr)
+            p1.upload(p3s.synthetic_frame(W1, H1, frame_seed(i * world + rank)), d.addr)
             ring1.append(d)
-        # throughput: 128 frames pipelined over 4 plans (graph replay, inpaint on a quarter of
-        # the SMs, as the 4K lanes); stage times from a separate event-timed pass on p1
         lanes1 = [p3s.Pipeline(W1, H1, cfg) for _ in range(4)]
         for ln in lanes1:
             ln.set_inpaint_ctas(p3s.sm_count() // 4)
-            for i in range(8):
-                ln.run(ring1[i].addr)
+            for i in range(n1):
+                ln.run(ring1[i].addr)  # one graph per (lane, ring frame)
         p3s.device_sync()
+        if rank == 0:
+            d1 = digests["default_1920x1080"]
+            lanes1[0].run(ring1[0].addr)
+            _, f1, a1 = lanes1[0].download()
+            if sha(a1) != d1["anaglyph"] or sha(f1) != d1["filtered"]:
+                raise SystemExit("bench: parity gate failed: 1080p")
+            parity["image_1080p"] = "seed 1: = reference digest"
         a1, z1 = p3s.Event(), p3s.Event()
         ends1 = [p3s.Event() for _ in lanes1]
-        barrier(world)
+        nf1 = 256
+        dist.barrier()
         a1.record(lanes1[0].stream)
         for ln in lanes1[1:]:
             a1.wait(ln.stream)
-        for i in range(128):
-            lanes1[i % 4].run(ring1[i % 8].addr)
+        for i in range(nf1):
+            lanes1[i % 4].run(ring1[i % n1].addr)
         for ln, e in zip(lanes1, ends1):
             e.record(ln.stream)
             e.wait(lanes1[0].stream)
         z1.record(lanes1[0].stream)
         p3s.stream_sync(lanes1[0].stream)
-        (ms1,) = allreduce_max([a1.elapsed_ms(z1)], world, use_dist)
+        (ms1,) = dist.max(a1.elapsed_ms(z1))
         for i in range(3):
             p1.run(ring1[i].addr, timed=True)
         p3s.stream_sync(p1.stream)
         p1.timing_sum(reset=True)
         for i in range(16):
-            p1.run(ring1[i % 8].addr, timed=True)
-        st1, n1 = p1.timing_sum(reset=True)
-        extra["image_1080p"] = {"frames_per_s": 128 * world / (ms1 / 1e3),
-                                "stages_ms": {k: v / n1 / 1e6 for k, v in st1.items()},
-                                "path": "device-resident, 1920x1080 anaglyph, ring of 8 frames "
-                                        "(50 MB; L2-resident), 128 frames over 4 plans/streams; "
-                                        "stages_ms from one stream"}
-        del lanes1
-        del p1, ring1
+            p1.run(ring1[i % n1].addr, timed=True)
+        st1, n1r = p1.timing_sum(reset=True)
+        extra["image_1080p"] = {"config": "BASELINE configs[0]", "frames_per_s": nf1 * world / (ms1 / 1e3),
+                                "stages_ms": {k: v / n1r / 1e6 for k, v in st1.items()},
+                                "l2": f"ring of {n1} distinct frames ({n1 * 3 * W1 * H1 / 1e6:.0f} MB "
+                                      f"> 3 x 126 MB L2): HBM-resident",
+                                "path": f"device-resident, 1920x1080 anaglyph, {nf1} frames over 4 "
+                                        "plans/streams; stages_ms from one stream"}
+        del lanes1, p1, ring1
 
     if rank != 0:
-        if use_dist:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        dist.close()
         return
 
     # ---- rooflines ----
@@ -605,22 +777,37 @@ def main():
                         "p3s_image, then p3s_result_output(anaglyph) read on the host; depth "
                         "and filtered depth stay on the GPU until p3s_result_depth asks"},
         "e2e_stream": e2e_stream,
-        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "gpu_launches": launches,
+        "gpu_launches_note": "kernels launched in the timed value loop on rank 0, counted by the "
+                             "library (p3s_gpu_launch_count: direct launches + kernel nodes of "
+                             "each graph replay)",
         "clocks": clk,
+        "parity": parity,
+        "numa": {"node": numa, "bound": numa_bound},
         "sweep_base": sweep,
         "configs_extra": extra,
     }
     if not args.no_cpu_baseline and world == 1:
-        kind, threads, times = cpu_reference_rate(args.cpu_budget, 3, frames[0])
-        v = len(times) / sum(times)
+        os.sched_setaffinity(0, host_affinity)  # the CPU reference gets every host core
+        threads = len(host_affinity)
+        if args.no_extra:
+            kind, walls, _, pns = reference_timings(frames[0], threads, 3, args.cpu_budget)
+            rows = None
+            v, pure = 1.0 / statistics.median(walls), statistics.median(pns) / 1e6
+            nrep = len(walls)
+        else:
+            kind, _, rows = cpu_baseline_rows(args.cpu_budget)
+            r4 = next(r for r in rows if r["size"] == "4K" and r["threads"] == threads)
+            v, pure, nrep = r4["frames_per_s"], r4["pure_ms_median"], r4["reps"]
         line["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": threads, "kind": kind,
-                                "sample": f"{len(times)} whole UHD frame(s), default config, "
-                                          f"{threads} host threads"}
+                                "cpu": cpu_info(), "pure_ms_median": pure,
+                                "sample": f"{nrep} whole UHD frame(s) (synthetic seed 1), default "
+                                          f"config, convert_image with Executor({threads}), median"}
+        if rows is not None:
+            line["cpu_baseline"]["rows"] = rows
         line["speedup_vs_cpu_e2e"] = e2e_fps / v
     print(json.dumps(line), flush=True)
-    if use_dist:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    dist.close()
 
 
 if __name__ == "__main__":

@@ -21,6 +21,12 @@ namespace p3s {
 void* pinned_alloc(std::size_t bytes);
 void pinned_free(void* p) noexcept;
 bool pinned_is_page_locked(const void* p);
+// NUMA placement for multi-GPU hosts: the node of a CUDA device (-1 unknown), a fresh pinned
+// block whose pages sit on that node (released with pinned_free), and binding the calling
+// thread to the node's CPUs.
+int device_numa_node(int device);
+void* pinned_alloc_near(int device, std::size_t bytes);
+bool bind_thread_to_device_node(int device);
 
 // A byte array backed by the pinned pool (the reference uses std::vector<uint8_t>).
 class Plane {

@@ -131,9 +131,12 @@ P3S_API p3s_status p3s_pipeline_upload(p3s_pipeline* p, const uint8_t* r, const 
 typedef struct p3s_video p3s_video;
 P3S_API p3s_status p3s_video_create(int w, int h, const p3s_config* cfg, int streams,
                                     p3s_video** out);
-/* Frame-sharded over several GPUs of one box: frame i runs on devices[i % ndev] (one host
- * thread per device, `streams` plans each); frames are independent, so nothing crosses
- * NVLink and no collective runs. A device may be listed more than once. */
+/* Frame-sharded over several GPUs of one box: one host thread per device (`streams` plans
+ * each) takes the next frame index from a shared counter, so frames of uneven cost balance
+ * themselves; outputs land at their index. Frames are independent, so nothing crosses
+ * NVLink and no collective runs. If a device fails, it is retired and every frame it took
+ * is re-run on the others (the call still succeeds while one device is healthy). A device
+ * may be listed more than once. */
 P3S_API p3s_status p3s_video_create_devices(int w, int h, const p3s_config* cfg,
                                             const int* devices, int ndev, int streams,
                                             p3s_video** out);
@@ -145,6 +148,17 @@ P3S_API p3s_status p3s_video_convert(p3s_video* v, const uint8_t* const* frames,
 P3S_API p3s_status p3s_video_convert_interleaved(p3s_video* v, const uint8_t* const* frames,
                                                  int n, uint8_t* const* outs);
 P3S_API void p3s_video_free(p3s_video* v);
+/* Frames re-run on healthy devices after a device failed (summed over calls), and the
+ * devices still in service. A failed device is retired for the video's lifetime. */
+P3S_API long long p3s_video_requeued(const p3s_video* v);
+P3S_API int p3s_video_healthy_shards(const p3s_video* v);
+/* NUMA node of a CUDA device (-1 unknown) and a pinned block whose pages sit on it (for
+ * per-GPU frame rings on multi-socket hosts; release with p3s_host_free). */
+P3S_API int p3s_gpu_numa_node(int device);
+/* Kernels this library has launched in this process (direct launches plus the kernel nodes
+ * of every graph replay): the bench's gpu_launches is a difference of two readings. */
+P3S_API unsigned long long p3s_gpu_launch_count(void);
+P3S_API void* p3s_host_alloc_near(int device, size_t bytes);
 
 /* ---- helpers ---- */
 P3S_API p3s_status p3s_gpu_malloc(size_t bytes, void** out); /* zero-filled */

@@ -172,6 +172,11 @@ _SIGS = {
     "p3s_gpu_smem_peak": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
     "p3s_gpu_bilateral_path": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "p3s_synthetic_frame": (C.c_int, [C.c_int, C.c_int, C.c_uint64, u8p, u8p, u8p]),
+    "p3s_video_requeued": (C.c_longlong, [vp]),
+    "p3s_video_healthy_shards": (C.c_int, [vp]),
+    "p3s_gpu_numa_node": (C.c_int, [C.c_int]),
+    "p3s_host_alloc_near": (vp, [C.c_int, C.c_size_t]),
+    "p3s_gpu_launch_count": (C.c_ulonglong, []),
 }
 
 _lib = None
@@ -538,6 +543,15 @@ class Video:
     def shards(self) -> int:
         return lib().p3s_video_shards(self.handle)
 
+    @property
+    def requeued(self) -> int:
+        """Frames re-run on healthy devices after a device failed."""
+        return lib().p3s_video_requeued(self.handle)
+
+    @property
+    def healthy_shards(self) -> int:
+        return lib().p3s_video_healthy_shards(self.handle)
+
     def __del__(self):
         if getattr(self, "handle", None) and _lib is not None:
             _lib.p3s_video_free(self.handle)
@@ -554,10 +568,14 @@ class Video:
 
 
 class PinnedBuffer:
-    """A pinned host allocation from the library's pool, viewed as a numpy array."""
+    """A pinned host allocation from the library's pool, viewed as a numpy array
+    (near_device: pages placed on that GPU's NUMA node)."""
 
-    def __init__(self, nbytes: int):
-        self.ptr = lib().p3s_host_alloc(nbytes)
+    def __init__(self, nbytes: int, near_device: int | None = None):
+        if near_device is None:
+            self.ptr = lib().p3s_host_alloc(nbytes)
+        else:
+            self.ptr = lib().p3s_host_alloc_near(near_device, nbytes)
         if not self.ptr:
             raise MemoryError("p3s_host_alloc")
         self.nbytes = nbytes
@@ -621,6 +639,16 @@ def synthetic_frame(w: int, h: int, seed: int = 1) -> np.ndarray:
     out = np.empty((3, h, w), np.uint8)
     _check(lib().p3s_synthetic_frame(w, h, seed, _p(out[0]), _p(out[1]), _p(out[2])))
     return out
+
+
+def launch_count() -> int:
+    """Kernels the library launched in this process (graph replays count their kernel
+    nodes)."""
+    return int(lib().p3s_gpu_launch_count())
+
+
+def numa_node(device: int) -> int:
+    return int(lib().p3s_gpu_numa_node(device))
 
 
 def bilateral_fast_path(cfg) -> bool:

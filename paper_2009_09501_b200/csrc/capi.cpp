@@ -8,8 +8,12 @@
 // errors) map to P3S_ERR_INTERNAL with the CUDA message; there is no CPU fallback.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <exception>
 #include <map>
 #include <mutex>
 #include <memory>
@@ -55,15 +59,23 @@ struct p3s_pipeline {
     std::unique_ptr<p3s::Pipeline> p;
 };
 struct p3s_video {
-    // One shard per GPU: frame i goes to shard i % shards.size() (frames are independent,
-    // reference sequence.cpp:59-77), and inside a shard to stream (i / G) % streams.
+    // One shard per GPU, one host thread each. Frames are independent (reference
+    // sequence.cpp:59-77), so shards take the next frame index from a shared counter (a
+    // dynamic queue: frames of uneven cost, e.g. parallax-dependent inpaint, balance
+    // themselves) and pipeline it over their streams; outputs land at their frame index.
+    // A shard whose device fails is retired and every frame it took is re-queued to the
+    // healthy shards.
     struct Shard {
         int device = 0;
+        bool failed = false;
         std::vector<std::unique_ptr<p3s::Pipeline>> pipes;
     };
     std::vector<Shard> shards;
     int w = 0, h = 0;
     unsigned format = 1;
+    long long requeued = 0;     // frames re-run after a shard failed (all calls)
+    int fail_shard = -1;        // test hook (P3S_VIDEO_FAIL="shard:frames"): that shard
+    int fail_after = 0;         // throws a DeviceError after taking `fail_after` frames
 };
 
 namespace {
@@ -765,42 +777,102 @@ p3s_status video_create(int w, int h, const p3s_config* cfg, const int* devices,
             throw;
         }
         cudaSetDevice(caller);
+        if (const char* f = std::getenv("P3S_VIDEO_FAIL")) {
+            v->fail_shard = std::atoi(f);
+            const char* c = std::strchr(f, ':');
+            v->fail_after = c ? std::atoi(c + 1) : 0;
+        }
         *out = v.release();
     });
 }
 
-// Frames k, k + G, k + 2G, ... of one shard, pipelined over its streams on its device.
-// interleaved: frames/outs are RGB-interleaved payloads (converted on the device).
-void video_shard(p3s_video& v, std::size_t k, const uint8_t* const* frames, int n,
-                 uint8_t* const* outs, bool interleaved = false) {
-    p3s_video::Shard& sh = v.shards[k];
-    if (cudaSetDevice(sh.device) != cudaSuccess) {
-        cudaGetLastError();
-        throw p3s::DeviceError("cannot select CUDA device " + std::to_string(sh.device));
+// One convert call's shared state: the frame counter, the re-queue of failed shards' frames
+// and the first failure.
+struct VideoRun {
+    const uint8_t* const* frames;
+    uint8_t* const* outs;
+    int n;
+    bool interleaved;
+    std::atomic<int> next{0};
+    std::mutex mu;
+    std::deque<int> retry;
+    std::exception_ptr first_error;
+
+    int take() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!retry.empty()) {
+                const int i = retry.front();
+                retry.pop_front();
+                return i;
+            }
+        }
+        const int i = next.fetch_add(1);
+        return i < n ? i : -1;
     }
-    const std::size_t N = static_cast<std::size_t>(v.w) * v.h;
-    const std::size_t on = v.format == 4u ? 2 * N : N;
-    const std::size_t G = v.shards.size();
-    const std::size_t S = sh.pipes.size();
-    std::size_t j = 0;
-    for (std::size_t i = k; i < static_cast<std::size_t>(n); i += G, ++j) {
-        p3s::Pipeline& p = *sh.pipes[j % S];
+};
+
+void video_frame(p3s::Pipeline& p, const p3s_video& v, const VideoRun& run, int i, std::size_t N,
+                 std::size_t on);
+
+// Shard k's host thread: takes frames until the run is drained, pipelined over its streams.
+// interleaved: frames/outs are RGB-interleaved payloads (converted on the device).
+void video_shard(p3s_video& v, std::size_t k, VideoRun& run) {
+    p3s_video::Shard& sh = v.shards[k];
+    std::vector<int> taken;
+    try {
+        if (cudaSetDevice(sh.device) != cudaSuccess) {
+            cudaGetLastError();
+            throw p3s::DeviceError("cannot select CUDA device " + std::to_string(sh.device));
+        }
+        const std::size_t N = static_cast<std::size_t>(v.w) * v.h;
+        const std::size_t on = v.format == 4u ? 2 * N : N;
+        const std::size_t S = sh.pipes.size();
+        std::size_t j = 0;
+        for (int i; (i = run.take()) >= 0; ++j) {
+            taken.push_back(i);
+            if (static_cast<int>(k) == v.fail_shard && static_cast<int>(taken.size()) > v.fail_after)
+                throw p3s::DeviceError("injected device failure (P3S_VIDEO_FAIL) on shard " + std::to_string(k));
+            p3s::Pipeline& p = *sh.pipes[j % S];
+            video_frame(p, v, run, i, N, on);
+        }
+        for (auto& p : sh.pipes) {
+            const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(p->stream()));
+            if (e != cudaSuccess) throw p3s::DeviceError(cudaGetErrorString(e));
+        }
+    } catch (...) {
+        // the device is retired; its frames (done or not: outputs are simply rewritten) go
+        // back to the healthy shards once its queued work has drained (or failed)
+        for (auto& p : sh.pipes) cudaStreamSynchronize(static_cast<cudaStream_t>(p->stream()));
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(run.mu);
+        sh.failed = true;
+        if (!run.first_error) run.first_error = std::current_exception();
+        for (int i : taken) run.retry.push_back(i);
+        v.requeued += static_cast<long long>(taken.size());
+    }
+}
+}  // namespace
+
+namespace {
+void video_frame(p3s::Pipeline& p, const p3s_video& v, const VideoRun& run, int i, std::size_t N,
+                 std::size_t on) {
+    const bool interleaved = run.interleaved;
+    const uint8_t* const* frames = run.frames;
+    uint8_t* const* outs = run.outs;
+    {
         const uint8_t* f = frames[i];
         if (interleaved) {
             p.upload_interleaved(f, p.d_input());
             p.run(p.d_input());
             p.download_interleaved(static_cast<p3s::StereoFormat>(v.format), outs[i], nullptr, false);
-            continue;
+            return;
         }
         p.upload(f, f + N, f + 2 * N, p.d_input());
         p.run(p.d_input());
         uint8_t* o[3] = {outs[i], outs[i] + on, outs[i] + 2 * on};
         p.download_to(nullptr, nullptr, static_cast<p3s::StereoFormat>(v.format), o, nullptr,
                       false);
-    }
-    for (auto& p : sh.pipes) {
-        const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(p->stream()));
-        if (e != cudaSuccess) throw p3s::DeviceError(cudaGetErrorString(e));
     }
 }
 
@@ -818,6 +890,27 @@ p3s_status p3s_video_create_devices(int w, int h, const p3s_config* cfg, const i
 
 int p3s_video_shards(const p3s_video* v) { return v ? static_cast<int>(v->shards.size()) : 0; }
 
+long long p3s_video_requeued(const p3s_video* v) { return v ? v->requeued : 0; }
+
+int p3s_video_healthy_shards(const p3s_video* v) {
+    if (!v) return 0;
+    int n = 0;
+    for (const auto& s : v->shards) n += !s.failed;
+    return n;
+}
+
+void* p3s_host_alloc_near(int device, size_t bytes) {
+    try {
+        return p3s::pinned_alloc_near(device, bytes);
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+int p3s_gpu_numa_node(int device) { return p3s::device_numa_node(device); }
+
+unsigned long long p3s_gpu_launch_count(void) { return p3s::cu::launch_count(); }
+
 namespace {
 p3s_status video_convert(p3s_video* v, const uint8_t* const* frames, int n, uint8_t* const* outs,
                          bool interleaved) {
@@ -829,24 +922,32 @@ p3s_status video_convert(p3s_video* v, const uint8_t* const* frames, int n, uint
             int d;
             ~Restore() { cudaSetDevice(d); }
         } restore{caller};
-        if (v->shards.size() == 1) {
-            video_shard(*v, 0, frames, n, outs, interleaved);
-            return;
+        if (n < 0) throw std::invalid_argument("frame count must be >= 0");
+        VideoRun run;
+        run.frames = frames;
+        run.outs = outs;
+        run.n = n;
+        run.interleaved = interleaved;
+        // one host thread per healthy GPU, no data crossing between GPUs; repeated while
+        // frames of a failed shard wait in the re-queue and a healthy shard is left
+        for (;;) {
+            std::vector<std::size_t> live;
+            for (std::size_t k = 0; k < v->shards.size(); ++k)
+                if (!v->shards[k].failed) live.push_back(k);
+            if (live.empty()) {
+                if (run.first_error) std::rethrow_exception(run.first_error);
+                throw p3s::DeviceError("video: every device of this video has failed");
+            }
+            if (live.size() == 1) {
+                video_shard(*v, live[0], run);
+            } else {
+                std::vector<std::thread> threads;
+                for (std::size_t k : live) threads.emplace_back([&, k] { video_shard(*v, k, run); });
+                for (auto& t : threads) t.join();
+            }
+            std::lock_guard<std::mutex> lk(run.mu);
+            if (run.retry.empty() && run.next.load() >= n) break;
         }
-        // one host thread per GPU; no data crosses between GPUs
-        std::vector<std::exception_ptr> errs(v->shards.size());
-        std::vector<std::thread> threads;
-        for (std::size_t k = 0; k < v->shards.size(); ++k)
-            threads.emplace_back([&, k] {
-                try {
-                    video_shard(*v, k, frames, n, outs, interleaved);
-                } catch (...) {
-                    errs[k] = std::current_exception();
-                }
-            });
-        for (auto& t : threads) t.join();
-        for (auto& e : errs)
-            if (e) std::rethrow_exception(e);
     });
 }
 }  // namespace

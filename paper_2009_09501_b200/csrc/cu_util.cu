@@ -1,4 +1,7 @@
 // Small device-query helpers shared by the kernel launchers.
+#include <atomic>
+#include <vector>
+
 #include "p3s_cu.h"
 
 namespace p3s {
@@ -28,6 +31,36 @@ __global__ void k_zero(ZeroRanges z) {
 }
 }  // namespace
 
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}
+
+void note_launch(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        cs = cudaStreamCaptureStatusNone;
+    }
+    if (cs == cudaStreamCaptureStatusNone) g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void note_graph_launch(std::size_t kernels) { g_launches.fetch_add(kernels, std::memory_order_relaxed); }
+
+std::size_t graph_kernel_nodes(cudaGraph_t g) {
+    std::size_t n = 0;
+    if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess || n == 0) return 0;
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return 0;
+    std::size_t k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+}
+
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
 cudaError_t zero(const ZeroRanges& z, cudaStream_t st, bool by_kernel) {
     if (!by_kernel) {
         for (int r = 0; r < z.n; ++r) {
@@ -40,6 +73,7 @@ cudaError_t zero(const ZeroRanges& z, cudaStream_t st, bool by_kernel) {
     unsigned most = 1;
     for (int r = 0; r < z.n; ++r) most = z.words[r] > most ? z.words[r] : most;
     const unsigned blocks = (most + 255) / 256 < 256u ? (most + 255) / 256 : 256u;
+    note_launch(st);
     k_zero<<<blocks, 256, 0, st>>>(z);
     return cudaGetLastError();
 }

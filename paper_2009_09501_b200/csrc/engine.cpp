@@ -380,6 +380,7 @@ struct Pipeline::Impl {
     cudaEvent_t ev_prior = nullptr, ev_d2h = nullptr, ev_start = nullptr;
     std::vector<cudaEvent_t> ev_dbg;  // P3S_DEBUG_CONV: per band, filter start / end (timing)
     cudaGraphExec_t band_exec = nullptr, band_exec2 = nullptr;  // head, body
+    std::size_t band_k1 = 0, band_k2 = 0;                        // their kernel nodes
     cudaStream_t aux_stream = nullptr;  // side copies beside the frame's tail
     cudaEvent_t aux_done = nullptr;
     cudaStream_t aux() {
@@ -716,6 +717,7 @@ struct Pipeline::Impl {
     struct GraphEntry {
         const uint8_t* src;
         cudaGraphExec_t exec;
+        std::size_t kernels;  // kernel nodes (launch accounting)
     };
     std::list<GraphEntry> graphs;  // LRU
     static constexpr std::size_t kMaxGraphs = 16;
@@ -741,6 +743,7 @@ struct Pipeline::Impl {
             if (it->src == s) {
                 cache.splice(cache.begin(), cache, it);
                 CK(cudaGraphLaunch(cache.front().exec, st));
+                cu::note_graph_launch(cache.front().kernels);
                 return;
             }
         }
@@ -758,15 +761,17 @@ struct Pipeline::Impl {
         cudaGraph_t g = nullptr;
         CK(cudaStreamEndCapture(cap, &g));
         cudaGraphExec_t exec = nullptr;
+        const std::size_t kernels = cu::graph_kernel_nodes(g);
         const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
         cudaGraphDestroy(g);
         CK(e);
-        cache.push_front(GraphEntry{s, exec});
+        cache.push_front(GraphEntry{s, exec, kernels});
         while (cache.size() > kMaxGraphs) {
             cudaGraphExecDestroy(cache.back().exec);
             cache.pop_back();
         }
         CK(cudaGraphLaunch(exec, st));
+        cu::note_graph_launch(kernels);
     }
 
     // A timed frame for a synchronous caller (convert_image): graph replay with the plan's
@@ -967,7 +972,8 @@ struct Pipeline::Impl {
         record_event(ev[5], st);
     }
 
-    cudaGraphExec_t capture(void (Impl::*fn)(cudaStream_t, const std::array<cudaEvent_t, 7>&)) {
+    cudaGraphExec_t capture(void (Impl::*fn)(cudaStream_t, const std::array<cudaEvent_t, 7>&),
+                            std::size_t& kernels) {
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         try {
             (this->*fn)(stream, conv_ev);
@@ -981,6 +987,7 @@ struct Pipeline::Impl {
         cudaGraph_t g = nullptr;
         CK(cudaStreamEndCapture(stream, &g));
         cudaGraphExec_t exec = nullptr;
+        kernels = cu::graph_kernel_nodes(g);
         const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
         cudaGraphDestroy(g);
         CK(e);
@@ -1052,11 +1059,13 @@ struct Pipeline::Impl {
             upload_banded(img, st, 1, K);
             enqueue_banded_body(st, conv_ev);
         } else {
-            if (!band_exec) band_exec = capture(&Impl::enqueue_banded_head);
-            if (!band_exec2) band_exec2 = capture(&Impl::enqueue_banded_body);
+            if (!band_exec) band_exec = capture(&Impl::enqueue_banded_head, band_k1);
+            if (!band_exec2) band_exec2 = capture(&Impl::enqueue_banded_body, band_k2);
             CK(cudaGraphLaunch(band_exec, st));
+            cu::note_graph_launch(band_k1);
             upload_banded(img, st, 1, K);
             CK(cudaGraphLaunch(band_exec2, st));
+            cu::note_graph_launch(band_k2);
         }
         if (!outs || !band_back()) return false;
         const StereoFormat f = route == kFusedAnaglyph ? kFormatAnaglyph : kFormatFsbs;

@@ -1,7 +1,13 @@
 // Host value types, configuration validation and the pinned host-memory pool.
 #include <cuda_runtime.h>
+#include <pthread.h>
+#include <sched.h>
 
 #include <atomic>
+#include <cctype>
+#include <fstream>
+#include <sstream>
+#include <string>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -46,6 +52,23 @@ public:
             }
         }
         if (!p) {
+            p = std::aligned_alloc(4096, bytes);
+            if (!p) throw std::bad_alloc();
+        }
+        std::lock_guard<std::mutex> lk(mu_);
+        live_[p] = Block{bytes, pinned};
+        return p;
+    }
+
+    // a new allocation (never a cached block: the caller wants pages placed now)
+    void* alloc_fresh(std::size_t n) {
+        const std::size_t bytes = round(n);
+        void* p = nullptr;
+        bool pinned = false;
+        if (cuda_usable() && cudaHostAlloc(&p, bytes, cudaHostAllocPortable) == cudaSuccess) {
+            pinned = true;
+        } else {
+            cudaGetLastError();
             p = std::aligned_alloc(4096, bytes);
             if (!p) throw std::bad_alloc();
         }
@@ -109,6 +132,76 @@ PinnedPool& pool() {
 }  // namespace
 
 void* pinned_alloc(std::size_t bytes) { return pool().alloc(bytes); }
+
+// NUMA node of a CUDA device (sysfs numa_node of its PCI function; -1 when unknown).
+int device_numa_node(int device) {
+    char bus[64] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::string id(bus);
+    for (auto& c : id) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    std::ifstream f("/sys/bus/pci/devices/" + id + "/numa_node");
+    int node = -1;
+    if (!(f >> node)) return -1;
+    return node;
+}
+
+namespace {
+// CPUs of a NUMA node from sysfs ("0-55,112-167").
+bool node_cpus(int node, cpu_set_t& set) {
+    std::ifstream f("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist");
+    std::string list;
+    if (node < 0 || !std::getline(f, list)) return false;
+    CPU_ZERO(&set);
+    std::stringstream ss(list);
+    std::string part;
+    int n = 0;
+    while (std::getline(ss, part, ',')) {
+        const auto dash = part.find('-');
+        const int a = std::atoi(part.c_str());
+        const int b = dash == std::string::npos ? a : std::atoi(part.c_str() + dash + 1);
+        for (int c = a; c <= b && c < CPU_SETSIZE; ++c) {
+            CPU_SET(c, &set);
+            ++n;
+        }
+    }
+    return n > 0;
+}
+}  // namespace
+
+// Runs f with the calling thread bound to the CPUs of `device`'s NUMA node (first-touch and
+// cudaHostAlloc pages then come from that node), restoring the affinity afterwards.
+template <class F>
+static void on_device_node(int device, F&& f) {
+    cpu_set_t old, want;
+    const bool saved = pthread_getaffinity_np(pthread_self(), sizeof(old), &old) == 0;
+    const bool bind = saved && node_cpus(device_numa_node(device), want) &&
+                      pthread_setaffinity_np(pthread_self(), sizeof(want), &want) == 0;
+    try {
+        f();
+    } catch (...) {
+        if (bind) pthread_setaffinity_np(pthread_self(), sizeof(old), &old);
+        throw;
+    }
+    if (bind) pthread_setaffinity_np(pthread_self(), sizeof(old), &old);
+}
+
+void* pinned_alloc_near(int device, std::size_t bytes) {
+    void* p = nullptr;
+    on_device_node(device, [&] {
+        p = pool().alloc_fresh(bytes);
+        std::memset(p, 0, bytes);  // fault the pages in while bound to the node
+    });
+    return p;
+}
+
+bool bind_thread_to_device_node(int device) {
+    cpu_set_t want;
+    return node_cpus(device_numa_node(device), want) &&
+           pthread_setaffinity_np(pthread_self(), sizeof(want), &want) == 0;
+}
 void pinned_free(void* p) noexcept { pool().release(p); }
 bool pinned_is_page_locked(const void* p) { return pool().pinned(p); }
 

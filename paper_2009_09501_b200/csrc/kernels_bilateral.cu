@@ -771,6 +771,7 @@ cudaError_t launch_tiled(const uint8_t* depth, const uint8_t* guide, Geom gm, in
     const int tiles_y = (gm.h + kTY - 1) / kTY;
     const int ntiles = tiles_x * tiles_y;
     const int grid = min(ntiles, per_sm * sm_count());
+    note_launch(st);
     k_bilateral_tiled<N><<<grid, kNW * 32, smem, st>>>(sp, depth, guide, gm.pitch, gm.w, gm.h, R,
                                                        range, out, raw, tiles_x, ntiles);
     return cudaGetLastError();
@@ -799,6 +800,7 @@ cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
     const int tiles_y = (gm.h + TY - 1) / TY;
     const int ntiles = tiles_x * tiles_y;
     const int grid = min(ntiles, per_sm * sm_count());
+    note_launch(st);
     k_bilateral_r<R, P, NW, MINB, N><<<grid, NW * 32, smem, st>>>(sp, depth, guide, gm.pitch, gm.w, gm.h,
                                                       range, out, raw, tiles_x, ntiles);
     return cudaGetLastError();
@@ -839,6 +841,7 @@ cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
     if (tr1 <= tr0) return cudaSuccess;
     const int t0 = tr0 * tiles_x, t1 = tr1 * tiles_x;
     const int grid = min(t1 - t0, per_sm * sm_count());
+    note_launch(st);
     k_bilateral_sep<R, P, NW, U><<<grid, NW * 32, smem, st>>>(
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, t0, t1, tile_ctr,
         table);
@@ -855,6 +858,7 @@ cudaError_t launch_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm
     constexpr int WPB = R <= 16 ? 4 : 2;
     int ctas = sm_count() * 32 / WPB;
     if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
+    note_launch(st);
     k_bilateral_fixup2<R, WPB><<<ctas, WPB * 32, 0, st>>>(
         depth, guide, gm.pitch, gm.w, gm.h, spatial_dev, range, out, list, count);
     return cudaGetLastError();
@@ -939,6 +943,7 @@ __global__ void k_build_sep_table(const double* __restrict__ range_g, float* __r
 
 cudaError_t build_sep_table(const double* range, float* table, cudaStream_t st) {
     const int n = kSepEntries * kF32Copies;
+    note_launch(st);
     k_build_sep_table<<<(n + 255) / 256, 256, 0, st>>>(range, table);
     return cudaGetLastError();
 }
@@ -955,6 +960,7 @@ cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int r
                       const double* spatial, const double* range, uint8_t* out, double* raw,
                       cudaStream_t st) {
     dim3 grid((gm.w + 127) / 128, gm.h);
+    note_launch(st);
     k_bilateral_generic<<<grid, 128, 0, st>>>(depth, guide, gm.pitch, gm.w, gm.h, radius,
                                               spatial, range, out, raw);
     return cudaGetLastError();

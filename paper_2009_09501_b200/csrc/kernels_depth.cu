@@ -278,6 +278,7 @@ cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Ge
     const unsigned magic = span * static_cast<unsigned>(block) < (1ull << 32)
                                ? static_cast<unsigned>((1ull << 32) / static_cast<unsigned>(block) + 1ull)
                                : 0u;
+    note_launch(st);
     k_depth_front<<<grid, 256, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, sums, block, bx,
                                         tile_row0, magic);
     return cudaGetLastError();
@@ -288,6 +289,7 @@ cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTab
     if (brow1 < 0 || brow1 > t.by) brow1 = t.by;
     const int i0 = brow0 * t.bx, i1 = brow1 * t.bx;
     if (i1 <= i0) return cudaSuccess;
+    note_launch(st);
     k_block_values<<<(i1 - i0 + 255) / 256, 256, 0, st>>>(sums, gm.w, gm.h, t.block, t.bx, t.by,
                                                           t.alpha255, t.beta, t.row_denom, values,
                                                           i0, i1);
@@ -300,6 +302,7 @@ cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_
     if (yb <= ya) return cudaSuccess;
     dim3 grid((gm.w + kUpThreads * kUpCols - 1) / (kUpThreads * kUpCols),
               (yb - ya + kUpRows - 1) / kUpRows);
+    note_launch(st);
     k_upsample<<<grid, kUpThreads, 0, st>>>(values, t.bx, t.col_i0, t.col_i1, t.col_f, t.row_i0,
                                             t.row_i1, t.row_f, gm.w, gm.h, gm.pitch, depth, ya, yb);
     return cudaGetLastError();

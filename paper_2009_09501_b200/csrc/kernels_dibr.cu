@@ -620,6 +620,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         int qper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, qk, 256, qsmem);
         if (qper < 1) qper = 1;
+        note_launch(st);
         qk<<<min(rows, qper * sm_count()), 256, qsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
                                                              cols, left, right, ya, yb);
         return cudaGetLastError();
@@ -638,6 +639,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         int vper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, vk, 256, vsmem);
         if (vper < 1) vper = 1;
+        note_launch(st);
         vk<<<min(rows, vper * sm_count()), 256, vsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
                                                              cols, left, right, ya, yb);
         return cudaGetLastError();
@@ -649,6 +651,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
     if (per_sm < 1) per_sm = 1;
     const int grid = min(rows, per_sm * sm_count());
+    note_launch(st);
     kern<<<grid, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h, shift, cols,
                                   backward ? 1 : 0, left, right, ya, yb);
     return cudaGetLastError();
@@ -658,6 +661,7 @@ cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* lis
                          uint32_t* count, cudaStream_t st, uint32_t* bits, int mwords) {
     const int chunks = (gm.w + 15) / 16;
     dim3 grid((chunks + 127) / 128, gm.h);
+    note_launch(st);
     k_mask_to_list<<<grid, 128, 0, st>>>(mask, mpitch, gm.w, gm.h, list, count, bits, mwords);
     return cudaGetLastError();
 }
@@ -684,6 +688,7 @@ cudaError_t side_by_side_half(const uint8_t* const* left, const uint8_t* const* 
                          static_cast<uintptr_t>(out_pitch);
     if (hw % 16 == 0 && (al & 15) == 0) {
         const long long items = 2LL * 3 * (hw / 16) * gm.h;
+        note_launch(st);
         k_hsbs16<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(
             left[0], left[1], left[2], right[0], right[1], right[2], gm.pitch, gm.w, gm.h, out[0],
             out[1], out[2], out_pitch);
@@ -691,6 +696,7 @@ cudaError_t side_by_side_half(const uint8_t* const* left, const uint8_t* const* 
     }
     const int items = 2 * ((hw + 15) / 16);
     dim3 grid((items + 127) / 128, gm.h);
+    note_launch(st);
     k_hsbs<<<grid, 128, 0, st>>>(left[0], left[1], left[2], right[0], right[1], right[2],
                                  gm.pitch, gm.w, out[0], out[1], out[2], out_pitch);
     return cudaGetLastError();

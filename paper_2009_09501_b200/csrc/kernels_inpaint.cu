@@ -774,6 +774,7 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
         cudaMemcpyToSymbol(g_inp_rdbg, &rdbg, sizeof(rdbg));
     }
     if (want) cudaMemsetAsync(rdbg, 0, (4 * kDbgRounds + 4) * sizeof(unsigned long long), st);
+    note_launch(st);
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_inpaint_tiles), dim3(blocks),
                                     dim3(kThreads), args, smem, st);
 #ifdef P3S_INPAINT_PHASES

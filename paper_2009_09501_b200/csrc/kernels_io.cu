@@ -112,9 +112,11 @@ cudaError_t deinterleave(const uint8_t* src, int w, int h, uint8_t* r, uint8_t* 
                          int pitch, cudaStream_t st) {
     if (vec_ok(src, r, g, b, w, pitch)) {
         const long long items = static_cast<long long>(w / 16) * h;
+        note_launch(st);
         k_deinterleave16<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(src, w, h, r, g, b, pitch);
     } else {
         const long long items = static_cast<long long>(w) * h;
+        note_launch(st);
         k_deinterleave1<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(src, w, h, r, g, b, pitch);
     }
     return cudaGetLastError();
@@ -124,9 +126,11 @@ cudaError_t interleave(const uint8_t* r, const uint8_t* g, const uint8_t* b, int
                        int h, uint8_t* dst, cudaStream_t st) {
     if (vec_ok(dst, r, g, b, w, pitch)) {
         const long long items = static_cast<long long>(w / 16) * h;
+        note_launch(st);
         k_interleave16<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(r, g, b, pitch, w, h, dst);
     } else {
         const long long items = static_cast<long long>(w) * h;
+        note_launch(st);
         k_interleave1<<<static_cast<unsigned>((items + 255) / 256), 256, 0, st>>>(r, g, b, pitch, w, h, dst);
     }
     return cudaGetLastError();
@@ -169,6 +173,7 @@ cudaError_t patch_host(PatchEye left, PatchEye right, Geom gm, cudaStream_t st) 
     const int mwords = (gm.w + 31) >> 5, groups = (mwords + 31) >> 5;
     const long long warps = 2LL * gm.h * groups;
     const int blocks = static_cast<int>(std::min<long long>((warps + 7) / 8, sm_count() * 8LL));
+    note_launch(st);
     k_patch_host<<<blocks, 256, 0, st>>>(left, right, gm.w, gm.h);
     return cudaGetLastError();
 }

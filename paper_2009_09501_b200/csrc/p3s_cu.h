@@ -104,6 +104,14 @@ inline void once_per_device(std::atomic<unsigned long long>& done, F&& setup) {
 // Zero several ranges of whole 4-byte words (4-byte aligned): one kernel launch when
 // by_kernel (copy engines busy with PCIe traffic), else one memset per range (SMs busy
 // with other streams' kernels).
+// Kernel-launch accounting (the bench's gpu_launches): every launch site calls note_launch
+// (not counted while its stream is being captured into a graph); a graph replay adds the
+// kernel nodes of its graph.
+void note_launch(cudaStream_t st);
+void note_graph_launch(std::size_t kernels);
+std::size_t graph_kernel_nodes(cudaGraph_t g);
+unsigned long long launch_count();
+
 constexpr int kZeroRanges = 4;
 struct ZeroRanges {
     void* p[kZeroRanges];

@@ -48,6 +48,9 @@ DIGEST_CASES = [
     *[(f"b{b}_3840x2160", 3840, 2160, 1, dict(base=b)) for b in (0, 2, 16, 60, 254, 510)],
     # configs[4]: 8K anamorph (HSBS) output
     ("hsbs_7680x4320", 7680, 4320, 1, dict(formats=2)),
+    # configs[2]/[3] video frames (frame i: seed 1 + i; seed 1 is default_3840x2160): the
+    # multi-device sharding test checks every frame against these
+    *[(f"video4k_seed{s}", 3840, 2160, s, {}) for s in range(2, 9)],
 ]
 
 

@@ -234,14 +234,17 @@ def test_inpaint_stress_vs_oracle(p3s, checker):
         assert tuple(sa) == tuple(sb), (i, w, h, sa, sb)
 
 
-def test_video_frame_sharding_matches_convert(p3s, checker):
-    """Multi-device frame sharding (p3s_video_create_devices): frame i -> devices[i % n], one
-    host thread per device. On a one-GPU box the device is listed several times, which runs
-    the same threading and ordering logic; bytes must equal per-frame p3s_convert."""
+def test_video_frame_sharding_matches_oracle(p3s, checker):
+    """Multi-device frame sharding (p3s_video_create_devices): one host thread per device
+    takes frames from a shared counter. On a one-GPU box the device is listed several times,
+    which runs the same threading, queue and ordering logic; bytes must equal the CPU
+    oracle's."""
+    import oracle
     w, h = 320, 200
-    cfg = p3s.Config(base=18, formats=p3s.FSBS)
-    frames = [checker.synthetic_frame(w, h, s) for s in range(1, 10)]
-    expect = [p3s.convert(f, cfg)["fsbs"] for f in frames]
+    over = dict(base=18, formats=p3s.FSBS)
+    cfg = p3s.Config(**over)
+    frames = [p3s.synthetic_frame(w, h, s) for s in range(1, 10)]
+    expect = [checker.convert(f, oracle.Cfg(**over), threads=NCPU)["fsbs"] for f in frames]
     ndev = p3s.device_count()
     devices = [i % ndev for i in range(3)]
     vid = p3s.Video(w, h, cfg, streams=2, devices=devices)
@@ -253,6 +256,55 @@ def test_video_frame_sharding_matches_convert(p3s, checker):
     vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst])
     for b, e in zip(dst, expect):
         assert np.array_equal(b.array.reshape(3, h, 2 * w), e)
+    assert vid.requeued == 0 and vid.healthy_shards == 3
+
+
+def test_video_4k_every_device_matches_reference_digests(p3s, manifest):
+    """configs[2]/[3]: 4K video frames (frame i: seed 1 + i) sharded over every visible
+    device (listed twice on a one-GPU box), pinned rings on each device's NUMA node, each
+    anaglyph against the SHA-256 digest of the REFERENCE's own output."""
+    names = ["default_3840x2160"] + [f"video4k_seed{s}" for s in range(2, 9)]
+    digests = [manifest["digests"][n] for n in names]
+    w, h = 3840, 2160
+    ndev = p3s.device_count()
+    devices = list(range(ndev)) if ndev > 1 else [0, 0]
+    vid = p3s.Video(w, h, p3s.Config(), streams=2, devices=devices)
+    src, dst = [], []
+    for i, d in enumerate(digests):
+        dev = devices[i % len(devices)]
+        b = p3s.PinnedBuffer(3 * w * h, near_device=dev)
+        b.array[:] = p3s.synthetic_frame(w, h, d["seed"]).reshape(-1)
+        src.append(b)
+        dst.append(p3s.PinnedBuffer(3 * w * h, near_device=dev))
+    vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst])
+    for b, d in zip(dst, digests):
+        assert sha(b.array) == d["anaglyph"], d["seed"]
+
+
+def test_video_failed_device_frames_are_requeued(p3s, checker, monkeypatch):
+    """A device failure (injected on shard 1 after 2 frames) retires that shard and re-runs
+    every frame it took on the healthy shards; the call succeeds with the oracle's bytes."""
+    import oracle
+    monkeypatch.setenv("P3S_VIDEO_FAIL", "1:2")
+    w, h = 160, 96
+    over = dict(base=12)
+    frames = [p3s.synthetic_frame(w, h, s) for s in range(1, 13)]
+    expect = [checker.convert(f, oracle.Cfg(**over), threads=NCPU)["anaglyph"] for f in frames]
+    vid = p3s.Video(w, h, p3s.Config(**over), streams=2, devices=[0, 0, 0])
+    src = [p3s.PinnedBuffer(3 * w * h) for _ in frames]
+    dst = [p3s.PinnedBuffer(3 * w * h) for _ in frames]
+    for b, f in zip(src, frames):
+        b.array[:] = f.reshape(-1)
+    vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst])
+    assert vid.healthy_shards == 2 and vid.requeued >= 3
+    for b, e in zip(dst, expect):
+        assert np.array_equal(b.array.reshape(3, h, w), e)
+    # the retired shard stays out of later calls
+    for b in dst:
+        b.array[:] = 0
+    vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst])
+    for b, e in zip(dst, expect):
+        assert np.array_equal(b.array.reshape(3, h, w), e)
 
 
 def _ppm_bytes(img):
@@ -303,14 +355,17 @@ def test_convert_sequence_files_match_oracle(p3s, checker, tmp_path):
         f"f_{i:03d}_{n}.ppm" for i in (1, 2) for n in ("anaglyph", "fsbs"))
 
 
-def test_video_interleaved_matches_convert(p3s, checker):
+def test_video_interleaved_matches_oracle(p3s, checker):
     """p3s_video_convert_interleaved: PPM-order payloads in/out, (de)interleave on the GPU;
-    both the 16-pixel vector path (w % 16 == 0) and the per-pixel path (odd width)."""
+    both the 16-pixel vector path (w % 16 == 0) and the per-pixel path (odd width), against
+    the CPU oracle's planar output interleaved on the host."""
+    import oracle
     for (w, h, fmt) in ((128, 72, p3s.ANAGLYPH), (97, 41, p3s.FSBS)):
-        cfg = p3s.Config(base=12, formats=fmt)
-        frames = [checker.synthetic_frame(w, h, s) for s in range(1, 5)]
+        over = dict(base=12, formats=fmt)
+        cfg = p3s.Config(**over)
+        frames = [p3s.synthetic_frame(w, h, s) for s in range(1, 5)]
         key = "anaglyph" if fmt == p3s.ANAGLYPH else "fsbs"
-        expect = [p3s.convert(f, cfg)[key] for f in frames]
+        expect = [checker.convert(f, oracle.Cfg(**over), threads=NCPU)[key] for f in frames]
         ow = 2 * w if fmt == p3s.FSBS else w
         src = [p3s.PinnedBuffer(3 * w * h) for _ in frames]
         dst = [p3s.PinnedBuffer(3 * ow * h) for _ in frames]
@@ -319,7 +374,7 @@ def test_video_interleaved_matches_convert(p3s, checker):
         vid = p3s.Video(w, h, cfg, streams=2)
         vid.convert_ptrs([b.ptr for b in src], [b.ptr for b in dst], interleaved=True)
         for b, e in zip(dst, expect):
-            assert np.array_equal(b.array.reshape(h, ow, 3).transpose(2, 0, 1), e)
+            assert np.array_equal(b.array.reshape(h, ow, 3), np.ascontiguousarray(e.transpose(1, 2, 0)))
 
 
 @pytest.mark.parametrize("sigma_s", [3.1, 4.0, 4.3, 5.0, 5.5, 6.0, 6.5, 7.0, 7.4, 8.0, 8.3, 9.0,
