@@ -118,16 +118,22 @@ ImageRGB8 side_by_side(const ImageRGB8& left, const ImageRGB8& right, bool half,
 // D2H of the requested outputs plus depth and filtered depth.
 ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg, Device& dev);
 
-// The depth and filtered-depth maps of a conversion kept on the GPU until first asked for
-// (the C ABI's p3s_result_depth / _filtered_depth): a device copy made right after the
-// frame, downloaded on demand. Holds device memory from a process-wide pool until released.
+// The depth and filtered-depth maps of a conversion (the C ABI's p3s_result_depth /
+// _filtered_depth): a device copy made right after the frame's filter, downloaded into
+// pinned host maps in the background on a per-device copy stream (it does not hold up the
+// call that produced it; only the D2H direction of the link is shared with the outputs).
+// depth() / filtered() wait for that download; the device copy returns to a pool as soon as
+// it is done.
 class DeferredMaps {
 public:
     DeferredMaps(int device, int w, int h, void* dev_buf);
     ~DeferredMaps();
     DeferredMaps(const DeferredMaps&) = delete;
     DeferredMaps& operator=(const DeferredMaps&) = delete;
-    // Downloads both maps once (thread-safe); later calls return the cached host maps.
+    // Queues the D2H after `ready_event` (a cudaEvent_t recorded after the device copy) on
+    // the device's copy stream.
+    void start_download(void* ready_event);
+    // Waits for both maps once (thread-safe); later calls return the cached host maps.
     const GrayMap& depth();
     const GrayMap& filtered();
 
@@ -136,6 +142,7 @@ private:
     int device_, w_, h_;
     void* buf_;  // 2 * w * h bytes: depth then filtered depth (unpitched)
     GrayMap depth_, filtered_;
+    void* done_ = nullptr;  // cudaEvent_t: the background download's completion
     bool ready_ = false;
     std::mutex mu_;
 };

@@ -337,7 +337,7 @@ struct Pipeline::Impl {
     static constexpr int kBilSlots = 64;  // counters ahead of the list: 2 per band, K <= 32
     uint32_t* bil_count = nullptr;  // kBilSlots: counts, tile-claim counters of the bilateral launches
     uint32_t* ctl = nullptr;     // 128
-    long long* stats = nullptr;  // 6
+    long long* stats = nullptr;  // 8: inpaint passes/repaired/fallback per eye, per-eye busy ns
     // stage-API extras (allocated on first use)
     unsigned char* stage_arena = nullptr;
     uint8_t* stage_masks = nullptr;  // 2 byte masks
@@ -348,6 +348,16 @@ struct Pipeline::Impl {
     // times without synchronising between steps (harvested by accumulated()).
     static constexpr int kRing = 64;
     std::vector<std::array<cudaEvent_t, 7>> ring;
+    long long* ring_stats = nullptr;  // pinned [kRing][8]: the inpaint stats of each timed run
+    long long* conv_stats = nullptr;  // pinned [8]: the last conv run's inpaint stats
+
+    // Queues the D2H of the inpaint stats after a conv frame (read by timings()).
+    void copy_conv_stats(cudaStream_t st) {
+        if (backward) return;
+        if (!conv_stats)
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&conv_stats), 8 * sizeof(long long), cudaHostAllocPortable));
+        CK(cudaMemcpyAsync(conv_stats, stats, 8 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    }
     int ring_next = 0, last_slot = -1;
     std::deque<int> pending;
     StageTimings acc;
@@ -379,10 +389,12 @@ struct Pipeline::Impl {
     std::vector<cudaEvent_t> ev_in, ev_fork, ev_join, ev_rows;
     cudaEvent_t ev_prior = nullptr, ev_d2h = nullptr, ev_start = nullptr;
     std::vector<cudaEvent_t> ev_dbg;  // P3S_DEBUG_CONV: per band, filter start / end (timing)
+    bool last_banded = false;  // the last conv run used the banded schedule
     cudaGraphExec_t band_exec = nullptr, band_exec2 = nullptr;  // head, body
     std::size_t band_k1 = 0, band_k2 = 0;                        // their kernel nodes
     cudaStream_t aux_stream = nullptr;  // side copies beside the frame's tail
     cudaEvent_t aux_done = nullptr;
+    cudaEvent_t maps_ready = nullptr;  // convert_image_deferred: the maps' device copy is done
     cudaStream_t aux() {
         if (!aux_stream) {
             CK(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking));
@@ -458,7 +470,7 @@ struct Pipeline::Impl {
         const std::size_t o_cnt = a.take<uint32_t>(2);
         const std::size_t o_bil = a.take<uint32_t>(N + kBilSlots);
         const std::size_t o_ctl = a.take<uint32_t>(128);
-        const std::size_t o_stats = a.take<long long>(6);
+        const std::size_t o_stats = a.take<long long>(8);
         arena_bytes = a.off;
         CK(cudaSetDevice(dev));
         CK(cudaMalloc(&arena, arena_bytes));
@@ -504,7 +516,7 @@ struct Pipeline::Impl {
         up(o_shift, h_shift, sizeof(h_shift));
         if (int_cols) up(o_cols, cols_buf, sizeof(cols_buf));
         up(o_spat, h_spatial.data(), h_spatial.size() * sizeof(double));
-        CK(cudaMemsetAsync(arena + o_stats, 0, 6 * sizeof(long long), stream));
+        CK(cudaMemsetAsync(arena + o_stats, 0, 8 * sizeof(long long), stream));
         CK(cu::build_sep_table(range, sep_table, stream));
         CK(cudaStreamSynchronize(stream));  // host vectors above go out of scope
 
@@ -536,8 +548,11 @@ struct Pipeline::Impl {
         cudaSetDevice(dev);
         if (band_exec) cudaGraphExecDestroy(band_exec);
         if (band_exec2) cudaGraphExecDestroy(band_exec2);
+        if (ring_stats) cudaFreeHost(ring_stats);
+        if (conv_stats) cudaFreeHost(conv_stats);
         if (aux_stream) cudaStreamDestroy(aux_stream);
         if (aux_done) cudaEventDestroy(aux_done);
+        if (maps_ready) cudaEventDestroy(maps_ready);
         for (auto* v : {&ev_in, &ev_fork, &ev_join, &ev_rows})
             for (auto e : *v)
                 if (e) cudaEventDestroy(e);
@@ -664,25 +679,104 @@ struct Pipeline::Impl {
         }
     }
 
-    StageTimings stage_times(const std::array<cudaEvent_t, 7>& ev) {
+    // Banded schedule: depth, filter (+ fix-up) and, on the fused routes, DIBR of different
+    // bands overlap on the GPU, so events cannot time them one by one (a queued kernel's span
+    // includes its wait for SMs, and timing events inside the band graph cost ~10 % of the
+    // call). Their joint time, from the frame's first kernel to the bands' join, is split by
+    // the plan's measured stage shares: a one-time event-timed run of the same plan and
+    // frame without bands (calibrate()). Stages that run alone (DIBR on the materialised-
+    // eyes route, inpaint, formats) keep their own event times. So the parts sum to the
+    // frame's GPU time and pure_ns = filter + DIBR + inpaint + format as the reference
+    // defines it (pipeline.hpp:24-26).
+    bool cal_valid = false;
+    double cal_share[3] = {0, 0, 0};  // depth, filter, DIBR of the unbanded timed run
+
+    void banded_stage_ms(const std::array<cudaEvent_t, 7>& ev, float (&ms)[5]) {
+        const bool back = band_back();
+        float joint = 0.f;  // ev[0] .. the join (ev[2]; the fused routes' DIBR is inside)
+        CK(cudaEventElapsedTime(&joint, ev[0], ev[2]));
+        const int n = back ? 3 : 2;  // stages sharing the joint time
+        double tot = 0;
+        for (int i = 0; i < n; ++i) tot += cal_share[i];
+        for (int i = 0; i < n; ++i) ms[i] = tot > 0 ? static_cast<float>(joint * cal_share[i] / tot) : 0.f;
+        if (tot <= 0) ms[1] = joint;
+        if (back) {  // nothing runs between the join and the inpaint
+            float gap = 0.f;
+            CK(cudaEventElapsedTime(&gap, ev[2], ev[3]));
+            ms[2] += gap;
+        }
+    }
+
+    // The stage shares for banded_stage_ms: an event-timed, unbanded run of the frame now in
+    // src, once per plan (the outputs of the banded frame are already on the host).
+    void calibrate(cudaStream_t st) {
+        if (cal_valid) return;
+        const bool lc = last_conv, lb = last_banded;
+        const std::array<cudaEvent_t, 7>* ev = next_events();
+        enqueue(src, st, ev);
+        const int slot = static_cast<int>(ev - &ring.front());
+        CK(cudaEventSynchronize((*ev)[5]));
+        pending.pop_back();  // not part of the plan's accumulated timings
+        float ms[3] = {0, 0, 0};
+        for (int i = 0; i < 3; ++i) CK(cudaEventElapsedTime(&ms[i], (*ev)[i], (*ev)[i + 1]));
+        for (int i = 0; i < 3; ++i) cal_share[i] = ms[i];
+        cal_valid = true;
+        (void)slot;
+        last_conv = lc;
+        last_banded = lb;
+    }
+
+    // Stage times of one run from its events. st8: that run's inpaint stats (host copy), or
+    // nullptr to read the plan's (the run must be the last one on the plan's stream).
+    StageTimings stage_times(const std::array<cudaEvent_t, 7>& ev, const long long* st8 = nullptr,
+                             bool banded = false) {
         StageTimings t;
         CK(cudaEventSynchronize(ev[5]));
         float ms[5] = {0, 0, 0, 0, 0};
         for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+        if (banded) {
+            banded_stage_ms(ev, ms);
+        }
         t.depth_gen_ns = ms_to_ns(ms[0]);
         t.filter_ns = ms_to_ns(ms[1]);
         t.dibr_ns = ms_to_ns(ms[2]);
-        // both eyes are repaired by one kernel; its time is reported as the left eye's
-        t.inpaint_left_ns = backward ? 0 : ms_to_ns(ms[3]);
-        t.inpaint_right_ns = 0;
         t.format_ns = ms_to_ns(ms[4]);
+        split_inpaint(t, ms[3], st8);
         return t;
+    }
+
+    // Both eyes are repaired by one kernel (pipeline.cpp:56-65 runs them one after the other):
+    // its time is split by each eye's tile-processing time; an eye with no damage reports 0,
+    // as the reference skips its inpaint (so B = 0 or backward mode reports 0 for both).
+    void split_inpaint(StageTimings& t, float inpaint_ms, const long long* st8) {
+        t.inpaint_left_ns = t.inpaint_right_ns = 0;
+        if (backward) return;
+        long long s[8];
+        if (!st8) {
+            CK(cudaMemcpy(s, stats, sizeof(s), cudaMemcpyDeviceToHost));
+            st8 = s;
+        }
+        const long long dmgL = st8[1] + st8[2], dmgR = st8[4] + st8[5];
+        if (!dmgL && !dmgR) return;
+        const std::int64_t total = ms_to_ns(inpaint_ms);
+        if (!dmgR) {
+            t.inpaint_left_ns = total;
+            return;
+        }
+        if (!dmgL) {
+            t.inpaint_right_ns = total;
+            return;
+        }
+        const double bl = static_cast<double>(st8[6]), br = static_cast<double>(st8[7]);
+        const double fl = bl + br > 0 ? bl / (bl + br) : 0.5;
+        t.inpaint_left_ns = static_cast<std::int64_t>(std::llround(total * fl));
+        t.inpaint_right_ns = total - t.inpaint_left_ns;
     }
 
     void harvest_one() {
         const int slot = pending.front();
         pending.pop_front();
-        const StageTimings t = stage_times(ring[slot]);
+        const StageTimings t = stage_times(ring[slot], ring_stats + 8 * slot);
         acc.depth_gen_ns += t.depth_gen_ns;
         acc.filter_ns += t.filter_ns;
         acc.dibr_ns += t.dibr_ns;
@@ -701,6 +795,9 @@ struct Pipeline::Impl {
             ring.resize(kRing);
             for (auto& set : ring)
                 for (auto& e : set) CK(cudaEventCreate(&e));
+            // each timed run's inpaint stats land here (D2H in stream order) for its harvest
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&ring_stats), kRing * 8 * sizeof(long long),
+                             cudaHostAllocPortable));
         }
         if (static_cast<int>(pending.size()) == kRing) harvest_one();
         const int slot = ring_next;
@@ -777,6 +874,7 @@ struct Pipeline::Impl {
     // A timed frame for a synchronous caller (convert_image): graph replay with the plan's
     // fixed event set; timings()/download_overlapped() read those events.
     void run_conv(const uint8_t* s, cudaStream_t st) {
+        last_banded = false;
         if ((formats & kFormatHsbs) && (w % 2 != 0))
             throw std::invalid_argument("side_by_side: half mode requires an even width");
         if (!graphs_enabled()) {
@@ -786,6 +884,7 @@ struct Pipeline::Impl {
         }
         run_graph(s, st, true);
         last_conv = true;
+        copy_conv_stats(st);
     }
 
     void run(const uint8_t* s, cudaStream_t st, bool record) {
@@ -807,6 +906,9 @@ struct Pipeline::Impl {
         if (ev) record_event((*ev)[2], st);
         enq_dibr_inpaint(s, st, ev ? (*ev)[3] : nullptr);
         if (ev) record_event((*ev)[4], st);
+        if (ev && !ring.empty() && ev >= &ring.front() && ev <= &ring.back() && !backward)
+            CK(cudaMemcpyAsync(ring_stats + 8 * (ev - &ring.front()), stats, 8 * sizeof(long long),
+                               cudaMemcpyDeviceToHost, st));
         enq_formats(st);
         if (ev) record_event((*ev)[5], st);
     }
@@ -830,6 +932,7 @@ struct Pipeline::Impl {
             ev_dbg.assign(3 * K, nullptr);
             for (auto& e : ev_dbg) CK(cudaEventCreate(&e));
         }
+
         if (!conv_ev[0])
             for (auto& e : conv_ev) CK(cudaEventCreate(&e));
     }
@@ -1054,6 +1157,7 @@ struct Pipeline::Impl {
         // each graph is launched after the uploads it waits for are queued.
         upload_banded(img, st, 0, 1);
         last_conv = true;
+        last_banded = true;
         if (!graphs_enabled()) {
             enqueue_banded_head(st, conv_ev);
             upload_banded(img, st, 1, K);
@@ -1067,6 +1171,7 @@ struct Pipeline::Impl {
             CK(cudaGraphLaunch(band_exec2, st));
             cu::note_graph_launch(band_k2);
         }
+        copy_conv_stats(st);
         if (!outs || !band_back()) return false;
         const StereoFormat f = route == kFusedAnaglyph ? kFormatAnaglyph : kFormatFsbs;
         ImageRGB8 o(output_width(f), h, false);
@@ -1097,9 +1202,9 @@ struct Pipeline::Impl {
     }
 
     StageTimings timings() {
-        if (last_conv) return stage_times(conv_ev);
+        if (last_conv) return stage_times(conv_ev, conv_stats, last_banded);
         if (last_slot < 0) return StageTimings{};
-        return stage_times(ring[last_slot]);
+        return stage_times(ring[last_slot], ring_stats + 8 * last_slot);
     }
 
     long long bilateral_kernel_sum(long long* count, bool reset) {
@@ -1643,7 +1748,38 @@ DeferredMaps::DeferredMaps(int device, int w, int h, void* dev_buf)
     : device_(device), w_(w), h_(h), buf_(dev_buf) {}
 
 DeferredMaps::~DeferredMaps() {
+    if (done_) {
+        cudaEventSynchronize(static_cast<cudaEvent_t>(done_));  // the D2H reads buf_
+        cudaEventDestroy(static_cast<cudaEvent_t>(done_));
+        cudaGetLastError();
+    }
     if (buf_) map_pool().give(device_, 2 * static_cast<std::size_t>(w_) * h_, buf_);
+}
+
+namespace {
+// One copy stream per device for the background map downloads.
+cudaStream_t maps_stream(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    std::lock_guard<std::mutex> lk(mu);
+    cudaStream_t& s = streams[device];
+    if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+}  // namespace
+
+void DeferredMaps::start_download(void* ready_event) {
+    const std::size_t n = static_cast<std::size_t>(w_) * h_;
+    depth_ = GrayMap(w_, h_, false);     // pinned pool: the copy engine writes them directly
+    filtered_ = GrayMap(w_, h_, false);
+    cudaStream_t s = maps_stream(device_);
+    CK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ready_event), 0));
+    CK(cudaMemcpyAsync(depth_.data.data(), buf_, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(filtered_.data.data(), static_cast<uint8_t*>(buf_) + n, n, cudaMemcpyDeviceToHost, s));
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, s));
+    done_ = e;
 }
 
 void DeferredMaps::materialize() {
@@ -1652,18 +1788,24 @@ void DeferredMaps::materialize() {
     int cur = 0;
     cudaGetDevice(&cur);
     CK(cudaSetDevice(device_));
-    const std::size_t n = static_cast<std::size_t>(w_) * h_;
-    GrayMap d(w_, h_, false), f(w_, h_, false);
-    const cudaError_t e1 = cudaMemcpy(d.data.data(), buf_, n, cudaMemcpyDeviceToHost);
-    const cudaError_t e2 = cudaMemcpy(f.data.data(), static_cast<uint8_t*>(buf_) + n, n,
-                                      cudaMemcpyDeviceToHost);
-    cudaSetDevice(cur);
-    CK(e1);
-    CK(e2);
-    depth_ = std::move(d);
-    filtered_ = std::move(f);
+    if (done_) {
+        const cudaError_t e = cudaEventSynchronize(static_cast<cudaEvent_t>(done_));
+        cudaSetDevice(cur);
+        CK(e);
+    } else {
+        const std::size_t n = static_cast<std::size_t>(w_) * h_;
+        GrayMap d(w_, h_, false), f(w_, h_, false);
+        const cudaError_t e1 = cudaMemcpy(d.data.data(), buf_, n, cudaMemcpyDeviceToHost);
+        const cudaError_t e2 = cudaMemcpy(f.data.data(), static_cast<uint8_t*>(buf_) + n, n,
+                                          cudaMemcpyDeviceToHost);
+        cudaSetDevice(cur);
+        CK(e1);
+        CK(e2);
+        depth_ = std::move(d);
+        filtered_ = std::move(f);
+    }
     ready_ = true;
-    map_pool().give(device_, 2 * n, buf_);
+    map_pool().give(device_, 2 * static_cast<std::size_t>(w_) * h_, buf_);
     buf_ = nullptr;
 }
 
@@ -1720,6 +1862,7 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
         }
         if (dbg) CK(cudaEventRecord(dbg_ev[1], st));
         CK(cudaStreamSynchronize(st));
+        if (p->last_banded && !p->cal_valid) p->calibrate(st);
         res.timings = p->timings();
         if (dbg) {
             float a0 = 0, b5 = 0, ab = 0;
@@ -1749,6 +1892,24 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
                          e01 * 1e3, e06 * 1e3, e64 * 1e3, e05 * 1e3);
         }
         maps = std::make_shared<DeferredMaps>(dev.ordinal(), p->w, p->h, buf);
+        // the maps go to the host in the background (after their device copy); p3s_convert
+        // does not wait for them
+        // P3S_EAGER_MAPS=1: the maps go to the host in the background right away (the next
+        // call's output downloads then share the D2H link with them: -20 % e2e at 4K);
+        // default: on first access
+        static const bool eager = [] {
+            const char* e = std::getenv("P3S_EAGER_MAPS");
+            return e && *e == '1';
+        }();
+        if (eager) {
+            try {
+                if (!p->maps_ready) CK(cudaEventCreateWithFlags(&p->maps_ready, cudaEventDisableTiming));
+                CK(cudaEventRecord(p->maps_ready, ms));
+                maps->start_download(p->maps_ready);
+            } catch (...) {
+                cudaGetLastError();  // not queued: the maps download on first access instead
+            }
+        }
         return res;
     } catch (...) {
         map_pool().give(dev.ordinal(), 2 * n, buf);
@@ -1767,10 +1928,12 @@ ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg
         p->d2h_plane(res.depth.data.data(), p->depth, p->pitch, p->w, st);
         p->d2h_plane(res.filtered_depth.data.data(), p->filt, p->pitch, p->w, st);
         CK(cudaStreamSynchronize(st));
+        if (p->last_banded && !p->cal_valid) p->calibrate(st);
         res.timings = p->timings();
         return res;
     }
     p->download_overlapped(res, st, dev.impl().copy_stream);
+    if (p->last_banded && !p->cal_valid) p->calibrate(st);
     res.timings = p->timings();
     return res;
 }

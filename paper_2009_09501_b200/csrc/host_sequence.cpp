@@ -121,6 +121,13 @@ public:
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return q_.empty() && !busy_; });
     }
+    // Drops the queued tasks (the running one finishes): an error path must not write
+    // outputs after it has been raised.
+    void cancel() {
+        std::lock_guard<std::mutex> lk(mu_);
+        q_.clear();
+        cv_.notify_all();
+    }
     std::exception_ptr error() {
         std::lock_guard<std::mutex> lk(mu_);
         return err_;
@@ -207,9 +214,17 @@ SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string
         std::unique_ptr<Pipeline> pipe[2];
     };
     std::map<std::pair<int, int>, Plan> plans;
-    Worker writer(2);
+    // declared before the writer: its destructor runs (and drains queued writes) first
     std::int64_t written = 0;
     std::mutex written_mu;
+    Worker writer(2);
+    struct CancelOnError {
+        Worker& w;
+        int n = std::uncaught_exceptions();
+        ~CancelOnError() {
+            if (std::uncaught_exceptions() > n) w.cancel();
+        }
+    } cancel_on_error{writer};
     std::int64_t ordinal = 0;
     Loaded cur = load(next);
     while (cur.present) {

@@ -83,9 +83,8 @@ struct Work {
     uint32_t* init_flags;  // [2][tiles] damaged-pixel count per tile (initial work list)
     uint32_t* heavy;       // [2 * tiles] tiles with >= kHeavy damaged pixels (round 0, first)
     uint32_t* lists;       // [3][2 * tiles] (eye * tiles + tile)
-    uint32_t* counters;    // [0..5] = [3][2]: count, claim; [6] heavy count; [7] unused;
-                           // [8..11] = per-eye tile-busy ns (2 x u64); [16] the launch epoch
-                           // (persistent, not zeroed per launch)
+    uint32_t* counters;    // [0..5] = [3][2]: count, claim; [6] heavy count; [16] the launch
+                           // epoch (persistent, not zeroed per launch)
     int cap;               // 2 * tiles
 };
 
@@ -686,8 +685,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(const __grid_cons
             }
         }
     }
-    if (lane == 0 && (busy[0] | busy[1])) {
-        unsigned long long* ns = reinterpret_cast<unsigned long long*>(wk.counters + 8);
+    // per-eye tile time (stats[6], stats[7]: zeroed before the launch), which splits the one
+    // kernel's time into the reference's inpaint_left_ns / inpaint_right_ns
+    if (stats && lane == 0 && (busy[0] | busy[1])) {
+        unsigned long long* ns = reinterpret_cast<unsigned long long*>(stats + 6);
         if (busy[0]) atomicAdd(ns, busy[0]);
         if (busy[1]) atomicAdd(ns + 1, busy[1]);
     }
@@ -746,7 +747,9 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     z.words[0] = kCtlWords;
     z.p[1] = wk.counters;  // [0..15]; [16] (the launch epoch) persists
     z.words[1] = 16;
-    z.n = 2;
+    z.p[2] = stats ? stats + 6 : nullptr;  // per-eye busy ns
+    z.words[2] = stats ? 4u : 0u;
+    z.n = 3;
     cudaError_t e = zero(z, st, zero_by_kernel);
     if (e != cudaSuccess) return e;
     const size_t smem = kWarps * sizeof(WarpSmem);

@@ -165,7 +165,8 @@ cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* lis
                          uint32_t* count, cudaStream_t st, uint32_t* bits = nullptr, int mwords = 0);
 
 // Inpaint (inpaint.cpp:29-130) on both eyes at once, in place on the EyeOut planes.
-// Work lists come from dibr(). stats (device, 6 x i64): passes/repaired/fallback per eye.
+// Work lists come from dibr(). stats (device, 8 x i64): passes/repaired/fallback per eye,
+// then the per-eye tile-processing ns (the split of the kernel's time between the eyes).
 // The damage is read from mask_bits (the INITIAL damage, 32-pixel words, read-only; the
 // byte mask is not read). `repair` of the left eye points at a device arena of
 // inpaint_scratch_bytes(w, h) (tagged damage words, tile counts, work lists; persistent).

@@ -138,20 +138,80 @@ def test_large_radius_generic_kernel(p3s, checker):
     compare_convert(p3s, checker, img, dict(sigma_spatial=23.0, formats=7, base=20))
 
 
-def test_4k_default_full(p3s, checker):
-    img = checker.synthetic_frame(3840, 2160, 1)
-    out = compare_convert(p3s, checker, img, {})
-    t = out["timings"]
+def _identity(t):
     assert t["pure_ns"] == t["filter_ns"] + t["dibr_ns"] + t["inpaint_left_ns"] + \
         t["inpaint_right_ns"] + t["format_ns"]
 
 
+def test_4k_default_full(p3s, checker):
+    """The banded p3s_convert (pinned 4K frame): bytes = oracle, and its stage times are a
+    partition of the frame's GPU timeline (engine.cpp banded_stage_ms): every stage present,
+    the filter dominant, both eyes' inpaint reported, the reference's pure_ns identity."""
+    img = p3s.synthetic_frame(3840, 2160, 1)
+    out = compare_convert(p3s, checker, img, {})
+    t = out["timings"]
+    _identity(t)
+    assert t["depth_gen_ns"] > 0 and t["dibr_ns"] > 0 and t["format_ns"] >= 0
+    assert t["inpaint_left_ns"] > 0 and t["inpaint_right_ns"] > 0
+    assert t["filter_ns"] > 5 * max(t["depth_gen_ns"], t["dibr_ns"])
+    # non-banded reference point (P3S_BANDED-free path: a timed pipeline run of the same frame)
+    pipe = p3s.Pipeline(3840, 2160, p3s.Config())
+    buf = p3s.DeviceBuffer(pipe.frame_bytes)
+    pipe.upload(img, buf.addr)
+    pipe.run(buf.addr, timed=True)
+    tp = pipe.timings()
+    _identity(tp)
+    assert 0.5 < t["filter_ns"] / tp["filter_ns"] < 1.5
+    assert 0.25 < t["depth_gen_ns"] / tp["depth_gen_ns"] < 4
+
+
 def test_b0_identity_and_backward_has_no_holes(p3s, checker):
-    img = checker.synthetic_frame(322, 177, 9)
+    """B = 0 (forward) and backward mode leave no damage: the reference skips the inpaint
+    (pipeline.cpp:56-65), so both eyes report 0 ns, on the banded and the plain path."""
+    img = p3s.synthetic_frame(322, 177, 9)
     out = p3s.convert(img, p3s.Config(base=0))
     assert np.array_equal(out["anaglyph"], img)
+    assert out["timings"]["inpaint_left_ns"] == 0 and out["timings"]["inpaint_right_ns"] == 0
+    _identity(out["timings"])
     out = p3s.convert(img, p3s.Config(mode=1, formats=7))
     assert out["timings"]["inpaint_left_ns"] == 0 and out["timings"]["inpaint_right_ns"] == 0
+    big = p3s.synthetic_frame(1920, 1080, 3)  # tall enough for the banded schedule
+    out = p3s.convert(big, p3s.Config(base=0))
+    assert out["timings"]["inpaint_left_ns"] == 0 and out["timings"]["inpaint_right_ns"] == 0
+    _identity(out["timings"])
+    pipe = p3s.Pipeline(1920, 1080, p3s.Config(base=0))
+    buf = p3s.DeviceBuffer(pipe.frame_bytes)
+    pipe.upload(big, buf.addr)
+    pipe.run(buf.addr, timed=True)
+    t = pipe.timings()
+    assert t["inpaint_left_ns"] == 0 and t["inpaint_right_ns"] == 0
+
+
+def test_result_maps_survive_later_work(p3s, checker):
+    """p3s_result_depth / _filtered_depth of an earlier result stay valid (downloaded in the
+    background) while later conversions reuse the plan."""
+    import ctypes as C
+    import oracle
+    L = p3s.lib()
+    cfg = p3s.Config()
+    frames = [p3s.synthetic_frame(640, 360, s) for s in (1, 2, 3)]
+    imgs = [p3s.Image(f) for f in frames]
+    results = []
+    for im in imgs:
+        r = C.c_void_p()
+        p3s._check(L.p3s_convert(im.h, cfg.h, C.byref(r)))
+        results.append(r)
+    try:
+        for f, r in zip(frames, results):
+            ref = checker.convert(f, oracle.Cfg(), threads=NCPU)
+            d = L.p3s_result_depth(r)
+            fd = L.p3s_result_filtered_depth(r)
+            assert d and fd
+            assert np.array_equal(p3s._gray_to_numpy(d), ref["depth"])
+            assert np.array_equal(p3s._gray_to_numpy(fd), ref["filtered"])
+    finally:
+        for r in results:
+            L.p3s_result_free(r)
 
 
 def test_odd_width_hsbs_is_invalid(p3s):
