@@ -3,6 +3,7 @@ itself under torchrun with N ranks (rendezvous on 127.0.0.1), and a launch whose
 count differs from --gpus fails instead of measuring fewer GPUs."""
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -21,7 +22,9 @@ def test_gpus_n_relaunches_n_ranks():
     r = subprocess.run([sys.executable, BENCH, "--gpus", "2", "--launch-selftest"],
                        capture_output=True, text=True, timeout=300, env=_env())
     assert r.returncode == 0, r.stderr[-2000:]
-    ranks = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    # both ranks share torchrun's stdout pipe: pick the records out by pattern, since a
+    # line of one rank may be split by the other's
+    ranks = [json.loads(m) for m in re.findall(r'\{"rank": \d+, "world": \d+, "local": \d+\}', r.stdout)]
     assert sorted(d["rank"] for d in ranks) == [0, 1]
     assert all(d["world"] == 2 for d in ranks)
 
