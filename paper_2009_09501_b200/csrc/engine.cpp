@@ -598,12 +598,29 @@ struct Pipeline::Impl {
     }
 
     // ---- stage launchers ----
+    // Depth stage of depth tile rows [d0, d1) / block rows [b0, b1) / image rows [u0, u1):
+    // the fused front (luma + block values, 16-pixel blocks) or front + block_values, then
+    // the upsample. sums must be zeroed for the unfused front.
+    bool depth_fused() const {
+        static const bool off = std::getenv("P3S_DEPTH_UNFUSED") != nullptr;
+        return !off && cu::depth_fused_ok(gm, dt.block);
+    }
+    void enq_depth_rows(const uint8_t* s, cudaStream_t st, int d0, int d1, int b0, int b1, int u0,
+                        int u1) {
+        if (depth_fused()) {
+            CK(cu::depth_front_fused(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, dt,
+                                     values, st, d0, d1));
+        } else {
+            CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
+                               dt.block, dt.bx, st, d0, d1));
+            CK(cu::block_values(sums, gm, dt, values, st, b0, b1));
+        }
+        CK(cu::upsample(values, gm, dt, depth, st, u0, u1));
+    }
+
     void enq_depth(const uint8_t* s, cudaStream_t st) {
-        CK(cu::zero(zr({{sums, 2u * dt.bx * dt.by}}), st));
-        CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
-                           dt.block, dt.bx, st));
-        CK(cu::block_values(sums, gm, dt, values, st));
-        CK(cu::upsample(values, gm, dt, depth, st));
+        if (!depth_fused()) CK(cu::zero(zr({{sums, 2u * dt.bx * dt.by}}), st));
+        enq_depth_rows(s, st, 0, -1, 0, -1, 0, -1);
     }
 
     void enq_bilateral(const uint8_t* dmap, const uint8_t* guide, uint8_t* out, double* raw,
@@ -1008,14 +1025,11 @@ struct Pipeline::Impl {
         const int K = static_cast<int>(bands.size());
         wait_event_any(st, ev_in[0]);
         record_event(ev[0], st);
-        CK(cu::zero(zr({{sums, 2u * dt.bx * dt.by},
+        CK(cu::zero(zr({{sums, depth_fused() ? 0u : 2u * dt.bx * dt.by},
                         {bil_count, 2u * K},
                         {counts, backward ? 0u : 2u}}), st, true));
         const Band& b = bands[0];
-        CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
-                           dt.block, dt.bx, st, 0, b.dtile));
-        CK(cu::block_values(sums, gm, dt, values, st, 0, b.brow));
-        CK(cu::upsample(values, gm, dt, depth, st, 0, b.urow));
+        enq_depth_rows(s, st, 0, b.dtile, 0, b.brow, 0, b.urow);
         record_event(ev[1], st);
     }
 
@@ -1036,10 +1050,7 @@ struct Pipeline::Impl {
             cudaStream_t ds = depth_stream, bs = band_streams[k];
             if (k > 0) {
                 wait_event_any(ds, ev_in[k]);
-                CK(cu::depth_front(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, sums,
-                                   dt.block, dt.bx, ds, prev.dtile, b.dtile));
-                CK(cu::block_values(sums, gm, dt, values, ds, prev.brow, b.brow));
-                CK(cu::upsample(values, gm, dt, depth, ds, prev.urow, b.urow));
+                enq_depth_rows(s, ds, prev.dtile, b.dtile, prev.brow, b.brow, prev.urow, b.urow);
             }
             CK(cudaEventRecord(ev_fork[k], ds));
             CK(cudaStreamWaitEvent(bs, ev_fork[k], 0));

@@ -9,6 +9,8 @@
 // Integer arithmetic only in K1, so it is exact by construction. block_values/upsample
 // reproduce the reference's double expressions with explicit round-to-nearest intrinsics
 // (no FMA contraction regardless of compiler flags).
+#include <cstdlib>
+
 #include "p3s_cu.h"
 
 namespace p3s {
@@ -265,6 +267,216 @@ __global__ void __launch_bounds__(kUpThreads) k_upsample(const double* __restric
     }
 }
 
+// ---- fused depth front for 16-pixel blocks (the default depth_block) ----------------------
+// K1 with the block values folded in: a CTA of 256 threads covers 1024 columns x one block
+// row (16 image rows), i.e. 64 blocks of 16 x 16; four adjacent lanes own one block (four
+// output rows each), reduce its Sobel sum with two shuffles and the first of them writes the
+// block VALUE (depth.cpp:55-71) itself — no sums buffer, no atomics, no block_values launch.
+//  phase 1  R, G, B rows y0-1 .. y0+16 (edge-clamped) with 16-byte loads (every thread issues
+//           all of its rows' loads before converting), luma for 16 pixels at a time in 16-bit
+//           lanes (luma4), into a shared 18-row luma tile (+ the two halo columns) and, for the
+//           16 block rows, to the luma plane (16-byte stores);
+//  phase 2  the 3x3 Sobel magnitude of 16 pixels per row in 16-bit lanes (2 pixels per 32-bit
+//           word). With the window rows t (y-1), m (y), b (y+1):
+//               gx + gy = 2 (A+ - A-),  A+ = m(x+1) + b(x+1) + b(x),  A- = t(x-1) + m(x-1) + t(x)
+//               gx - gy = 2 (B+ - B-),  B+ = t(x+1) + m(x+1) + t(x),  B- = b(x-1) + m(x-1) + b(x)
+//           and |gx| + |gy| = max(|gx + gy|, |gx - gy|), so the reference's
+//           min(255, (|gx| + |gy|) / 4) = min(510, max(|A+ - A-|, |B+ - B-|)) >> 1 exactly
+//           (integers, depth.cpp:34-37). |a - b| per lane = max - min (VIMNMX.U16x2).
+// Requires block == 16, w % 16 == 0 and a 16-byte aligned pitch (depth_fused_ok).
+constexpr int kFT = 256;           // threads per CTA
+constexpr int kFW = 1024;          // columns per CTA (64 blocks)
+constexpr int kFL = 16;            // smem column of image column x0 (halo at kFL - 1)
+constexpr int kFS = kFL + kFW + 16;  // smem row stride
+
+__device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+__device__ __forceinline__ uint32_t absdiff2(uint32_t a, uint32_t b) { return vmax2(a, b) - vmin2(a, b); }
+
+// One smem luma row as 16-bit pairs: P[j] = (c2j, c2j+1), S[j] = (c2j-1, c2j) for j = 0..8
+// (S[8] = (c15, c16)); row[-1] / row[16] are the neighbouring columns.
+struct PairRow {
+    uint32_t P[8], S[9];
+};
+__device__ __forceinline__ void load_pair_row(const uint8_t* row, PairRow& pr) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row);
+    const uint32_t hl = static_cast<uint32_t>(row[-1]) << 16, hr = row[16];
+    const uint32_t L[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pr.P[j] = __byte_perm(L[j >> 1], 0u, (j & 1) ? 0x4342 : 0x4140);
+    pr.S[0] = __byte_perm(hl, pr.P[0], 0x5432);
+#pragma unroll
+    for (int j = 1; j < 8; ++j) pr.S[j] = __byte_perm(pr.P[j - 1], pr.P[j], 0x5432);
+    pr.S[8] = __byte_perm(pr.P[7], hr, 0x5432);
+}
+
+__global__ void __launch_bounds__(kFT) k_depth_fused(const uint8_t* __restrict__ R,
+                                                     const uint8_t* __restrict__ G,
+                                                     const uint8_t* __restrict__ B, int pitch,
+                                                     int w, int h, uint8_t* __restrict__ luma,
+                                                     double* __restrict__ values, int bx_total,
+                                                     double alpha255, double beta,
+                                                     double row_denom, int tile_row0) {
+    __shared__ __align__(16) uint8_t s_l[kTH + 2][kFS];
+    const int x0 = blockIdx.x * kFW;
+    const int y0 = (tile_row0 + blockIdx.y) * kTH;
+    const int t = threadIdx.x;
+    const int ncols = min(kFW, w - x0);
+
+    // ---- phase 1: luma tile (rows y0-1 .. y0+16, clamped); thread = chunk t & 63, rows
+    // (t >> 6) + 4k ----
+    {
+        const int c0 = 16 * (t & 63), rq = t >> 6;
+        if (c0 < ncols) {
+            const size_t col = static_cast<size_t>(x0 + c0);
+            uint4 vr[5], vg[5], vb[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const int r = rq + 4 * k;
+                if (r < kTH + 2) {
+                    const int gy = clampi(y0 - 1 + r, h - 1);
+                    const size_t off = static_cast<size_t>(gy) * pitch + col;
+                    vr[k] = __ldg(reinterpret_cast<const uint4*>(R + off));
+                    vg[k] = __ldg(reinterpret_cast<const uint4*>(G + off));
+                    vb[k] = __ldg(reinterpret_cast<const uint4*>(B + off));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const int r = rq + 4 * k;
+                if (r < kTH + 2) {
+                    const uint4 yv = make_uint4(luma4(vr[k].x, vg[k].x, vb[k].x), luma4(vr[k].y, vg[k].y, vb[k].y),
+                                                luma4(vr[k].z, vg[k].z, vb[k].z), luma4(vr[k].w, vg[k].w, vb[k].w));
+                    *reinterpret_cast<uint4*>(&s_l[r][kFL + c0]) = yv;
+                    const int oy = y0 - 1 + r;
+                    if (r >= 1 && r <= kTH && oy < h)
+                        *reinterpret_cast<uint4*>(luma + static_cast<size_t>(oy) * pitch + col) = yv;
+                }
+            }
+        }
+        // halo columns x0-1 and x0+ncols (edge-clamped), 18 rows each
+        if (t >= kFT - 2 * (kTH + 2)) {
+            const int i = t - (kFT - 2 * (kTH + 2));
+            const int r = i >> 1, side = i & 1;
+            const int gy = clampi(y0 - 1 + r, h - 1);
+            const int gx = side ? min(x0 + ncols, w - 1) : max(x0 - 1, 0);
+            const size_t off = static_cast<size_t>(gy) * pitch + gx;
+            s_l[r][side ? kFL + ncols : kFL - 1] = luma_px(R[off], G[off], B[off]);
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 2: lanes 4b..4b+3 own block b; lane quarter q sums rows 4q..4q+3 ----
+    const int blk = t >> 2, q = t & 3;
+    const int c0 = 16 * blk;
+    const int rows = min(kTH, h - y0);
+    uint32_t acc = 0;
+    if (c0 < ncols) {
+        const int i0 = 4 * q, i1 = min(4 * q + 4, rows);
+        PairRow top, mid, bot;
+        load_pair_row(&s_l[i0][kFL + c0], top);
+        load_pair_row(&s_l[i0 + 1][kFL + c0], mid);
+        for (int i = i0; i < i1; ++i) {
+            load_pair_row(&s_l[i + 2][kFL + c0], bot);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t ap = mid.S[j + 1] + bot.S[j + 1] + bot.P[j];
+                const uint32_t an = top.S[j] + mid.S[j] + top.P[j];
+                const uint32_t bp = top.S[j + 1] + mid.S[j + 1] + top.P[j];
+                const uint32_t bn = bot.S[j] + mid.S[j] + bot.P[j];
+                const uint32_t m = vmin2(vmax2(absdiff2(ap, an), absdiff2(bp, bn)), 0x01FE01FEu);
+                acc += (m >> 1) & 0x00FF00FFu;  // <= 4 rows x 8 words x 255 per lane
+            }
+            top = mid;
+            mid = bot;
+        }
+    }
+    unsigned long long sum = (acc & 0xFFFFu) + (acc >> 16);
+    sum += __shfl_xor_sync(0xFFFFFFFFu, sum, 1);
+    sum += __shfl_xor_sync(0xFFFFFFFFu, sum, 2);
+    if (q == 0 && c0 < ncols) {
+        // depth.cpp:55-71 (same expression order as k_block_values)
+        const int ya = y0, yb = y0 + rows;
+        const double centre = __dadd_rn(static_cast<double>(ya), __ddiv_rn(static_cast<double>(yb - 1 - ya), 2.0));
+        const double ramp = __dmul_rn(alpha255, __ddiv_rn(centre, row_denom));
+        const double mean = __ddiv_rn(static_cast<double>(sum), static_cast<double>(rows * 16));
+        values[static_cast<size_t>(tile_row0 + blockIdx.y) * bx_total + (x0 + c0) / 16] =
+            __dadd_rn(ramp, __dmul_rn(beta, mean));
+    }
+}
+
+// ---- upsample: a CTA = 1024 columns x 16 rows, a thread = 4 columns x 16 rows ------------
+// Same arithmetic as k_upsample (depth.cpp:104-120, each double operation separately
+// rounded); the CTA's 16 row-table entries are staged in shared memory first (no global
+// load latency inside the row loop), and floor(v + 0.5) is taken on the FP64 pipe:
+// t = v + 0.5 (the reference's add), then t + 2^52 rounded toward zero holds floor(t) in its
+// low word (t in [0, 2^31)); v >= 0 since every block value and lerp weight is >= 0.
+constexpr int kU2Cols = 4, kU2Rows = 16, kU2Threads = 256;
+
+__global__ void __launch_bounds__(kU2Threads) k_upsample_rows(const double* __restrict__ values, int bx,
+                                                              const int* __restrict__ ci0,
+                                                              const int* __restrict__ ci1,
+                                                              const double* __restrict__ cf,
+                                                              const int* __restrict__ ri0,
+                                                              const int* __restrict__ ri1,
+                                                              const double* __restrict__ rf, int w,
+                                                              int pitch, uint8_t* __restrict__ depth,
+                                                              int ya, int yb) {
+    __shared__ int s_i0[kU2Rows], s_i1[kU2Rows];
+    __shared__ double s_f[kU2Rows];
+    const int y0 = ya + blockIdx.y * kU2Rows;
+    const int y1 = min(y0 + kU2Rows, yb);
+    if (threadIdx.x < y1 - y0) {
+        s_i0[threadIdx.x] = __ldg(ri0 + y0 + threadIdx.x);
+        s_i1[threadIdx.x] = __ldg(ri1 + y0 + threadIdx.x);
+        s_f[threadIdx.x] = __ldg(rf + y0 + threadIdx.x);
+    }
+    const int x0 = (blockIdx.x * kU2Threads + threadIdx.x) * kU2Cols;
+    int a[kU2Cols], b[kU2Cols];
+    double fx[kU2Cols];
+#pragma unroll
+    for (int k = 0; k < kU2Cols; ++k) {
+        const int x = min(x0 + k, w - 1);
+        a[k] = __ldg(ci0 + x);
+        b[k] = __ldg(ci1 + x);
+        fx[k] = __ldg(cf + x);
+    }
+    __syncthreads();
+    if (x0 >= w) return;
+    int cur0 = -1, cur1 = -1;
+    double top[kU2Cols], bot[kU2Cols];
+    const bool full = x0 + kU2Cols <= pitch;  // pitch % 16 == 0: 4-byte aligned, padding is scratch
+    for (int y = y0; y < y1; ++y) {
+        const int i0 = s_i0[y - y0], i1 = s_i1[y - y0];
+        if (i0 != cur0 || i1 != cur1) {
+            const double* vt = values + static_cast<size_t>(i0) * bx;
+            const double* vb = values + static_cast<size_t>(i1) * bx;
+#pragma unroll
+            for (int k = 0; k < kU2Cols; ++k) {
+                top[k] = lerp_ref(__ldg(vt + a[k]), __ldg(vt + b[k]), fx[k]);
+                bot[k] = lerp_ref(__ldg(vb + a[k]), __ldg(vb + b[k]), fx[k]);
+            }
+            cur0 = i0;
+            cur1 = i1;
+        }
+        const double fy = s_f[y - y0];
+        const double omf = __dsub_rn(1.0, fy);
+        uint32_t packed = 0;
+#pragma unroll
+        for (int k = 0; k < kU2Cols; ++k) {
+            const double v = __dadd_rn(__dmul_rn(top[k], omf), __dmul_rn(bot[k], fy));
+            const double f = __dadd_rz(__dadd_rn(v, 0.5), 4503599627370496.0);
+            packed |= min(static_cast<uint32_t>(__double2loint(f)), 255u) << (8 * k);
+        }
+        uint8_t* dst = depth + static_cast<size_t>(y) * pitch + x0;
+        if (full) {
+            *reinterpret_cast<uint32_t*>(dst) = packed;
+        } else {
+            for (int k = 0; k < kU2Cols && x0 + k < w; ++k) dst[k] = static_cast<uint8_t>(packed >> (8 * k));
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
@@ -300,6 +512,14 @@ cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_
                      cudaStream_t st, int ya, int yb) {
     if (yb < 0 || yb > gm.h) yb = gm.h;
     if (yb <= ya) return cudaSuccess;
+    if (gm.pitch % 16 == 0 && !std::getenv("P3S_UPSAMPLE4")) {
+        dim3 grid((gm.w + kU2Threads * kU2Cols - 1) / (kU2Threads * kU2Cols),
+                  (yb - ya + kU2Rows - 1) / kU2Rows);
+        note_launch(st);
+        k_upsample_rows<<<grid, kU2Threads, 0, st>>>(values, t.bx, t.col_i0, t.col_i1, t.col_f, t.row_i0,
+                                                 t.row_i1, t.row_f, gm.w, gm.pitch, depth, ya, yb);
+        return cudaGetLastError();
+    }
     dim3 grid((gm.w + kUpThreads * kUpCols - 1) / (kUpThreads * kUpCols),
               (yb - ya + kUpRows - 1) / kUpRows);
     note_launch(st);
@@ -309,6 +529,23 @@ cudaError_t upsample(const double* values, Geom gm, const DepthTables& t, uint8_
 }
 
 int depth_tile_rows() { return kTH; }
+
+bool depth_fused_ok(Geom gm, int block) {
+    return block == kTH && gm.w % 16 == 0 && gm.pitch % 16 == 0 && gm.w >= 16;
+}
+
+cudaError_t depth_front_fused(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
+                              uint8_t* luma, const DepthTables& t, double* values, cudaStream_t st,
+                              int tile_row0, int tile_row1) {
+    const int rows = (gm.h + kTH - 1) / kTH;
+    if (tile_row1 < 0 || tile_row1 > rows) tile_row1 = rows;
+    if (tile_row1 <= tile_row0) return cudaSuccess;
+    dim3 grid((gm.w + kFW - 1) / kFW, tile_row1 - tile_row0);
+    note_launch(st);
+    k_depth_fused<<<grid, kFT, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, values, t.bx, t.alpha255,
+                                        t.beta, t.row_denom, tile_row0);
+    return cudaGetLastError();
+}
 
 }  // namespace cu
 }  // namespace p3s

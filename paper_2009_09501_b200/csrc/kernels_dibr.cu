@@ -344,13 +344,19 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
 // bytes as k_dibr_ana<false> with far fewer instructions per pixel.
 //   stage    lane-contiguous 4-pixel words of R, G, B, depth (128-byte warp requests); the
 //            source row is kept as one packed 0x00BBGGRR word per pixel, so a gather is one
-//            LDS.32 for all channels;
+//            LDS.32 for all channels; slot wpad is a zero word (unsplatted destinations);
 //   splat    lane-interleaved sources (consecutive destinations across the warp:
-//            conflict-free shared atomicMax on the packed key);
-//   resolve  each thread owns 4 consecutive destinations: one 16-byte key load per eye, two
-//            gathers per pixel, the output bytes assembled in registers and written with one
-//            4-byte store per plane (128-byte warp stores); 4-bit damage nibbles are merged
-//            into 32-bit mask words over 8-lane groups; one list atomic per warp and eye.
+//            conflict-free shared atomicMax on the packed key). Columns: the integer tables
+//            give col = x + off + (x >= X), 0 at x == z; every X < w and z lies below
+//            x_safe (the CTA's max over the 256 depths), so for x >= x_safe both eyes'
+//            columns are x + off2[d] (off2 = off + (X < w)), formed by one add on a packed
+//            pair of biased 16-bit offsets; x < x_safe (a few dozen pixels at the left edge)
+//            takes the exact general form;
+//   resolve  each thread owns 4 consecutive destinations: one 16-byte key load per eye, a
+//            branch-free gather per pixel (index = ~key & 0x3FFFFF, clamped to the zero slot),
+//            the output bytes assembled with byte permutes and written with one 4-byte store
+//            per plane (128-byte warp stores); 4-bit damage nibbles are merged into 32-bit
+//            mask words over 8-lane groups; one list atomic per warp and eye.
 // MODE 0: anaglyph planes (left R, right G/B); MODE 1: all six eye planes (HSBS / FSBS
 // routes), same z-buffer, masks and lists.
 template <int MODE>
@@ -362,15 +368,36 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                                                    EyeOut L, EyeOut Rt, int ya, int yb) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int4 s_cols[256];
+    __shared__ uint32_t s_off[256];
+    __shared__ int s_xsafe;
     const int wpad = (w + 15) & ~15;
     const int nq = wpad >> 2;  // quads
-    uint32_t* s_rgb = reinterpret_cast<uint32_t*>(smem);      // [wpad]
-    uint32_t* keyL = s_rgb + wpad;                             // [wpad]
+    uint32_t* s_rgb = reinterpret_cast<uint32_t*>(smem);      // [wpad + 4]
+    uint32_t* keyL = s_rgb + wpad + 4;                         // [wpad]
     uint32_t* keyR = keyL + wpad;                              // [wpad]
     uint8_t* s_d = reinterpret_cast<uint8_t*>(keyR + wpad);    // [wpad]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < 256; i += blockDim.x) s_cols[i] = cols_g[i];
+    if (tid == 0) s_xsafe = 0;
+    if (tid < 4) s_rgb[wpad + tid] = 0u;
+    __syncthreads();
+    for (int i = tid; i < 256; i += blockDim.x) {
+        const int4 c = cols_g[i];
+        s_cols[i] = c;
+        const int offP = static_cast<short>(c.x & 0xFFFF), XP = static_cast<int>(static_cast<unsigned>(c.x) >> 16);
+        const int offM = static_cast<short>(c.y & 0xFFFF), XM = static_cast<int>(static_cast<unsigned>(c.y) >> 16);
+        const int offP2 = offP + (XP < w ? 1 : 0), offM2 = offM + (XM < w ? 1 : 0);
+        s_off[i] = (static_cast<uint32_t>(offP2 + 0x8000) & 0xFFFFu) | (static_cast<uint32_t>(offM2 + 0x8000) << 16);
+        int xs = 0;
+        if (XP < w) xs = max(xs, XP);
+        if (XM < w) xs = max(xs, XM);
+        if (c.z >= 0) xs = max(xs, c.z + 1);
+        if (c.w >= 0) xs = max(xs, c.w + 1);
+        // the packed add must not carry between the 16-bit lanes: x + off2 + 0x8000 < 2^16
+        if (offP2 + w >= 0x8000 || offM2 + w >= 0x8000) xs = w;
+        if (xs) atomicMax(&s_xsafe, xs);
+    }
     const int nqr = (nq + 31) & ~31;
+    const uint32_t wz = static_cast<uint32_t>(wpad);
 
     for (int y = ya + static_cast<int>(blockIdx.x); y < yb; y += gridDim.x) {
         __syncthreads();
@@ -392,11 +419,20 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
             reinterpret_cast<uint4*>(keyR)[q] = make_uint4(0, 0, 0, 0);
         }
         __syncthreads();
+        const int xsafe = s_xsafe;
         for (int x = tid; x < w; x += blockDim.x) {
             const int d = s_d[x];
-            const int4 t = s_cols[d];
-            const int a = col_int(t.x, t.z, x), b = col_int(t.y, t.w, x);
             const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
+            int a, b;
+            if (x >= xsafe) {
+                const uint32_t ab = s_off[d] + static_cast<uint32_t>(x) * 0x10001u;
+                a = static_cast<int>(ab & 0xFFFFu) - 0x8000;
+                b = static_cast<int>(ab >> 16) - 0x8000;
+            } else {
+                const int4 t = s_cols[d];
+                a = col_int(t.x, t.z, x);
+                b = col_int(t.y, t.w, x);
+            }
             if (static_cast<unsigned>(a) < static_cast<unsigned>(w)) atomicMax(&keyL[a], key);
             if (static_cast<unsigned>(b) < static_cast<unsigned>(w)) atomicMax(&keyR[b], key);
         }
@@ -410,30 +446,23 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                 const uint4 kl = reinterpret_cast<const uint4*>(keyL)[q];
                 const uint4 kr = reinterpret_cast<const uint4*>(keyR)[q];
                 const uint32_t kla[4] = {kl.x, kl.y, kl.z, kl.w}, kra[4] = {kr.x, kr.y, kr.z, kr.w};
-                uint32_t oR = 0, oG = 0, oB = 0, lG = 0, lB = 0, rR = 0;
-                // pixels x >= w have zero keys (never splatted); their mask bits are dropped
-                // below instead of testing x per pixel
+                uint32_t vl[4], vr[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    if (kla[k]) {
-                        const uint32_t v = s_rgb[kXMask - (kla[k] & kXMask)];
-                        oR |= (v & 0xFFu) << (8 * k);
-                        if (MODE == 1) {
-                            lG |= ((v >> 8) & 0xFFu) << (8 * k);
-                            lB |= ((v >> 16) & 0xFFu) << (8 * k);
-                        }
-                    } else {
-                        mL |= 1u << k;
-                    }
-                    if (kra[k]) {
-                        const uint32_t v = s_rgb[kXMask - (kra[k] & kXMask)];
-                        oG |= ((v >> 8) & 0xFFu) << (8 * k);
-                        oB |= ((v >> 16) & 0xFFu) << (8 * k);
-                        if (MODE == 1) rR |= (v & 0xFFu) << (8 * k);
-                    } else {
-                        mR |= 1u << k;
-                    }
+                    // the winning source column, or the zero slot for an unsplatted destination
+                    vl[k] = s_rgb[min(~kla[k] & kXMask, wz)];
+                    vr[k] = s_rgb[min(~kra[k] & kXMask, wz)];
+                    mL |= (kla[k] == 0u ? 1u : 0u) << k;
+                    mR |= (kra[k] == 0u ? 1u : 0u) << k;
                 }
+                auto bytes = [](uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, unsigned sel) {
+                    return __byte_perm(__byte_perm(v0, v1, sel), __byte_perm(v2, v3, sel), 0x5410);
+                };
+                const uint32_t oR = bytes(vl[0], vl[1], vl[2], vl[3], 0x0040);
+                const uint32_t oG = bytes(vr[0], vr[1], vr[2], vr[3], 0x0051);
+                const uint32_t oB = bytes(vr[0], vr[1], vr[2], vr[3], 0x0062);
+                // pixels x >= w have zero keys (never splatted); their mask bits are dropped
+                // below instead of testing x per pixel
                 if (x0 + 4 > w) {
                     const unsigned valid = x0 >= w ? 0u : (1u << (w - x0)) - 1u;
                     mL &= valid;
@@ -454,9 +483,9 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                     put(Rt.plane[1], ro, oG);
                     put(Rt.plane[2], ro, oB);
                     if (MODE == 1) {
-                        put(L.plane[1], lo, lG);
-                        put(L.plane[2], lo, lB);
-                        put(Rt.plane[0], ro, rR);
+                        put(L.plane[1], lo, bytes(vl[0], vl[1], vl[2], vl[3], 0x0051));
+                        put(L.plane[2], lo, bytes(vl[0], vl[1], vl[2], vl[3], 0x0062));
+                        put(Rt.plane[0], ro, bytes(vr[0], vr[1], vr[2], vr[3], 0x0040));
                     }
                 }
             }
@@ -608,7 +637,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                        reinterpret_cast<uintptr_t>(right.plane[1]) | reinterpret_cast<uintptr_t>(right.plane[2]) |
                        static_cast<uintptr_t>(left.pitch) | static_cast<uintptr_t>(right.pitch)) & 3) == 0;
     if (cols && !backward && left.mask_bits && right.mask_bits && left.list && right.list &&
-        vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 <= kMax) {
+        vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 + 16 <= kMax) {
         void (*qk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
                    const int4*, EyeOut, EyeOut, int, int) = ana ? k_dibr_quad<0> : k_dibr_quad<1>;
         static std::atomic<unsigned long long> qconf{0};
@@ -616,7 +645,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
             cudaFuncSetAttribute(k_dibr_quad<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
             cudaFuncSetAttribute(k_dibr_quad<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         });
-        const size_t qsmem = static_cast<size_t>(wpad) * 13;
+        const size_t qsmem = static_cast<size_t>(wpad) * 13 + 16;
         int qper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, qk, 256, qsmem);
         if (qper < 1) qper = 1;

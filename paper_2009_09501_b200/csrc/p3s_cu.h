@@ -44,6 +44,13 @@ cudaError_t depth_front(const uint8_t* r, const uint8_t* g, const uint8_t* b, Ge
                         uint8_t* luma, unsigned long long* sums, int block, int bx,
                         cudaStream_t st, int tile_row0 = 0, int tile_row1 = -1);
 int depth_tile_rows();
+// K1 with the block values folded in, for depth_block == depth_tile_rows() (16), w % 16 == 0
+// and a 16-byte aligned pitch (depth_fused_ok): luma plane + block values of block rows
+// [tile_row0, tile_row1) in one launch, no sums buffer (block_values is not called).
+bool depth_fused_ok(Geom gm, int block);
+cudaError_t depth_front_fused(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
+                              uint8_t* luma, const DepthTables& t, double* values, cudaStream_t st,
+                              int tile_row0 = 0, int tile_row1 = -1);
 // Block values (depth.cpp:55-71) from the sums, block rows [brow0, brow1).
 cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTables& t,
                          double* values, cudaStream_t st, int brow0 = 0, int brow1 = -1);

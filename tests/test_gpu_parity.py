@@ -126,6 +126,17 @@ def test_random_sizes_and_configs(p3s, checker):
         compare_convert(p3s, checker, img, over)
 
 
+@pytest.mark.parametrize("w,h", [(16, 1), (16, 16), (32, 9), (48, 33), (1024, 17), (1040, 40),
+                                 (2064, 50), (3072, 31)])
+def test_fused_depth_front_shapes(p3s, checker, w, h):
+    """The fused depth front (16-pixel blocks, w % 16 == 0: one thread per block, block
+    values written directly) at its edges: one-block frames, partial last block rows,
+    partial last CTAs (w not a multiple of 1024), one-row frames (clamped Sobel rows)."""
+    img = checker.synthetic_frame(w, h, w + h)
+    compare_convert(p3s, checker, img, dict(formats=1))
+    compare_convert(p3s, checker, img, dict(formats=1, alpha=0.0, beta=1.0, base=8))
+
+
 @pytest.mark.parametrize("base", [0, 2, 16, 30, 60, 120, 254, 510])
 def test_parallax_sweep_540p(p3s, checker, base):
     img = checker.synthetic_frame(960, 540, 3)
