@@ -327,6 +327,7 @@ struct Pipeline::Impl {
     double* values = nullptr;
     double *range = nullptr, *spatial = nullptr, *shift = nullptr;
     float* sep_table = nullptr;  // the certified bilateral's replicated FP32 range table
+    uint32_t* wide_keys = nullptr;  // DIBR z-buffer slots for rows wider than shared memory
     int4* cols = nullptr;  // integer DIBR column tables (nullptr: FP64 device path)
     uint8_t *ana = nullptr, *hsbs = nullptr, *fsbs = nullptr, *eyes = nullptr;
     uint32_t* mbits = nullptr;
@@ -410,10 +411,6 @@ struct Pipeline::Impl {
         : dev(device), w(width), h(height), cfg(c), stream(st) {
         cfg.validate();
         pixel_count(w, h);
-        if (w > cu::dibr_max_width())
-            throw std::invalid_argument("frame width " + std::to_string(w) +
-                                        " exceeds the GPU DIBR row limit of " +
-                                        std::to_string(cu::dibr_max_width()) + " pixels");
         pitch = round_up(w, 16);
         fpitch = round_up(2 * w, 16);
         mwords = (w + 31) / 32;
@@ -471,6 +468,7 @@ struct Pipeline::Impl {
         const std::size_t o_bil = a.take<uint32_t>(N + kBilSlots);
         const std::size_t o_ctl = a.take<uint32_t>(128);
         const std::size_t o_stats = a.take<long long>(8);
+        const std::size_t o_wkeys = a.take<uint32_t>(cu::dibr_wide_key_words(w));
         arena_bytes = a.off;
         CK(cudaSetDevice(dev));
         CK(cudaMalloc(&arena, arena_bytes));
@@ -502,6 +500,7 @@ struct Pipeline::Impl {
         bil_list = bil_count + kBilSlots;
         ctl = reinterpret_cast<uint32_t*>(arena + o_ctl);
         stats = reinterpret_cast<long long*>(arena + o_stats);
+        wide_keys = cu::dibr_wide_key_words(w) ? reinterpret_cast<uint32_t*>(arena + o_wkeys) : nullptr;
 
         auto up = [&](std::size_t off, const void* p, std::size_t n) {
             CK(cudaMemcpyAsync(arena + off, p, n, cudaMemcpyHostToDevice, stream));
@@ -539,6 +538,7 @@ struct Pipeline::Impl {
         bands.clear();
         const char* env = std::getenv("P3S_BANDED");
         if (env && std::atoi(env) == 0) return;
+        if (cu::dibr_wide_key_words(w)) return;  // wide rows: one DIBR launch owns the key slots
         for (const BandEnd& e : band_plan(w, h, radius, blk, std::getenv("P3S_BAND_ENDS")))
             bands.push_back(Band{e.in_rows, e.dtile, e.brow, e.urow, e.btile});
         band_ok = !bands.empty();
@@ -672,7 +672,7 @@ struct Pipeline::Impl {
         dibr_eyes(eo);
         if (!backward) CK(cu::zero(zr({{counts, 2u}}), st));
         CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols, backward,
-                    eo[0], eo[1], st));
+                    eo[0], eo[1], st, 0, -1, wide_keys));
         if (mid) record_event(mid, st);
         enq_inpaint(st);
     }
@@ -1078,7 +1078,7 @@ struct Pipeline::Impl {
         record_event(ev[2], st);
         if (!back)
             CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols,
-                        backward, eo[0], eo[1], st));
+                        backward, eo[0], eo[1], st, 0, -1, wide_keys));
         record_event(ev[3], st);
         enq_inpaint(st, true);  // the copy engines are busy with the bands' downloads
         record_event(ev[4], st);
@@ -1607,7 +1607,7 @@ StereoFrames reconstruct(const ImageRGB8& src, const GrayMap& depth, const Conve
         eo[e].count = p->counts + e;
     }
     CK(cu::dibr(p->src, p->src + p->plane(), p->src + 2 * p->plane(), p->filt, p->gm, p->shift,
-                p->cols, p->backward, eo[0], eo[1], st));
+                p->cols, p->backward, eo[0], eo[1], st, 0, -1, p->wide_keys));
     StereoFrames f;
     f.left = ImageRGB8(src.width, src.height, false);
     f.right = ImageRGB8(src.width, src.height, false);

@@ -94,21 +94,27 @@ __device__ __forceinline__ int col_int(int packed, int z, int x) {
 // lane-interleaved mapping (lane l handles pixel base + l): shared-memory accesses are
 // consecutive across the warp, a warp's 32 output bytes per plane are one 32-byte sector
 // store, and 32 pixels' damage flags are one __ballot_sync word.
-template <int ROUTE, bool INT>
+// WIDE: rows wider than a CTA's shared memory (w > dibr_max_width()): the source row is
+// read straight from global memory (L1-cached) and the two key rows live in a global
+// per-CTA slot (wide_keys + blockIdx.x * 2 * wpad); the splat uses global atomicMax (same
+// order-independent maximum). Same output bytes, masks and lists.
+template <int ROUTE, bool INT, bool WIDE = false>
 __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
                                               const uint8_t* __restrict__ G,
                                               const uint8_t* __restrict__ B,
                                               const uint8_t* __restrict__ D, int pitch, int w, int h,
                                               const double* __restrict__ shift_g,
                                               const int4* __restrict__ cols_g, int backward,
-                                              EyeOut L, EyeOut Rt, int ya, int yb) {
+                                              EyeOut L, EyeOut Rt, int ya, int yb,
+                                              uint32_t* __restrict__ wide_keys = nullptr) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ double s_shift[INT ? 1 : 256];
     __shared__ int4 s_cols[INT ? 256 : 1];
     const int wpad = (w + 15) & ~15;
     const int nvec = wpad >> 4;
     uint8_t* s_src = smem;  // [4][wpad]: R, G, B, depth
-    uint32_t* keyL = reinterpret_cast<uint32_t*>(smem + 4 * wpad);
+    uint32_t* keyL = WIDE ? wide_keys + static_cast<size_t>(blockIdx.x) * 2 * wpad
+                          : reinterpret_cast<uint32_t*>(smem + 4 * wpad);
     uint32_t* keyR = keyL + wpad;
     const int tid = threadIdx.x, lane = tid & 31;
     const uint8_t* s_r = s_src;
@@ -142,12 +148,19 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
     for (int y = ya + static_cast<int>(blockIdx.x); y < yb; y += gridDim.x) {
         __syncthreads();  // previous row's readers are done with shared memory
         const size_t row = static_cast<size_t>(y) * pitch;
-        const uint8_t* planes_in[4] = {R + row, G + row, B + row, D + row};
+        if (WIDE) {
+            s_r = R + row;
+            s_g = G + row;
+            s_b = B + row;
+            s_d = D + row;
+        } else {
+            const uint8_t* planes_in[4] = {R + row, G + row, B + row, D + row};
 #pragma unroll
-        for (int pl = 0; pl < 4; ++pl)
-            for (int v = tid; v < nvec; v += blockDim.x)
-                reinterpret_cast<uint4*>(s_src + pl * wpad)[v] =
-                    __ldg(reinterpret_cast<const uint4*>(planes_in[pl]) + v);
+            for (int pl = 0; pl < 4; ++pl)
+                for (int v = tid; v < nvec; v += blockDim.x)
+                    reinterpret_cast<uint4*>(s_src + pl * wpad)[v] =
+                        __ldg(reinterpret_cast<const uint4*>(planes_in[pl]) + v);
+        }
         if (!backward) {
             const uint4 z = make_uint4(0, 0, 0, 0);
             for (int c = tid; c < 2 * wpad / 4; c += blockDim.x) reinterpret_cast<uint4*>(keyL)[c] = z;
@@ -183,7 +196,10 @@ __global__ void __launch_bounds__(256) k_dibr(const uint8_t* __restrict__ R,
                     sl = b >= 0 ? b : x;  // trunc(p.left)
                     sr = a >= 0 ? a : x;  // trunc(p.right)
                 } else {
-                    const unsigned kl = keyL[x], kr = keyR[x];
+                    // (WIDE: the keys were formed by L2 atomics; bypass L1, which may hold
+                    // this slot's lines from the previous row)
+                    const unsigned kl = WIDE ? __ldcg(keyL + x) : keyL[x];
+                    const unsigned kr = WIDE ? __ldcg(keyR + x) : keyR[x];
                     sl = kl ? static_cast<int>(kXMask - (kl & kXMask)) : -1;
                     sr = kr ? static_cast<int>(kXMask - (kr & kXMask)) : -1;
                 }
@@ -603,9 +619,16 @@ __global__ void k_hsbs16(const uint8_t* __restrict__ l0, const uint8_t* __restri
 
 }  // namespace
 
+int dibr_wide_slots() { return 2 * sm_count(); }
+
+size_t dibr_wide_key_words(int w) {
+    if (w <= dibr_max_width()) return 0;
+    return static_cast<size_t>(dibr_wide_slots()) * 2 * static_cast<size_t>((w + 15) & ~15);
+}
+
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
-                 EyeOut right, cudaStream_t st, int ya, int yb) {
+                 EyeOut right, cudaStream_t st, int ya, int yb, uint32_t* wide_keys) {
     if (yb < 0 || yb > gm.h) yb = gm.h;
     if (yb <= ya) return cudaSuccess;
     const int rows = yb - ya;
@@ -619,7 +642,17 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         cudaFuncSetAttribute(k_dibr<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         cudaFuncSetAttribute(k_dibr<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
     });
-    if (smem > kMax) return cudaErrorInvalidValue;
+    if (smem > kMax) {
+        // rows wider than shared memory: global per-CTA key slots (dibr_wide_key_words)
+        if (!wide_keys) return cudaErrorInvalidValue;
+        void (*wk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
+                   const double*, const int4*, int, EyeOut, EyeOut, int, int, uint32_t*) =
+            cols ? k_dibr<1, true, true> : k_dibr<1, false, true>;
+        note_launch(st);
+        wk<<<min(rows, dibr_wide_slots()), 256, 0, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h, shift, cols,
+                                                          backward ? 1 : 0, left, right, ya, yb, wide_keys);
+        return cudaGetLastError();
+    }
     // the fused anaglyph route: left R and right G/B only, bit masks, lists
     const bool ana = left.plane[0] && !left.plane[1] && !left.plane[2] && !right.plane[0] &&
                      right.plane[1] && right.plane[2] && !left.mask_bytes && !right.mask_bytes;
@@ -674,7 +707,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         return cudaGetLastError();
     }
     void (*kern)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
-                 const double*, const int4*, int, EyeOut, EyeOut, int, int) =
+                 const double*, const int4*, int, EyeOut, EyeOut, int, int, uint32_t*) =
         ana ? (cols ? k_dibr<0, true> : k_dibr<0, false>) : (cols ? k_dibr<1, true> : k_dibr<1, false>);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
@@ -682,7 +715,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
     const int grid = min(rows, per_sm * sm_count());
     note_launch(st);
     kern<<<grid, 256, smem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h, shift, cols,
-                                  backward ? 1 : 0, left, right, ya, yb);
+                                  backward ? 1 : 0, left, right, ya, yb, nullptr);
     return cudaGetLastError();
 }
 

@@ -147,10 +147,13 @@ struct EyeOut {
 // x + sigma; see engine.cpp). cols (optional, 256 int4): the host-verified integer column
 // tables (engine.cpp dibr_col_table); when given, no FP64 runs on the device.
 // backward = cfg.dibr_mode == kBackwardFallback.
-// A DIBR row lives in one CTA's shared memory (12 bytes per pixel for the general kernel):
-// frames wider than dibr_max_width() are rejected at plan creation.
+// A DIBR row lives in one CTA's shared memory (12 bytes per pixel for the general kernel)
+// up to dibr_max_width(); wider rows keep their z-buffer keys in global per-CTA slots of
+// dibr_wide_key_words(w) u32 (0 when not needed), passed to dibr() as wide_keys.
 constexpr size_t kDibrMaxSmem = 220 * 1024;  // + the kernels' static tables <= 227 KB
 inline int dibr_max_width() { return static_cast<int>(kDibrMaxSmem / 12) & ~15; }
+int dibr_wide_slots();
+size_t dibr_wide_key_words(int w);
 // Host patch after a banded early download: every 32-pixel word whose mask bit is set
 // (damage the inpaint repaired after the rows left) is copied from the device planes to the
 // host planes (pinned, so device-visible under UVA) with coalesced 32-byte stores.
@@ -164,7 +167,8 @@ struct PatchEye {
 cudaError_t patch_host(PatchEye left, PatchEye right, Geom gm, cudaStream_t st);
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
-                 EyeOut right, cudaStream_t st, int ya = 0, int yb = -1);  // rows [ya, yb)
+                 EyeOut right, cudaStream_t st, int ya = 0, int yb = -1,  // rows [ya, yb)
+                 uint32_t* wide_keys = nullptr);
 
 // Byte mask -> damaged list and (bits != nullptr) 32-pixel damage words of mwords per row
 // (stage-level inpaint entry point).

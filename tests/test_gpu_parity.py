@@ -458,17 +458,24 @@ def test_certified_bilateral_radii(p3s, checker, sigma_s):
     compare_convert(p3s, checker, img, dict(sigma_spatial=sigma_s, sigma_range=float(6 + sigma_s)))
 
 
-def test_widest_supported_rows(p3s, checker):
-    """A DIBR row lives in one CTA's shared memory: the widest supported frame (18768 px)
-    converts bit-exactly in every route; one column more is rejected with INVALID and a
-    message (never a silent wrong result)."""
+def test_widest_shared_memory_rows(p3s, checker):
+    """Up to 18768 px a DIBR row lives in one CTA's shared memory: the widest such frame
+    converts bit-exactly in every route."""
     wmax = 18768
     img = checker.synthetic_frame(wmax, 6, 5)
     compare_convert(p3s, checker, img, dict(formats=7, base=60))
     compare_convert(p3s, checker, img, dict(formats=1))
-    with pytest.raises(p3s.P3SError) as e:
-        p3s.convert(np.zeros((3, 2, wmax + 16), np.uint8), p3s.Config())
-    assert e.value.status == 1 and "exceeds the GPU DIBR row limit" in e.value.message
+
+
+@pytest.mark.parametrize("w,h", [(18784, 5), (20001, 4), (33000, 3)])
+def test_rows_wider_than_shared_memory(p3s, checker, w, h):
+    """Wider rows (the reference converts any width, dibr.cpp:65-104) keep the DIBR z-buffer
+    in global per-CTA key slots: same bytes in every route, forward and backward, with the
+    integer column tables (w < 32768) and the FP64 shift path (w >= 32768)."""
+    img = checker.synthetic_frame(w, h, w % 97)
+    compare_convert(p3s, checker, img, dict(formats=1))
+    compare_convert(p3s, checker, img, dict(formats=5 if w % 2 else 7, base=90))
+    compare_convert(p3s, checker, img, dict(formats=1, mode=1, base=40))
 
 
 @pytest.mark.parametrize("w,h,block,sigma_s", [(500, 700, 4, 8.0), (1283, 389, 37, 3.1),
