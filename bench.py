@@ -580,6 +580,31 @@ def main():
                                      "frames": 300,
                                      "path": "p3s_video_convert, 4 streams, pinned ring of 8 "
                                              "distinct frames, anaglyph out (e2e)"}
+            # the same video as PPM-order payloads (p3s_video_convert_interleaved): the fused
+            # depth front and DIBR read the interleaved frame, DIBR + inpaint write the
+            # interleaved anaglyph (no (de)interleave pass on either side)
+            isrc = [p3s.PinnedBuffer(3 * N, near_device=local) for _ in range(RING)]
+            idst = [p3s.PinnedBuffer(3 * N, near_device=local) for _ in range(RING)]
+            for b, f in zip(isrc, frames):
+                b.array[:] = np.ascontiguousarray(f.transpose(1, 2, 0)).reshape(-1)
+            fp = [isrc[i % RING].ptr for i in range(96)]
+            op = [idst[i % RING].ptr for i in range(96)]
+            vid.convert_ptrs(fp[:8], op[:8], interleaved=True)
+            ipar = None
+            if gate is not None:
+                planar = np.ascontiguousarray(idst[0].array.reshape(H4K, W4K, 3).transpose(2, 0, 1))
+                if sha(planar) != gate["anaglyph"]:
+                    raise SystemExit("bench: parity gate failed: p3s_video_convert_interleaved output differs")
+                ipar = f"seed {seeds[0]}: = reference digest"
+            t0 = time.perf_counter()
+            vid.convert_ptrs(fp, op, interleaved=True)
+            vt = time.perf_counter() - t0
+            extra["video_4k_interleaved"] = {
+                "frames_per_s": 96 / vt, "frames": 96, "parity": ipar,
+                "path": "p3s_video_convert_interleaved, 4 streams, pinned PPM-order payloads in and "
+                        "interleaved anaglyph out (e2e); the fused kernels read / write the "
+                        "interleaved bytes directly"}
+            del isrc, idst
         del vid
         # configs[4]: 8K anamorph (HSBS), 8 frames per GPU (64 over 8 GPUs), device-resident
         W8, H8 = 7680, 4320

@@ -204,6 +204,12 @@ public:
     void upload_interleaved(const std::uint8_t* rgb, std::uint8_t* d_dst, void* stream = nullptr);
     void download_interleaved(StereoFormat f, std::uint8_t* rgb_out, void* stream = nullptr,
                               bool sync = true);
+    // One interleaved frame (host payload, width*height*3 bytes) through the pipeline: H2D into
+    // the staging buffer, then the fused kernels read the payload directly and write the
+    // anaglyph interleaved (anaglyph-only forward configs with 16-pixel blocks and w % 16 == 0),
+    // or the payload is split into planes on the GPU first (every other config). Read the
+    // outputs back with download_interleaved. Async on `stream`; timed = run_timed's events.
+    void run_interleaved(const std::uint8_t* rgb, bool timed = false, void* stream = nullptr);
     struct Impl;
 
 private:

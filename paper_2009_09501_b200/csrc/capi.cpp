@@ -863,8 +863,7 @@ void video_frame(p3s::Pipeline& p, const p3s_video& v, const VideoRun& run, int 
     {
         const uint8_t* f = frames[i];
         if (interleaved) {
-            p.upload_interleaved(f, p.d_input());
-            p.run(p.d_input());
+            p.run_interleaved(f);
             p.download_interleaved(static_cast<p3s::StereoFormat>(v.format), outs[i], nullptr, false);
             return;
         }

@@ -583,6 +583,20 @@ struct Pipeline::Impl {
         return ilv;
     }
 
+    // RGB-interleaved frames (the PPM payload) straight through the fused kernels: the fused
+    // depth front and the quad DIBR read the payload from the staging buffer's first 3N
+    // bytes, DIBR + inpaint write the anaglyph interleaved into its second 3N bytes, so the
+    // file / interleaved-video path makes no separate (de)interleave pass. Other routes and
+    // shapes split the payload into planes first (cu::deinterleave).
+    bool ilv_run = false;         // the frame being enqueued is interleaved (fused kernels)
+    bool last_ilv_fused = false;  // the last run wrote the interleaved anaglyph
+    bool ilv_fused_ok() const {
+        static const bool off = std::getenv("P3S_ILV_UNFUSED") != nullptr;
+        return !off && route == kFusedAnaglyph && !backward && depth_fused() && cols != nullptr &&
+               w % 16 == 0 && !wide_keys &&
+               static_cast<std::size_t>(pitch) * 13 + 16 <= cu::kDibrMaxSmem;
+    }
+
     uint8_t* src_plane(const uint8_t* s, int c) const { return const_cast<uint8_t*>(s) + c * plane(); }
     uint32_t* list_ptr(int eye, int which) const {
         (void)which;
@@ -607,7 +621,9 @@ struct Pipeline::Impl {
     }
     void enq_depth_rows(const uint8_t* s, cudaStream_t st, int d0, int d1, int b0, int b1, int u0,
                         int u1) {
-        if (depth_fused()) {
+        if (ilv_run) {  // s: the interleaved payload
+            CK(cu::depth_front_fused(s, nullptr, nullptr, gm, luma, dt, values, st, d0, d1, 3 * w));
+        } else if (depth_fused()) {
             CK(cu::depth_front_fused(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), gm, luma, dt,
                                      values, st, d0, d1));
         } else {
@@ -646,7 +662,13 @@ struct Pipeline::Impl {
 
     void eye_planes(uint8_t* (&L)[3], uint8_t* (&R)[3], int& lp) const {
         for (int c = 0; c < 3; ++c) L[c] = R[c] = nullptr;
-        if (route == kFusedAnaglyph) {
+        if (route == kFusedAnaglyph && ilv_run) {
+            uint8_t* o = ilv + 3 * npix();  // interleaved anaglyph, row stride 3w
+            L[0] = o;
+            R[1] = o + 1;
+            R[2] = o + 2;
+            lp = 3 * w;
+        } else if (route == kFusedAnaglyph) {
             L[0] = ana;
             R[1] = ana + plane();
             R[2] = ana + 2 * plane();
@@ -671,8 +693,12 @@ struct Pipeline::Impl {
         cu::EyeOut eo[2];
         dibr_eyes(eo);
         if (!backward) CK(cu::zero(zr({{counts, 2u}}), st));
-        CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols, backward,
-                    eo[0], eo[1], st, 0, -1, wide_keys));
+        if (ilv_run)
+            CK(cu::dibr(s, nullptr, nullptr, filt, gm, shift, cols, backward, eo[0], eo[1], st, 0, -1,
+                        nullptr, 3 * w));
+        else
+            CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols, backward,
+                        eo[0], eo[1], st, 0, -1, wide_keys));
         if (mid) record_event(mid, st);
         enq_inpaint(st);
     }
@@ -907,6 +933,7 @@ struct Pipeline::Impl {
     void run(const uint8_t* s, cudaStream_t st, bool record) {
         if ((formats & kFormatHsbs) && (w % 2 != 0))
             throw std::invalid_argument("side_by_side: half mode requires an even width");
+        last_ilv_fused = ilv_run;
         if (!record && graphs_enabled()) {
             run_graph(s, st);
             return;
@@ -989,6 +1016,7 @@ struct Pipeline::Impl {
         for (int e = 0; e < 2; ++e) {
             for (int c = 0; c < 3; ++c) eo[e].plane[c] = e ? R[c] : L[c];
             eo[e].pitch = lp;
+            eo[e].stride = route == kFusedAnaglyph && ilv_run ? 3 : 1;
             eo[e].mask_bytes = nullptr;
             eo[e].mask_bits = backward ? nullptr : mbits + static_cast<std::size_t>(e) * mwords * h;
             eo[e].mask_pitch = mwords;
@@ -1005,6 +1033,7 @@ struct Pipeline::Impl {
         for (int e = 0; e < 2; ++e) {
             for (int c = 0; c < 3; ++c) ie[e].plane[c] = eo[e].plane[c];
             ie[e].pitch = eo[e].pitch;
+            ie[e].stride = eo[e].stride;
             ie[e].mask_bytes = nullptr;
             ie[e].mask_bits = eo[e].mask_bits;
             ie[e].mask_pitch = mwords;
@@ -1439,10 +1468,36 @@ void Pipeline::upload_interleaved(const std::uint8_t* rgb, std::uint8_t* d_dst, 
     CK(cudaMemcpyAsync(buf, rgb, 3 * p.npix(), cudaMemcpyHostToDevice, st));
     CK(cu::deinterleave(buf, p.w, p.h, d_dst, d_dst + p.plane(), d_dst + 2 * p.plane(), p.pitch, st));
 }
+void Pipeline::run_interleaved(const std::uint8_t* rgb, bool timed, void* stream) {
+    Impl& p = *impl_;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
+    uint8_t* buf = p.interleave_buffer();
+    CK(cudaMemcpyAsync(buf, rgb, 3 * p.npix(), cudaMemcpyHostToDevice, st));
+    if (!p.ilv_fused_ok()) {
+        uint8_t* d = p.src;
+        CK(cu::deinterleave(buf, p.w, p.h, d, d + p.plane(), d + 2 * p.plane(), p.pitch, st));
+        p.run(d, st, timed);
+        return;
+    }
+    p.ilv_run = true;
+    try {
+        p.run(buf, st, timed);
+    } catch (...) {
+        p.ilv_run = false;
+        throw;
+    }
+    p.ilv_run = false;
+}
 void Pipeline::download_interleaved(StereoFormat f, std::uint8_t* rgb_out, void* stream, bool sync) {
     Impl& p = *impl_;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p.stream;
     if (!(p.formats & f)) throw std::invalid_argument("format was not requested in the configuration");
+    if (p.last_ilv_fused && f == kFormatAnaglyph) {  // already interleaved by DIBR + inpaint
+        CK(cudaMemcpyAsync(rgb_out, p.interleave_buffer() + 3 * p.npix(), 3 * p.npix(),
+                           cudaMemcpyDeviceToHost, st));
+        if (sync) CK(cudaStreamSynchronize(st));
+        return;
+    }
     uint8_t* buf = p.interleave_buffer();
     const int ow = p.output_width(f), op = p.output_pitch(f);
     const std::size_t ps = static_cast<std::size_t>(op) * p.h;

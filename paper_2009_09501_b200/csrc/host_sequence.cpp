@@ -205,8 +205,9 @@ SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string
         return l;
     };
 
-    // Frames go to the GPU as raw PPM payload (de-interleaved on the device) and come back
-    // as ready-to-write interleaved payload (interleaved on the device): the host never
+    // Frames go to the GPU as raw PPM payload (read interleaved by the fused kernels, or
+    // de-interleaved on the device) and come back as ready-to-write interleaved payload
+    // (written interleaved by DIBR + inpaint, or interleaved on the device): the host never
     // touches pixels. One plan per frame size (two alternating); file reads of frame i+1
     // and writes of frame i-1 run on host threads while frame i is on the device.
     Device& dev = Device::current();
@@ -259,8 +260,7 @@ SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string
         std::unique_ptr<Pipeline>& slot = plan.pipe[ordinal & 1];
         if (!slot) slot = std::make_unique<Pipeline>(view.width, view.height, cfg, dev);
         Pipeline& pipe = *slot;
-        pipe.upload_interleaved(view.payload, pipe.d_input());
-        pipe.run_timed(pipe.d_input());
+        pipe.run_interleaved(view.payload, true);
         struct Out {
             StereoFormat fmt;
             Plane bytes;

@@ -310,13 +310,25 @@ __device__ __forceinline__ void load_pair_row(const uint8_t* row, PairRow& pr) {
     pr.S[8] = __byte_perm(pr.P[7], hr, 0x5432);
 }
 
+// R,G,B of 4 interleaved pixels (3 words r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3) as byte
+// planes (4 pixels per word).
+__device__ __forceinline__ void split_rgb4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& r,
+                                           uint32_t& g, uint32_t& b) {
+    r = __byte_perm(__byte_perm(w0, w1, 0x0630), w2, 0x5210);
+    g = __byte_perm(__byte_perm(w0, w1, 0x0741), w2, 0x6210);
+    b = __byte_perm(__byte_perm(w0, w1, 0x0052), w2, 0x7410);
+}
+
+// ILV: R is one RGB-interleaved image (row stride src_pitch; the PPM payload as uploaded),
+// G and B are unused.
+template <bool ILV>
 __global__ void __launch_bounds__(kFT) k_depth_fused(const uint8_t* __restrict__ R,
                                                      const uint8_t* __restrict__ G,
                                                      const uint8_t* __restrict__ B, int pitch,
                                                      int w, int h, uint8_t* __restrict__ luma,
                                                      double* __restrict__ values, int bx_total,
                                                      double alpha255, double beta,
-                                                     double row_denom, int tile_row0) {
+                                                     double row_denom, int tile_row0, int src_pitch) {
     __shared__ __align__(16) uint8_t s_l[kTH + 2][kFS];
     const int x0 = blockIdx.x * kFW;
     const int y0 = (tile_row0 + blockIdx.y) * kTH;
@@ -335,10 +347,30 @@ __global__ void __launch_bounds__(kFT) k_depth_fused(const uint8_t* __restrict__
                 const int r = rq + 4 * k;
                 if (r < kTH + 2) {
                     const int gy = clampi(y0 - 1 + r, h - 1);
-                    const size_t off = static_cast<size_t>(gy) * pitch + col;
-                    vr[k] = __ldg(reinterpret_cast<const uint4*>(R + off));
-                    vg[k] = __ldg(reinterpret_cast<const uint4*>(G + off));
-                    vb[k] = __ldg(reinterpret_cast<const uint4*>(B + off));
+                    if (ILV) {  // 48 interleaved bytes, planes recovered below
+                        const uint4* src = reinterpret_cast<const uint4*>(R + static_cast<size_t>(gy) * src_pitch + 3 * col);
+                        vr[k] = __ldg(src);
+                        vg[k] = __ldg(src + 1);
+                        vb[k] = __ldg(src + 2);
+                    } else {
+                        const size_t off = static_cast<size_t>(gy) * pitch + col;
+                        vr[k] = __ldg(reinterpret_cast<const uint4*>(R + off));
+                        vg[k] = __ldg(reinterpret_cast<const uint4*>(G + off));
+                        vb[k] = __ldg(reinterpret_cast<const uint4*>(B + off));
+                    }
+                }
+            }
+            if (ILV) {
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    const uint32_t W[12] = {vr[k].x, vr[k].y, vr[k].z, vr[k].w, vg[k].x, vg[k].y,
+                                            vg[k].z, vg[k].w, vb[k].x, vb[k].y, vb[k].z, vb[k].w};
+                    uint32_t pr[4], pg[4], pb[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) split_rgb4(W[3 * i], W[3 * i + 1], W[3 * i + 2], pr[i], pg[i], pb[i]);
+                    vr[k] = make_uint4(pr[0], pr[1], pr[2], pr[3]);
+                    vg[k] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+                    vb[k] = make_uint4(pb[0], pb[1], pb[2], pb[3]);
                 }
             }
 #pragma unroll
@@ -360,8 +392,13 @@ __global__ void __launch_bounds__(kFT) k_depth_fused(const uint8_t* __restrict__
             const int r = i >> 1, side = i & 1;
             const int gy = clampi(y0 - 1 + r, h - 1);
             const int gx = side ? min(x0 + ncols, w - 1) : max(x0 - 1, 0);
-            const size_t off = static_cast<size_t>(gy) * pitch + gx;
-            s_l[r][side ? kFL + ncols : kFL - 1] = luma_px(R[off], G[off], B[off]);
+            if (ILV) {
+                const uint8_t* p = R + static_cast<size_t>(gy) * src_pitch + 3 * static_cast<size_t>(gx);
+                s_l[r][side ? kFL + ncols : kFL - 1] = luma_px(p[0], p[1], p[2]);
+            } else {
+                const size_t off = static_cast<size_t>(gy) * pitch + gx;
+                s_l[r][side ? kFL + ncols : kFL - 1] = luma_px(R[off], G[off], B[off]);
+            }
         }
     }
     __syncthreads();
@@ -536,14 +573,18 @@ bool depth_fused_ok(Geom gm, int block) {
 
 cudaError_t depth_front_fused(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
                               uint8_t* luma, const DepthTables& t, double* values, cudaStream_t st,
-                              int tile_row0, int tile_row1) {
+                              int tile_row0, int tile_row1, int src_ipitch) {
     const int rows = (gm.h + kTH - 1) / kTH;
     if (tile_row1 < 0 || tile_row1 > rows) tile_row1 = rows;
     if (tile_row1 <= tile_row0) return cudaSuccess;
     dim3 grid((gm.w + kFW - 1) / kFW, tile_row1 - tile_row0);
     note_launch(st);
-    k_depth_fused<<<grid, kFT, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, values, t.bx, t.alpha255,
-                                        t.beta, t.row_denom, tile_row0);
+    if (src_ipitch > 0)
+        k_depth_fused<true><<<grid, kFT, 0, st>>>(r, nullptr, nullptr, gm.pitch, gm.w, gm.h, luma, values,
+                                                  t.bx, t.alpha255, t.beta, t.row_denom, tile_row0, src_ipitch);
+    else
+        k_depth_fused<false><<<grid, kFT, 0, st>>>(r, g, b, gm.pitch, gm.w, gm.h, luma, values, t.bx,
+                                                   t.alpha255, t.beta, t.row_denom, tile_row0, 0);
     return cudaGetLastError();
 }
 

@@ -375,13 +375,17 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
 //            mask words over 8-lane groups; one list atomic per warp and eye.
 // MODE 0: anaglyph planes (left R, right G/B); MODE 1: all six eye planes (HSBS / FSBS
 // routes), same z-buffer, masks and lists.
-template <int MODE>
+// ILV (MODE 0, w % 16 == 0): the source is one RGB-interleaved image (R = its base, row
+// stride ipitch; the PPM payload as uploaded) and the anaglyph is written interleaved
+// (L.plane[0] = its base, row stride L.pitch): the file / interleaved-video path with no
+// separate (de)interleave pass.
+template <int MODE, bool ILV = false>
 __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R,
                                                    const uint8_t* __restrict__ G,
                                                    const uint8_t* __restrict__ B,
                                                    const uint8_t* __restrict__ D, int pitch,
                                                    int w, int h, const int4* __restrict__ cols_g,
-                                                   EyeOut L, EyeOut Rt, int ya, int yb) {
+                                                   EyeOut L, EyeOut Rt, int ya, int yb, int ipitch) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int4 s_cols[256];
     __shared__ uint32_t s_off[256];
@@ -419,16 +423,26 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
         __syncthreads();
         const size_t row = static_cast<size_t>(y) * pitch;
         for (int q = tid; q < nq; q += blockDim.x) {
-            const uint32_t r4 = __ldg(reinterpret_cast<const uint32_t*>(R + row) + q);
-            const uint32_t g4 = __ldg(reinterpret_cast<const uint32_t*>(G + row) + q);
-            const uint32_t b4 = __ldg(reinterpret_cast<const uint32_t*>(B + row) + q);
             const uint32_t d4 = __ldg(reinterpret_cast<const uint32_t*>(D + row) + q);
-            const uint32_t rg_lo = __byte_perm(r4, g4, 0x5140), rg_hi = __byte_perm(r4, g4, 0x7362);
             uint4 px;
-            px.x = __byte_perm(rg_lo, b4, 0x0410) & 0x00FFFFFFu;  // r0 g0 b0 0
-            px.y = __byte_perm(rg_lo, b4, 0x0532) & 0x00FFFFFFu;
-            px.z = __byte_perm(rg_hi, b4, 0x0610) & 0x00FFFFFFu;
-            px.w = __byte_perm(rg_hi, b4, 0x0732) & 0x00FFFFFFu;
+            if (ILV) {
+                // 4 interleaved pixels = 3 words r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(R + static_cast<size_t>(y) * ipitch) + 3 * q;
+                const uint32_t w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
+                px.x = w0 & 0x00FFFFFFu;
+                px.y = __byte_perm(w0, w1, 0x0543) & 0x00FFFFFFu;
+                px.z = __byte_perm(w1, w2, 0x0432) & 0x00FFFFFFu;
+                px.w = w2 >> 8;
+            } else {
+                const uint32_t r4 = __ldg(reinterpret_cast<const uint32_t*>(R + row) + q);
+                const uint32_t g4 = __ldg(reinterpret_cast<const uint32_t*>(G + row) + q);
+                const uint32_t b4 = __ldg(reinterpret_cast<const uint32_t*>(B + row) + q);
+                const uint32_t rg_lo = __byte_perm(r4, g4, 0x5140), rg_hi = __byte_perm(r4, g4, 0x7362);
+                px.x = __byte_perm(rg_lo, b4, 0x0410) & 0x00FFFFFFu;  // r0 g0 b0 0
+                px.y = __byte_perm(rg_lo, b4, 0x0532) & 0x00FFFFFFu;
+                px.z = __byte_perm(rg_hi, b4, 0x0610) & 0x00FFFFFFu;
+                px.w = __byte_perm(rg_hi, b4, 0x0732) & 0x00FFFFFFu;
+            }
             reinterpret_cast<uint4*>(s_rgb)[q] = px;
             reinterpret_cast<uint32_t*>(s_d)[q] = d4;
             reinterpret_cast<uint4*>(keyL)[q] = make_uint4(0, 0, 0, 0);
@@ -494,7 +508,13 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                         for (int k = 0; x0 + k < w; ++k) plane[row + x0 + k] = static_cast<uint8_t>(v >> (8 * k));
                     }
                 };
-                if (x0 < w) {
+                if (ILV) {  // w % 16 == 0: whole quads; 12 interleaved bytes
+                    const uint32_t rg0 = __byte_perm(oR, oG, 0x5140), rg1 = __byte_perm(oR, oG, 0x7362);
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(L.plane[0] + lo) + 3 * q;
+                    dst[0] = __byte_perm(rg0, oB, 0x2410);                              // R0 G0 B0 R1
+                    dst[1] = __byte_perm(__byte_perm(rg0, oB, 0x5353), rg1, 0x5410);   // G1 B1 R2 G2
+                    dst[2] = __byte_perm(rg1, oB, 0x7326);                              // B2 R3 G3 B3
+                } else if (x0 < w) {
                     put(L.plane[0], lo, oR);
                     put(Rt.plane[1], ro, oG);
                     put(Rt.plane[2], ro, oB);
@@ -628,7 +648,14 @@ size_t dibr_wide_key_words(int w) {
 
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
-                 EyeOut right, cudaStream_t st, int ya, int yb, uint32_t* wide_keys) {
+                 EyeOut right, cudaStream_t st, int ya, int yb, uint32_t* wide_keys, int src_ipitch) {
+    if (left.stride == 3) {
+        // interleaved source + interleaved anaglyph: the quad kernel's ILV variant only
+        const bool ok = cols && !backward && gm.w % 16 == 0 && left.plane[0] && right.plane[1] &&
+                        right.plane[2] && left.mask_bits && right.mask_bits && left.list && right.list &&
+                        static_cast<size_t>((gm.w + 15) & ~15) * 13 + 16 <= kDibrMaxSmem && src_ipitch > 0;
+        if (!ok) return cudaErrorInvalidValue;
+    }
     if (yb < 0 || yb > gm.h) yb = gm.h;
     if (yb <= ya) return cudaSuccess;
     const int rows = yb - ya;
@@ -669,14 +696,17 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                        reinterpret_cast<uintptr_t>(left.plane[2]) | reinterpret_cast<uintptr_t>(right.plane[0]) |
                        reinterpret_cast<uintptr_t>(right.plane[1]) | reinterpret_cast<uintptr_t>(right.plane[2]) |
                        static_cast<uintptr_t>(left.pitch) | static_cast<uintptr_t>(right.pitch)) & 3) == 0;
-    if (cols && !backward && left.mask_bits && right.mask_bits && left.list && right.list &&
-        vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 + 16 <= kMax) {
+    const bool ilv = left.stride == 3;  // checked above: the quad kernel's ILV variant
+    if (ilv || (cols && !backward && left.mask_bits && right.mask_bits && left.list && right.list &&
+                vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 + 16 <= kMax)) {
         void (*qk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
-                   const int4*, EyeOut, EyeOut, int, int) = ana ? k_dibr_quad<0> : k_dibr_quad<1>;
+                   const int4*, EyeOut, EyeOut, int, int, int) =
+            ilv ? k_dibr_quad<0, true> : ana ? k_dibr_quad<0> : k_dibr_quad<1>;
         static std::atomic<unsigned long long> qconf{0};
         once_per_device(qconf, [] {
             cudaFuncSetAttribute(k_dibr_quad<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
             cudaFuncSetAttribute(k_dibr_quad<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
+            cudaFuncSetAttribute(k_dibr_quad<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         });
         const size_t qsmem = static_cast<size_t>(wpad) * 13 + 16;
         int qper = 0;
@@ -684,7 +714,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         if (qper < 1) qper = 1;
         note_launch(st);
         qk<<<min(rows, qper * sm_count()), 256, qsmem, st>>>(r, g, b, depth, gm.pitch, gm.w, gm.h,
-                                                             cols, left, right, ya, yb);
+                                                             cols, left, right, ya, yb, src_ipitch);
         return cudaGetLastError();
     }
     if (ana && cols && aligned && (backward || (left.mask_bits && right.mask_bits && left.list &&

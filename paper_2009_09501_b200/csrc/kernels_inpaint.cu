@@ -194,14 +194,26 @@ __device__ __forceinline__ void pack16(const uint4& r, const uint4& g, const uin
     }
 }
 
+// 16 interleaved pixels (48 bytes r0 g0 b0 r1 ...) into 16 words 0x??BBGGRR (the top byte
+// is never read).
+__device__ __forceinline__ void unpack_rgb16(const uint4& a, const uint4& b, const uint4& c, uint4 (&o)[4]) {
+    const unsigned W[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // pixels 4i..4i+3: bytes 12i..12i+11 = words 3i..3i+2
+        const unsigned w0 = W[3 * i], w1 = W[3 * i + 1], w2 = W[3 * i + 2];
+        o[i] = make_uint4(w0, __byte_perm(w0, w1, 0x6543), __byte_perm(w1, w2, 0x5432), w2 >> 8);
+    }
+}
+
 // 16 bytes of a plane row from column c, in-image columns only (0 elsewhere / no plane).
-__device__ __noinline__ uint4 load16_bytes(const uint8_t* pl, int pitch, int gy, int c, int w) {
+__device__ __noinline__ uint4 load16_bytes(const uint8_t* pl, int pitch, int gy, int c, int w, int stride) {
     unsigned b[4] = {0u, 0u, 0u, 0u};
     if (pl) {
 #pragma unroll 1
         for (int k = 0; k < 16; ++k)
             if (c + k >= 0 && c + k < w)
-                b[k >> 2] |= static_cast<unsigned>(__ldcg(pl + static_cast<size_t>(gy) * pitch + c + k)) << (8 * (k & 3));
+                b[k >> 2] |= static_cast<unsigned>(__ldcg(pl + static_cast<size_t>(gy) * pitch +
+                                                          static_cast<size_t>(c + k) * stride)) << (8 * (k & 3));
     }
     return make_uint4(b[0], b[1], b[2], b[3]);
 }
@@ -210,6 +222,7 @@ __device__ __noinline__ uint4 load16_bytes(const uint8_t* pl, int pitch, int gy,
 // start and 8-adjacent to damage (need: [64] region-row masks), by 16-pixel quads. A warp
 // instruction covers 8 rows x 4 quads (each row's 64 bytes contiguous: 8 rows are 8-16
 // cache lines, not 32); all loads are issued before any is used.
+template <int STRIDE>
 __device__ __forceinline__ void load_colours(const InpaintEye& io, WarpSmem& S, const unsigned long long* need,
                                              int x0, int y0, int w, int h, bool vec, long long* sub = nullptr) {
 #ifdef P3S_INPAINT_PHASES
@@ -222,11 +235,20 @@ __device__ __forceinline__ void load_colours(const InpaintEye& io, WarpSmem& S, 
     for (int i = 0; i < 8; ++i) {
         const int r = 8 * i + (lane >> 2), c = x0 + 16 * (lane & 3), gy = y0 + r;
         ok[i] = ((need[r] >> (16 * (lane & 3))) & 0xFFFFull) != 0ull;  // in-image by construction
-        fast[i] = ok[i] && vec && c >= 0 && c + 16 <= io.pitch;
-        const size_t o = static_cast<size_t>(gy) * io.pitch + c;
+        fast[i] = ok[i] && vec && c >= 0 && STRIDE * (c + 16) <= io.pitch;
+        if (STRIDE == 3) {
+            // interleaved rows: the quad's 48 bytes (every channel; the ones this eye does
+            // not produce are read but never used or written)
+            const uint8_t* base = io.plane[0] ? io.plane[0] : io.plane[1] ? io.plane[1] - 1 : io.plane[2] - 2;
+            const size_t o = static_cast<size_t>(gy) * io.pitch + 3 * static_cast<size_t>(c);
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch)
-            v[i][ch] = ldcg_if(io.plane[ch] + o, fast[i] && io.plane[ch] != nullptr);
+            for (int ch = 0; ch < 3; ++ch) v[i][ch] = ldcg_if(base + o + 16 * ch, fast[i]);
+        } else {
+            const size_t o = static_cast<size_t>(gy) * io.pitch + c;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+                v[i][ch] = ldcg_if(io.plane[ch] + o, fast[i] && io.plane[ch] != nullptr);
+        }
     }
 #ifdef P3S_INPAINT_PHASES
     long long _s1 = clock64();
@@ -243,13 +265,17 @@ __device__ __forceinline__ void load_colours(const InpaintEye& io, WarpSmem& S, 
 #endif
         if (!ok[i]) continue;
         const int r = 8 * i + (lane >> 2), q = lane & 3, c = x0 + 16 * q, gy = y0 + r;
-        if (!fast[i]) {  // image edge or unaligned planes: bytes, in-image columns only
-            v[i][0] = load16_bytes(io.plane[0], io.pitch, gy, c, w);
-            v[i][1] = load16_bytes(io.plane[1], io.pitch, gy, c, w);
-            v[i][2] = load16_bytes(io.plane[2], io.pitch, gy, c, w);
-        }
         uint4 o[4];
-        pack16(v[i][0], v[i][1], v[i][2], o);
+        if (!fast[i]) {  // image edge or unaligned planes: bytes, in-image columns only
+            v[i][0] = load16_bytes(io.plane[0], io.pitch, gy, c, w, STRIDE);
+            v[i][1] = load16_bytes(io.plane[1], io.pitch, gy, c, w, STRIDE);
+            v[i][2] = load16_bytes(io.plane[2], io.pitch, gy, c, w, STRIDE);
+            pack16(v[i][0], v[i][1], v[i][2], o);
+        } else if (STRIDE == 3) {
+            unpack_rgb16(v[i][0], v[i][1], v[i][2], o);
+        } else {
+            pack16(v[i][0], v[i][1], v[i][2], o);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             S.col[16 * q + 4 * k + 0][r] = o[k].x;
@@ -308,6 +334,7 @@ __device__ __forceinline__ void repair(const InpaintEye& io, WarpSmem& S, const 
 // memory) from S.col to the planes: lane = 4-pixel group of a row, 4 rows per instruction,
 // so the byte stores of a row land in one 32-byte segment. Other tiles read only pixels that
 // were intact at the round's start, so the deferred writes are invisible to them.
+template <int STRIDE>
 __device__ __forceinline__ void publish_colours(const InpaintEye& io, const WarpSmem& S,
                                                 const unsigned long long* rep, int x0, int y0, bool vec) {
     const int lane = threadIdx.x & 31;
@@ -317,9 +344,21 @@ __device__ __forceinline__ void publish_colours(const InpaintEye& io, const Warp
         const int r = kPasses + 4 * b + (lane >> 3);
         const unsigned m = static_cast<unsigned>(rep[r] >> (kPasses + 4 * g)) & 0xFu;
         if (!m) continue;
-        const size_t o = static_cast<size_t>(y0 + r) * io.pitch + (x0 + kPasses + 4 * g);
+        const size_t o = static_cast<size_t>(y0 + r) * io.pitch +
+                         static_cast<size_t>(x0 + kPasses + 4 * g) * STRIDE;
         const int c = kPasses + 4 * g;
         const uint32_t q0 = S.col[c][r], q1 = S.col[c + 1][r], q2 = S.col[c + 2][r], q3 = S.col[c + 3][r];
+        if (STRIDE == 3) {  // interleaved: byte stores of this eye's channels only
+            const uint32_t q[4] = {q0, q1, q2, q3};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!((m >> k) & 1u)) continue;
+                if (io.plane[0]) io.plane[0][o + 3 * k] = static_cast<uint8_t>(q[k]);
+                if (io.plane[1]) io.plane[1][o + 3 * k] = static_cast<uint8_t>(q[k] >> 8);
+                if (io.plane[2]) io.plane[2][o + 3 * k] = static_cast<uint8_t>(q[k] >> 16);
+            }
+            continue;
+        }
         if (m == 0xFu && vec) {  // the whole group: one 4-byte store per plane
             if (io.plane[0]) *reinterpret_cast<uint32_t*>(io.plane[0] + o) = __byte_perm(__byte_perm(q0, q1, 0x0040), __byte_perm(q2, q3, 0x0040), 0x5410);
             if (io.plane[1]) *reinterpret_cast<uint32_t*>(io.plane[1] + o) = __byte_perm(__byte_perm(q0, q1, 0x0051), __byte_perm(q2, q3, 0x0051), 0x5410);
@@ -362,6 +401,7 @@ __device__ unsigned long long g_phase[20];
 #endif
 
 // One warp simulates up to kPasses Jacobi passes of one tile (+ halo) in shared memory.
+template <int STRIDE>
 __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int round, unsigned epoch,
                              WarpSmem& S, const uint32_t* magic, bool vec, uint32_t* counts_slot,
                              bool& remains) {
@@ -429,9 +469,9 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
     __syncwarp();
     const unsigned long long ds0 = d0, ds1 = d1;  // damage at the round's start
 #ifdef P3S_INPAINT_PHASES
-    load_colours(io, S, need, x0, y0, w, h, vec, &_ph[10]);
+    load_colours<STRIDE>(io, S, need, x0, y0, w, h, vec, &_ph[10]);
 #else
-    load_colours(io, S, need, x0, y0, w, h, vec);
+    load_colours<STRIDE>(io, S, need, x0, y0, w, h, vec);
 #endif
     __syncwarp();
     PH_MARK(1);
@@ -506,7 +546,7 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
     repaired[lane] = ds0 & ~d0;
     repaired[lane + 32] = ds1 & ~d1;
     __syncwarp();
-    publish_colours(io, S, repaired, x0, y0, vec);
+    publish_colours<STRIDE>(io, S, repaired, x0, y0, vec);
     if (my_count) atomicAdd(&counts_slot[lane + 1], my_count);
     const unsigned long long dint = lane >= 16 ? d0 : d1;
     const int gyi = lane >= 16 ? gy0 : gy1;
@@ -530,6 +570,8 @@ __device__ void process_tile(const Eye& E, int tx, int ty, int w, int h, int rou
 constexpr int kDbgRounds = 64;
 __device__ unsigned long long* g_inp_rdbg = nullptr;
 
+// STRIDE 3: the eyes' planes are channels of one RGB-interleaved image (InpaintEye.stride).
+template <int STRIDE>
 __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(const __grid_constant__ Eyes eyes, Work wk, int w, int h,
                                                                int tiles_x, int tiles_y, uint32_t* ctl,
                                                                long long* stats, int vec) {
@@ -619,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(const __grid_cons
             if (!skip) {
                 bool remains = false;
                 const unsigned long long tt0 = gtimer();
-                process_tile(eyes.e[e], t % tiles_x, t / tiles_x, w, h, round, epoch, S, s_magic, vec != 0,
+                process_tile<STRIDE>(eyes.e[e], t % tiles_x, t / tiles_x, w, h, round, epoch, S, s_magic, vec != 0,
                              ctl + (e * 3 + slot) * (kPasses + 1), remains);
                 const unsigned long long tt1 = gtimer();
                 (e ? busy[1] : busy[0]) += tt1 - tt0;  // selects keep both in registers
@@ -674,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_inpaint_tiles(const __grid_cons
                     const int y = static_cast<int>(idx / static_cast<uint32_t>(w));
                     // damage as of the end of this round (tags <= round + 1)
                     if (!((word_state(eyes.e[e], y, x >> 5, h, round + 1, epoch) >> (x & 31)) & 1u)) continue;
-                    const size_t o = static_cast<size_t>(y) * io.pitch + x;
+                    const size_t o = static_cast<size_t>(y) * io.pitch + static_cast<size_t>(x) * io.stride;
                     for (int ch = 0; ch < 3; ++ch)
                         if (io.plane[ch]) io.plane[ch][o] = 128;
                 }
@@ -755,11 +797,16 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     const size_t smem = kWarps * sizeof(WarpSmem);
     static std::atomic<unsigned long long> configured{0};
     once_per_device(configured, [smem] {
-        cudaFuncSetAttribute(k_inpaint_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_inpaint_tiles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        cudaFuncSetAttribute(k_inpaint_tiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
     });
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_inpaint_tiles, kThreads, smem);
+    if (left.stride != right.stride || (left.stride != 1 && left.stride != 3)) return cudaErrorInvalidValue;
+    void* kern = left.stride == 3 ? reinterpret_cast<void*>(k_inpaint_tiles<3>)
+                                  : reinterpret_cast<void*>(k_inpaint_tiles<1>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     int blocks = per_sm * sm_count();
     if (max_ctas > 0 && max_ctas < blocks) blocks = max_ctas;
@@ -768,7 +815,7 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     int vec = (left.pitch % 16 == 0 && right.pitch % 16 == 0) ? 1 : 0;
     for (int c = 0; c < 3; ++c)
         for (const InpaintEye* io : {&left, &right})
-            if (io->plane[c] && (reinterpret_cast<uintptr_t>(io->plane[c]) & 15)) vec = 0;
+            if (io->plane[c] && (reinterpret_cast<uintptr_t>(io->plane[c] - (io->stride == 3 ? c : 0)) & 15)) vec = 0;
     void* args[] = {&E, &wk, &w, &h, &tx, &ty, &scratch, &stats, &vec};
     const bool want = getenv("P3S_DEBUG_INPAINT") != nullptr;
     static unsigned long long* rdbg = nullptr;
@@ -778,7 +825,7 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     }
     if (want) cudaMemsetAsync(rdbg, 0, (4 * kDbgRounds + 4) * sizeof(unsigned long long), st);
     note_launch(st);
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_inpaint_tiles), dim3(blocks),
+    e = cudaLaunchCooperativeKernel(kern, dim3(blocks),
                                     dim3(kThreads), args, smem, st);
 #ifdef P3S_INPAINT_PHASES
     if (e == cudaSuccess) {

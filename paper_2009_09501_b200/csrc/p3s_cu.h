@@ -48,9 +48,11 @@ int depth_tile_rows();
 // and a 16-byte aligned pitch (depth_fused_ok): luma plane + block values of block rows
 // [tile_row0, tile_row1) in one launch, no sums buffer (block_values is not called).
 bool depth_fused_ok(Geom gm, int block);
+// src_ipitch > 0: r is one RGB-interleaved image with that row stride (g, b unused; needs
+// src_ipitch % 16 == 0).
 cudaError_t depth_front_fused(const uint8_t* r, const uint8_t* g, const uint8_t* b, Geom gm,
                               uint8_t* luma, const DepthTables& t, double* values, cudaStream_t st,
-                              int tile_row0 = 0, int tile_row1 = -1);
+                              int tile_row0 = 0, int tile_row1 = -1, int src_ipitch = 0);
 // Block values (depth.cpp:55-71) from the sums, block rows [brow0, brow1).
 cudaError_t block_values(const unsigned long long* sums, Geom gm, const DepthTables& t,
                          double* values, cudaStream_t st, int brow0 = 0, int brow1 = -1);
@@ -134,8 +136,9 @@ cudaError_t bilateral(const uint8_t* depth, const uint8_t* guide, Geom gm, int r
 // DIBR output routing. Each eye writes up to three planes (nullptr = channel not needed,
 // e.g. anaglyph needs only left.R and right.G/B). Planes of one eye share a pitch.
 struct EyeOut {
-    uint8_t* plane[3];
+    uint8_t* plane[3];     // stride 3: one RGB-interleaved image, plane[c] = base + c
     int pitch;
+    int stride = 1;        // 1: planar; 3: interleaved (the fused-anaglyph quad kernel only)
     uint8_t* mask_bytes;   // byte mask (reference DamageMask layout), pitch = mask_pitch
     uint32_t* mask_bits;   // or bit mask: ceil(w/32) words per row, bit x%32, 1 = damaged
     int mask_pitch;        // bytes per row (bytes) or words per row (bits)
@@ -168,7 +171,8 @@ cudaError_t patch_host(PatchEye left, PatchEye right, Geom gm, cudaStream_t st);
 cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uint8_t* depth,
                  Geom gm, const double* shift, const int4* cols, bool backward, EyeOut left,
                  EyeOut right, cudaStream_t st, int ya = 0, int yb = -1,  // rows [ya, yb)
-                 uint32_t* wide_keys = nullptr);
+                 uint32_t* wide_keys = nullptr,
+                 int src_ipitch = 0 /* left.stride == 3: r = interleaved source, row stride */);
 
 // Byte mask -> damaged list and (bits != nullptr) 32-pixel damage words of mwords per row
 // (stage-level inpaint entry point).
@@ -182,8 +186,9 @@ cudaError_t mask_to_list(const uint8_t* mask, int mpitch, Geom gm, uint32_t* lis
 // byte mask is not read). `repair` of the left eye points at a device arena of
 // inpaint_scratch_bytes(w, h) (tagged damage words, tile counts, work lists; persistent).
 struct InpaintEye {
-    uint8_t* plane[3];
+    uint8_t* plane[3];     // channel c of pixel (x, y) at plane[c] + y * pitch + x * stride
     int pitch;
+    int stride = 1;        // 1: planar; 3: RGB-interleaved rows (plane[c] = base + c)
     uint8_t* mask_bytes;
     uint32_t* mask_bits;
     int mask_pitch;

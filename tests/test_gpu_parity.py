@@ -424,6 +424,18 @@ def test_convert_sequence_files_match_oracle(p3s, checker, tmp_path):
     assert b"frame 3" in L.p3s_last_error()
     assert sorted(p.name for p in out2.iterdir()) == sorted(
         f"f_{i:03d}_{n}.ppm" for i in (1, 2) for n in ("anaglyph", "fsbs"))
+    # anaglyph only: the fused interleaved kernels for the 96-wide frames, planes for 50x37
+    (src / "f_003.ppm").write_bytes(_ppm_bytes(frames[2]))
+    over = dict(base=10, formats=1)
+    out3 = tmp_path / "out3"
+    out3.mkdir()
+    cfg3 = p3s.Config(**over)
+    st = L.p3s_convert_sequence(str(src).encode(), b"f_%03d.ppm", str(out3).encode(), cfg3.h,
+                                None, None)
+    assert st == 0, L.p3s_last_error()
+    for i, f in enumerate(frames):
+        ref = checker.convert(f, oracle.Cfg(**over))
+        assert (out3 / f"f_{i + 1:03d}_anaglyph.ppm").read_bytes() == _ppm_bytes(ref["anaglyph"]), i
 
 
 def test_video_interleaved_matches_oracle(p3s, checker):
@@ -431,8 +443,12 @@ def test_video_interleaved_matches_oracle(p3s, checker):
     both the 16-pixel vector path (w % 16 == 0) and the per-pixel path (odd width), against
     the CPU oracle's planar output interleaved on the host."""
     import oracle
-    for (w, h, fmt) in ((128, 72, p3s.ANAGLYPH), (97, 41, p3s.FSBS)):
+    # anaglyph-only, forward, w % 16 == 0: the fused kernels read and write the payload
+    # directly (no (de)interleave pass); the others split / join planes on the GPU
+    for (w, h, fmt, extra) in ((128, 72, p3s.ANAGLYPH, {}), (1920, 1080, p3s.ANAGLYPH, dict(base=90)),
+                               (128, 72, p3s.ANAGLYPH, dict(mode=1)), (97, 41, p3s.FSBS, {})):
         over = dict(base=12, formats=fmt)
+        over.update(extra)
         cfg = p3s.Config(**over)
         frames = [p3s.synthetic_frame(w, h, s) for s in range(1, 5)]
         key = "anaglyph" if fmt == p3s.ANAGLYPH else "fsbs"
