@@ -419,35 +419,70 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
     const int nqr = (nq + 31) & ~31;
     const uint32_t wz = static_cast<uint32_t>(wpad);
 
+    // The first kPre quads per thread of the NEXT row are loaded into registers while this row
+    // is splatted and resolved (the row loads otherwise stall every row on HBM/L2 latency);
+    // quads beyond kPre * blockDim.x (rows wider than 4096 px) load when staged.
+    constexpr int kPre = 4;
+    uint32_t pre[kPre][4];
+    auto load_quad = [&](int yy, int q, uint32_t (&v)[4]) {
+        v[3] = __ldg(reinterpret_cast<const uint32_t*>(D + static_cast<size_t>(yy) * pitch) + q);
+        if (ILV) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(R + static_cast<size_t>(yy) * ipitch) + 3 * q;
+            v[0] = __ldg(src);
+            v[1] = __ldg(src + 1);
+            v[2] = __ldg(src + 2);
+        } else {
+            const size_t rr = static_cast<size_t>(yy) * pitch;
+            v[0] = __ldg(reinterpret_cast<const uint32_t*>(R + rr) + q);
+            v[1] = __ldg(reinterpret_cast<const uint32_t*>(G + rr) + q);
+            v[2] = __ldg(reinterpret_cast<const uint32_t*>(B + rr) + q);
+        }
+    };
+    auto prefetch = [&](int yy) {
+        if (yy >= yb) return;
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            const int q = tid + k * static_cast<int>(blockDim.x);
+            if (q < nq) load_quad(yy, q, pre[k]);
+        }
+    };
+    // packed 0x00BBGGRR words of 4 pixels (+ their depth bytes) into the row's shared arrays
+    auto stage = [&](int q, const uint32_t (&v)[4]) {
+        uint4 px;
+        if (ILV) {  // 4 interleaved pixels = 3 words r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
+            px.x = v[0] & 0x00FFFFFFu;
+            px.y = __byte_perm(v[0], v[1], 0x0543) & 0x00FFFFFFu;
+            px.z = __byte_perm(v[1], v[2], 0x0432) & 0x00FFFFFFu;
+            px.w = v[2] >> 8;
+        } else {
+            const uint32_t rg_lo = __byte_perm(v[0], v[1], 0x5140), rg_hi = __byte_perm(v[0], v[1], 0x7362);
+            px.x = __byte_perm(rg_lo, v[2], 0x0410) & 0x00FFFFFFu;  // r0 g0 b0 0
+            px.y = __byte_perm(rg_lo, v[2], 0x0532) & 0x00FFFFFFu;
+            px.z = __byte_perm(rg_hi, v[2], 0x0610) & 0x00FFFFFFu;
+            px.w = __byte_perm(rg_hi, v[2], 0x0732) & 0x00FFFFFFu;
+        }
+        reinterpret_cast<uint4*>(s_rgb)[q] = px;
+        reinterpret_cast<uint32_t*>(s_d)[q] = v[3];
+    };
+    prefetch(ya + static_cast<int>(blockIdx.x));
+
     for (int y = ya + static_cast<int>(blockIdx.x); y < yb; y += gridDim.x) {
         __syncthreads();
-        const size_t row = static_cast<size_t>(y) * pitch;
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            const int q = tid + k * static_cast<int>(blockDim.x);
+            if (q < nq) stage(q, pre[k]);
+        }
+        for (int q = tid + kPre * static_cast<int>(blockDim.x); q < nq; q += blockDim.x) {
+            uint32_t v[4];
+            load_quad(y, q, v);
+            stage(q, v);
+        }
         for (int q = tid; q < nq; q += blockDim.x) {
-            const uint32_t d4 = __ldg(reinterpret_cast<const uint32_t*>(D + row) + q);
-            uint4 px;
-            if (ILV) {
-                // 4 interleaved pixels = 3 words r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(R + static_cast<size_t>(y) * ipitch) + 3 * q;
-                const uint32_t w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
-                px.x = w0 & 0x00FFFFFFu;
-                px.y = __byte_perm(w0, w1, 0x0543) & 0x00FFFFFFu;
-                px.z = __byte_perm(w1, w2, 0x0432) & 0x00FFFFFFu;
-                px.w = w2 >> 8;
-            } else {
-                const uint32_t r4 = __ldg(reinterpret_cast<const uint32_t*>(R + row) + q);
-                const uint32_t g4 = __ldg(reinterpret_cast<const uint32_t*>(G + row) + q);
-                const uint32_t b4 = __ldg(reinterpret_cast<const uint32_t*>(B + row) + q);
-                const uint32_t rg_lo = __byte_perm(r4, g4, 0x5140), rg_hi = __byte_perm(r4, g4, 0x7362);
-                px.x = __byte_perm(rg_lo, b4, 0x0410) & 0x00FFFFFFu;  // r0 g0 b0 0
-                px.y = __byte_perm(rg_lo, b4, 0x0532) & 0x00FFFFFFu;
-                px.z = __byte_perm(rg_hi, b4, 0x0610) & 0x00FFFFFFu;
-                px.w = __byte_perm(rg_hi, b4, 0x0732) & 0x00FFFFFFu;
-            }
-            reinterpret_cast<uint4*>(s_rgb)[q] = px;
-            reinterpret_cast<uint32_t*>(s_d)[q] = d4;
             reinterpret_cast<uint4*>(keyL)[q] = make_uint4(0, 0, 0, 0);
             reinterpret_cast<uint4*>(keyR)[q] = make_uint4(0, 0, 0, 0);
         }
+        prefetch(y + static_cast<int>(gridDim.x));
         __syncthreads();
         const int xsafe = s_xsafe;
         for (int x = tid; x < w; x += blockDim.x) {
