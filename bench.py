@@ -793,8 +793,10 @@ def main():
         "roofline_hbm": [
             hbm_line("k_dibr (forward DIBR fused with anaglyph)", 7 * N, per["dibr_ns"],
                      "4N read (R,G,B,filtered depth) + 3N anaglyph write per frame"),
-            hbm_line("k_depth_front+k_block_values+k_upsample (depth stage)", 5 * N,
-                     per["depth_gen_ns"], "3N read + N luma write + N depth write per frame"),
+            hbm_line("k_depth_fused+k_upsample_rows (depth stage)", 5 * N,
+                     per["depth_gen_ns"], "3N read + N luma write + N depth write per frame; time "
+                     "= the stage's events in the timed pass (two launches, the gap between them "
+                     "included)"),
         ],
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 3 * N,
                 "d2h_bytes_per_step": 3 * N, "steps": e2e_steps,

@@ -5,8 +5,8 @@ import csv, io, json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NCU = "/usr/local/cuda/bin/ncu"
-KERNELS = ["k_depth_front", "k_block_values", "k_upsample", "k_bilateral_sep", "k_bilateral_fixup",
-           "k_dibr", "k_inpaint"]
+KERNELS = ["k_depth_fused", "k_upsample_rows", "k_bilateral_sep", "k_bilateral_fixup", "k_dibr_quad",
+           "k_inpaint"]
 WANT = {"Duration": "us", "DRAM Throughput": "%", "Compute (SM) Throughput": "%",
         "Issue Slots Busy": "%", "L1/TEX Cache Throughput": "%", "Achieved Occupancy": "%",
         "Registers Per Thread": ""}
@@ -58,11 +58,11 @@ def main():
         except (KeyError, TypeError):
             rw = float("nan")
         short = name.split("(")[0].replace("void ", "").replace("unnamed>::", "") or k
-        key = "k_dibr" if k == "k_dibr" else ("k_inpaint_tiles" if k == "k_inpaint" else
-                                              ("k_bilateral_fixup2" if k == "k_bilateral_fixup" else k))
+        key = "k_dibr" if k == "k_dibr_quad" else ("k_inpaint_tiles" if k == "k_inpaint" else
+                                                   ("k_bilateral_fixup2" if k == "k_bilateral_fixup" else k))
         traffic[key] = rw
         print(f"| {short} | " + " | ".join(d.get(x, "") for x in WANT) + f" | {rw / 1e6:.2f} MB |")
-    stage = ["k_depth_front", "k_block_values", "k_upsample"]
+    stage = ["k_depth_fused", "k_upsample_rows"]
     if all(k in traffic for k in stage):  # the depth stage as bench.py's roofline_hbm names it
         traffic["+".join(stage)] = sum(traffic[k] for k in stage)
     with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
