@@ -647,6 +647,65 @@ __global__ void __launch_bounds__(WPB * 32) k_bilateral_fixup2(
         const int gp = s_g[wib][R][R + off];
         const int dy0 = y - R < 0 ? -y : -R;
         const int dy1 = y + R >= h ? h - 1 - y : R;
+        // Every term (per window row: the centre tap, then each mirrored pair as the
+        // reference forms it, each separately rounded) is the reference's; only their
+        // accumulation order decides the last bits. The lanes sum them in any order (<= kM
+        // terms each, then a 5-level tree): the reference's sequential sum and this one are
+        // both within gamma_(n-1) resp. gamma_(kM+4) of the exact sum of these non-negative
+        // terms, so |v - v_ref| <= v (2 (n + kM + 3) + 2) u (u = 2^-53). When v + 0.5 is
+        // farther than that (+1e-12) from every integer both round to the same byte;
+        // otherwise (practically never) the serial reference-order chain below decides.
+        {
+            constexpr int kN = S * (R + 1);
+            constexpr int kM = (kN + 31) / 32;
+            double wsp = 0.0, vsp = 0.0;
+            for (int e = lane; e < kN; e += 32) {
+                const int r = e / (R + 1), j = e - r * (R + 1), dy = r - R;
+                if (dy < dy0 || dy > dy1) continue;
+                const uint8_t* gr = &s_g[wib][r][R + off];
+                const uint8_t* dr = &s_d[wib][r][R + off];
+                const double sj = __ldg(spatial + r * (R + 1) + j);
+                double t = 0.0, u = 0.0;
+                if (j == 0) {
+                    t = __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[0], 0)));
+                    u = __dmul_rn(t, static_cast<double>(dr[0]));
+                } else {
+                    const bool lin = x - j >= 0, rin = x + j < w;
+                    const double wl = lin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[-j], 0))) : 0.0;
+                    const double wr = rin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[j], 0))) : 0.0;
+                    if (lin && rin) {
+                        t = __dadd_rn(wl, wr);
+                        u = __dadd_rn(__dmul_rn(wl, static_cast<double>(dr[-j])),
+                                      __dmul_rn(wr, static_cast<double>(dr[j])));
+                    } else if (lin) {
+                        t = wl;
+                        u = __dmul_rn(wl, static_cast<double>(dr[-j]));
+                    } else if (rin) {
+                        t = wr;
+                        u = __dmul_rn(wr, static_cast<double>(dr[j]));
+                    }
+                }
+                wsp = __dadd_rn(wsp, t);
+                vsp = __dadd_rn(vsp, u);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                wsp = __dadd_rn(wsp, __shfl_xor_sync(0xFFFFFFFFu, wsp, o));
+                vsp = __dadd_rn(vsp, __shfl_xor_sync(0xFFFFFFFFu, vsp, o));
+            }
+            const double v = __ddiv_rn(vsp, wsp);
+            const double f = __dadd_rn(v, 0.5);
+            const double r = floor(f);
+            const double dist = fmin(f - r, r + 1.0 - f);
+            constexpr double kRel = (2.0 * (kN + kM + 3) + 2.0) * 1.1102230246251565e-16 * 1.01;
+            if (dist > v * kRel + 1e-12) {  // every lane holds the same sums: uniform branch
+                if (lane == 0)
+                    out[static_cast<size_t>(y) * pitch + x] =
+                        r <= 0.0 ? 0 : (r >= 255.0 ? 255 : static_cast<uint8_t>(static_cast<int>(r)));
+                __syncwarp();
+                continue;
+            }
+        }
         double ws = 0.0, vs = 0.0;
         for (int rb = 0; rb < S; rb += kBatch) {
             const int nr = min(kBatch, S - rb);
