@@ -16,7 +16,10 @@ cases = [(67, 33, dict()), (130, 72, dict(base=40, formats=7)), (96, 64, dict(mo
          # tall enough for the banded synchronous path (engine.cpp plan_bands): fused
          # anaglyph, direct FSBS, materialised eyes, backward
          (200, 300, dict()), (170, 420, dict(formats=4, base=24)), (150, 400, dict(formats=7, base=40)),
-         (130, 300, dict(mode=1, formats=1))]
+         (130, 300, dict(mode=1, formats=1)),
+         # fused depth stage (w % 16 == 0) through the banded path; a row wider than shared
+         # memory (global z-buffer key slots), forward and backward
+         (256, 300, dict(base=30)), (18784, 3, dict(base=40)), (18784, 3, dict(mode=1, formats=5))]
 for w, h, over in cases:
     img = chk.synthetic_frame(w, h, w + h)
     ref = chk.convert(img, oracle.Cfg(**over))
