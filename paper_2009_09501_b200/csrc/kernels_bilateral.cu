@@ -522,17 +522,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     // tiles [tile_begin, tile_end): the first one per CTA is blockIdx-based, the rest are
     // claimed from tile_ctr (dynamic: CTAs that start late, e.g. behind another launch's
     // tail, simply take fewer tiles)
-    __shared__ int s_next;
+    // the next tile index, double-buffered by iteration parity: slot it & 1 is written before
+    // this iteration's first barrier and read after its second, and written again only two
+    // iterations later, behind both barriers of the iteration in between
+    __shared__ int s_next[2];
     int tile = tile_begin + static_cast<int>(blockIdx.x);
     if (tile < tile_end) prefetch(tile);
     else cp_async_commit();
 
-    while (tile < tile_end) {
+    for (int it = 0; tile < tile_end; ++it) {
         const int tx0 = (tile % tiles_x) * kTX;
         const int ty0 = (tile / tiles_x) * TY;
         cp_async_wait_all();
         if (threadIdx.x == 0)
-            s_next = tile_begin + static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(tile_ctr, 1u));
+            s_next[it & 1] = tile_begin + static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(tile_ctr, 1u));
         __syncthreads();  // raw bytes of this tile landed; the previous tile's compute is done
         for (int e = threadIdx.x; e < SH * SW; e += blockDim.x) {
             const int sy = e / SW, sx = e - sy * SW;
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
             s_tile[e] = v;
         }
         __syncthreads();
-        const int next = s_next;
+        const int next = s_next[it & 1];
         if (next < tile_end) prefetch(next);
         tile = next;
 
