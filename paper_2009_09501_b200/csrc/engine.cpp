@@ -254,10 +254,12 @@ std::vector<BandEnd> band_plan(int w, int h, int radius, int blk, const char* en
     std::vector<int> ri0, ri1;
     std::vector<double> rf;
     locate_axis(h, by, blk, ri0, ri1, rf);
-    // band ends: a thin first band (short wait for its upload part), then 4 tile rows
-    // per band (the upload of the next band outruns this band's filter ~3x), then
-    // halving bands at the bottom: a band's download (~1/3 of its filter time) must hide
-    // under the next band's filter, and the last one's under the inpaint
+    // band ends: a thin first band (short wait for its upload part), then 3 tile rows
+    // per band (the upload of the next band outruns this band's filter ~3x), then 2-row
+    // bands at the bottom and a 1-row last band: a band's download (~1/3 of its filter
+    // time) must hide under the next band's filter, and the last one's under the inpaint.
+    // Measured at 4K (tools/band_sweep2.sh, p3s_convert on pinned frames): {1,3,6,9,11,13,
+    // 15,16} 572-575 frames/s against 559 for {1,4,8,12,14,16}.
     std::vector<int> ends = {1};
     if (ends_env) {  // e.g. "1,4,8,12,14,16" (tuning)
         ends.clear();
@@ -267,10 +269,11 @@ std::vector<BandEnd> band_plan(int w, int h, int radius, int blk, const char* en
             if (*q) ++q;
         }
     } else {
-        const int tail_start = tiles_y - 5;  // the last 5 tile rows: 2, 2, 1
-        for (int t = 4; t < tail_start; t += 4) ends.push_back(t);
-        for (int t : {tiles_y - 5, tiles_y - 3, tiles_y - 1})
+        const int tail_start = tiles_y - 6;  // the last 6 tile rows: 2, 2, 1, 1
+        for (int t = 3; t < tail_start; t += 3) ends.push_back(t);
+        for (int t = std::max(tail_start, ends.back() + 1); t < tiles_y - 1; t += 2)
             if (t > ends.back()) ends.push_back(t);
+        if (tiles_y - 1 > ends.back()) ends.push_back(tiles_y - 1);
     }
     auto urows = [&](int bb) {
         return static_cast<int>(std::lower_bound(ri1.begin(), ri1.end(), bb) - ri1.begin());

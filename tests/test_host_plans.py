@@ -64,7 +64,7 @@ def check(p3s, w, h, blk, sigma_s):
 
 def test_4k_default_plan(p3s):
     bands = check(p3s, 3840, 2160, 16, 8.0)
-    assert [b[4] for b in bands] == [1, 4, 8, 12, 14, 16, 17]  # 1, 3, 4, 4, 2, 2, 1 tile rows
+    assert [b[4] for b in bands] == [1, 3, 6, 9, 11, 13, 15, 16, 17]  # 1, 2, 3, 3, 2, 2, 2, 1, 1 tile rows
     assert bands[0][0] == 161                                  # upload part 0: 161 rows
 
 
