@@ -483,6 +483,47 @@ def main():
     (e2e_max,) = dist.max(e2e_s)
     e2e_fps = e2e_steps * world / e2e_max
 
+    # ---- the same synchronous call from several long-lived host threads at once (a server
+    # answering concurrent requests; plans are cached per thread, so each thread warms its
+    # own plan first; each has its own stream). Informational, not the headline ----
+    nthr, per_thr = 2, max(8, e2e_steps // 2)
+    gate_bar = threading.Barrier(nthr + 1)
+    errs = [None] * nthr
+
+    def conv_worker(k):
+        r, a = C.c_void_p(), C.c_void_p()
+        for phase in (RING, per_thr):
+            gate_bar.wait()
+            for j in range(phase):
+                if errs[k] is None and L.p3s_convert(images[(k + nthr * j) % RING].h, cfg.h, C.byref(r)) != 0:
+                    errs[k] = L.p3s_last_error().decode()
+                if errs[k] is None:
+                    L.p3s_result_output(r, 1, C.byref(a))
+                    L.p3s_result_free(r)
+            gate_bar.wait()
+
+    thr = [threading.Thread(target=conv_worker, args=(k,)) for k in range(nthr)]
+    for t in thr:
+        t.start()
+    gate_bar.wait()
+    gate_bar.wait()  # every thread's plan is warm
+    dist.barrier()
+    gate_bar.wait()
+    t0 = time.perf_counter()
+    gate_bar.wait()
+    ct_s = time.perf_counter() - t0
+    for t in thr:
+        t.join()
+    dist.barrier()
+    (ct_max,) = dist.max(ct_s)
+    if any(errs):
+        raise SystemExit(f"bench: concurrent p3s_convert failed: {errs}")
+    e2e_threads = {"value": nthr * per_thr * world / ct_max, "unit": "frames/s", "threads": nthr,
+                   "calls": nthr * per_thr,
+                   "path": f"p3s_convert + p3s_result_output from {nthr} long-lived host threads at "
+                           "once (pinned images, one plan and stream per thread); informational, "
+                           "the headline e2e above is one caller"}
+
     # ---- e2e through the streaming video API (pinned host frames, 4 streams) ----
     vid = p3s.Video(W4K, H4K, cfg, streams=4)
     src = [p3s.PinnedBuffer(3 * N, near_device=local) for _ in range(RING)]
@@ -804,6 +845,7 @@ def main():
                         "p3s_image, then p3s_result_output(anaglyph) read on the host; depth "
                         "and filtered depth stay on the GPU until p3s_result_depth asks"},
         "e2e_stream": e2e_stream,
+        "e2e_threads": e2e_threads,
         "gpu_launches": launches,
         "gpu_launches_note": "kernels launched in the timed value loop on rank 0, counted by the "
                              "library (p3s_gpu_launch_count: direct launches + kernel nodes of "

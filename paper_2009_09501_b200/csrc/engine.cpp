@@ -370,7 +370,10 @@ struct Pipeline::Impl {
     bool own_stream = false;
     // CTAs of the cooperative inpaint (0: one per SM). Fewer leave SMs to other pipelines'
     // frames: more aggregate throughput with several streams, longer single-frame latency.
-    int inpaint_ctas = 0;
+    int inpaint_ctas = [] {  // P3S_INPAINT_CTAS: experiment override of the default (0: one per SM)
+        const char* e = std::getenv("P3S_INPAINT_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
     void set_inpaint_ctas(int ctas);
 
     // Row-banded synchronous conversion (convert_image on pinned host planes). The frame is
