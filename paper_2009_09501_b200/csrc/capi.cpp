@@ -26,6 +26,7 @@
 #include "p3s_gpu.h"
 #include "p3s_cu.h"
 #include "p3s_host.hpp"
+#include "p3s_nvtx.hpp"
 #include "pseudo3d.h"
 
 struct p3s_image {
@@ -860,6 +861,7 @@ void video_frame(p3s::Pipeline& p, const p3s_video& v, const VideoRun& run, int 
     const bool interleaved = run.interleaved;
     const uint8_t* const* frames = run.frames;
     uint8_t* const* outs = run.outs;
+    p3s::NvtxRange nv(interleaved ? "p3s_video frame (interleaved)" : "p3s_video frame");
     {
         const uint8_t* f = frames[i];
         if (interleaved) {

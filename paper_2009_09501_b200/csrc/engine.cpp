@@ -25,6 +25,7 @@
 
 #include "p3s/pipeline.hpp"
 #include "p3s_cu.h"
+#include "p3s_nvtx.hpp"
 
 namespace p3s {
 
@@ -1892,6 +1893,7 @@ const GrayMap& DeferredMaps::filtered() {
 
 ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionConfig& cfg,
                                         Device& dev, std::shared_ptr<DeferredMaps>& maps) {
+    NvtxRange nv_conv("p3s_convert");
     cfg.validate();
     auto p = stage_plan(dev, src.width, src.height, cfg);
     cudaStream_t st = p->stream;
@@ -1904,7 +1906,11 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
     }
     const auto t0 = std::chrono::steady_clock::now();
     if (dbg) CK(cudaEventRecord(dbg_ev[0], st));
-    const bool have_outputs = p->upload_run_conv(src, st, &res.outputs);
+    bool have_outputs;
+    {
+        NvtxRange nv("p3s_convert: upload + enqueue");
+        have_outputs = p->upload_run_conv(src, st, &res.outputs);
+    }
     const auto t1 = std::chrono::steady_clock::now();
     const std::size_t n = p->npix();
     uint8_t* buf = static_cast<uint8_t*>(map_pool().take(dev.ordinal(), 2 * n));
@@ -1933,7 +1939,10 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
             res.outputs[f] = std::move(img);
         }
         if (dbg) CK(cudaEventRecord(dbg_ev[1], st));
-        CK(cudaStreamSynchronize(st));
+        {
+            NvtxRange nv("p3s_convert: wait");
+            CK(cudaStreamSynchronize(st));
+        }
         if (p->last_banded && !p->cal_valid) p->calibrate(st);
         res.timings = p->timings();
         if (dbg) {
@@ -1990,6 +1999,7 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
 }
 
 ConversionResult convert_image(const ImageRGB8& src, const ConversionConfig& cfg, Device& dev) {
+    NvtxRange nv_conv("p3s_convert");
     cfg.validate();
     auto p = stage_plan(dev, src.width, src.height, cfg);
     cudaStream_t st = p->stream;

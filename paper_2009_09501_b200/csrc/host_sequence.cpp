@@ -22,6 +22,7 @@
 #include <thread>
 
 #include "p3s_host.hpp"
+#include "p3s_nvtx.hpp"
 
 namespace p3s {
 
@@ -260,7 +261,10 @@ SequenceReport convert_sequence_dir(const std::string& in_dir, const std::string
         std::unique_ptr<Pipeline>& slot = plan.pipe[ordinal & 1];
         if (!slot) slot = std::make_unique<Pipeline>(view.width, view.height, cfg, dev);
         Pipeline& pipe = *slot;
-        pipe.run_interleaved(view.payload, true);
+        {
+            NvtxRange nv("p3s_convert_sequence frame");
+            pipe.run_interleaved(view.payload, true);
+        }
         struct Out {
             StereoFormat fmt;
             Plane bytes;
