@@ -60,7 +60,10 @@ constexpr int kE = kT + 2 * kPasses;   // region side (64: one u64 per row)
 constexpr int kWarps = 8;              // one tile per warp
 constexpr int kThreads = 32 * kWarps;
 constexpr uint32_t kHeavy = 128;       // damaged pixels that make a tile "heavy" (run first)
-constexpr int kDirect = 4;             // per-lane repairs up to which a pass skips compaction
+#ifndef P3S_INPAINT_KDIRECT  // experiment builds: make VARIANT=x EXTRA=-DP3S_INPAINT_KDIRECT=n
+#define P3S_INPAINT_KDIRECT 4
+#endif
+constexpr int kDirect = P3S_INPAINT_KDIRECT;  // per-lane repairs up to which a pass skips compaction
 constexpr int kCtlWords = 128;         // ctl scratch: [eye][slot 0..2][kPasses + 1] + barrier
 constexpr int kBarWord = 127;          // ctl word: the grid barrier's arrival counter
 constexpr unsigned long long kInner = 0x0000FFFFFFFF0000ull;  // interior columns 16..47
