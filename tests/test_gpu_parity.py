@@ -137,6 +137,31 @@ def test_fused_depth_front_shapes(p3s, checker, w, h):
     compare_convert(p3s, checker, img, dict(formats=1, alpha=0.0, beta=1.0, base=8))
 
 
+def test_random_fused_paths(p3s, checker):
+    """Random shapes on the round-2 fast paths: the fused depth stage (w % 16 == 0, 16-pixel
+    blocks), the quad DIBR splat fast path and its left-edge general region (large bases),
+    and the interleaved video path (PPM-order payloads in and out), against the oracle."""
+    import oracle
+    rng = np.random.default_rng(11)
+    for i in range(10):
+        w = 16 * int(rng.integers(1, 90))
+        h = int(rng.integers(1, 140))
+        over = dict(base=int(rng.choice([-1, 0, 2, 30, 100, 254])),
+                    pop_threshold=int(rng.integers(0, 256)),
+                    sigma_spatial=float(rng.choice([2.5, 8.0])), alpha=float(rng.choice([0.0, 0.7])),
+                    beta=float(rng.choice([0.0, 0.3])), formats=1)
+        img = checker.synthetic_frame(w, h, 100 + i)
+        compare_convert(p3s, checker, img, over)
+        if i % 3 == 0:
+            cfg = p3s.Config(**over)
+            src, dst = p3s.PinnedBuffer(3 * w * h), p3s.PinnedBuffer(3 * w * h)
+            src.array[:] = img.transpose(1, 2, 0).reshape(-1)
+            vid = p3s.Video(w, h, cfg, streams=1)
+            vid.convert_ptrs([src.ptr], [dst.ptr], interleaved=True)
+            ref = checker.convert(img, oracle.Cfg(**over), threads=NCPU)["anaglyph"]
+            assert np.array_equal(dst.array.reshape(h, w, 3), np.ascontiguousarray(ref.transpose(1, 2, 0))), over
+
+
 @pytest.mark.parametrize("base", [0, 2, 16, 30, 60, 120, 254, 510])
 def test_parallax_sweep_540p(p3s, checker, base):
     img = checker.synthetic_frame(960, 540, 3)
