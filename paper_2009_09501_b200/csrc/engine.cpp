@@ -601,7 +601,7 @@ struct Pipeline::Impl {
         static const bool off = std::getenv("P3S_ILV_UNFUSED") != nullptr;
         return !off && route == kFusedAnaglyph && !backward && depth_fused() && cols != nullptr &&
                w % 16 == 0 && !wide_keys &&
-               static_cast<std::size_t>(pitch) * 13 + 16 <= cu::kDibrMaxSmem;
+               static_cast<std::size_t>(pitch) * 13 + 48 <= cu::kDibrMaxSmem;
     }
 
     uint8_t* src_plane(const uint8_t* s, int c) const { return const_cast<uint8_t*>(s) + c * plane(); }

@@ -356,6 +356,20 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
     }
 }
 
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void red_max_shared(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // Forward DIBR + anaglyph, quad version (the default route): the same z-buffer and output
 // bytes as k_dibr_ana<false> with far fewer instructions per pixel.
 //   stage    lane-contiguous 4-pixel words of R, G, B, depth (128-byte warp requests); the
@@ -392,10 +406,10 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
     __shared__ int s_xsafe;
     const int wpad = (w + 15) & ~15;
     const int nq = wpad >> 2;  // quads
-    uint32_t* s_rgb = reinterpret_cast<uint32_t*>(smem);      // [wpad + 4]
-    uint32_t* keyL = s_rgb + wpad + 4;                         // [wpad]
-    uint32_t* keyR = keyL + wpad;                              // [wpad]
-    uint8_t* s_d = reinterpret_cast<uint8_t*>(keyR + wpad);    // [wpad]
+    uint32_t* s_rgb = reinterpret_cast<uint32_t*>(smem);      // [wpad + 4]: slot wpad = 0
+    uint32_t* keyL = s_rgb + wpad + 4;                         // [wpad + 4]: slot w = dump
+    uint32_t* keyR = keyL + wpad + 4;                          // [wpad + 4]
+    uint8_t* s_d = reinterpret_cast<uint8_t*>(keyR + wpad + 4);  // [wpad]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_xsafe = 0;
     if (tid < 4) s_rgb[wpad + tid] = 0u;
@@ -418,6 +432,14 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
     }
     const int nqr = (nq + 31) & ~31;
     const uint32_t wz = static_cast<uint32_t>(wpad);
+    const uint32_t kinit = kXMask - wz;
+    // 32-bit shared-window addresses, formed once (the splat's loads and atomics use them
+    // directly: no generic-to-shared conversion inside the loop)
+    const uint32_t sa_d = static_cast<uint32_t>(__cvta_generic_to_shared(s_d));
+    const uint32_t sa_off = static_cast<uint32_t>(__cvta_generic_to_shared(s_off));
+    const uint32_t sa_kl = static_cast<uint32_t>(__cvta_generic_to_shared(keyL));
+    const uint32_t sa_kr = static_cast<uint32_t>(__cvta_generic_to_shared(keyR));
+    const uint32_t uw = static_cast<uint32_t>(w);
 
     // The first kPre quads per thread of the NEXT row are loaded into registers while this row
     // is splatted and resolved (the row loads otherwise stall every row on HBM/L2 latency);
@@ -478,28 +500,36 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
             load_quad(y, q, v);
             stage(q, v);
         }
-        for (int q = tid; q < nq; q += blockDim.x) {
-            reinterpret_cast<uint4*>(keyL)[q] = make_uint4(0, 0, 0, 0);
-            reinterpret_cast<uint4*>(keyR)[q] = make_uint4(0, 0, 0, 0);
+        // unsplatted destinations keep kinit: depth field 0 (damaged), and its gather index
+        // ~kinit & kXMask is the zero slot wz, so the resolve needs no branch or clamp
+        for (int q = tid; q < nq + 1; q += blockDim.x) {
+            reinterpret_cast<uint4*>(keyL)[q] = make_uint4(kinit, kinit, kinit, kinit);
+            reinterpret_cast<uint4*>(keyR)[q] = make_uint4(kinit, kinit, kinit, kinit);
         }
         prefetch(y + static_cast<int>(gridDim.x));
         __syncthreads();
         const int xsafe = s_xsafe;
-        for (int x = tid; x < w; x += blockDim.x) {
+        // destinations outside [0, w) go to the dump slot w (unsigned min), so every source
+        // does both atomics unconditionally. Left edge (x < xsafe): the exact general form.
+        int x = tid;
+        for (; x < xsafe && x < w; x += blockDim.x) {
             const int d = s_d[x];
             const unsigned key = (static_cast<unsigned>(d + 1) << 22) | (kXMask - x);
-            int a, b;
-            if (x >= xsafe) {
-                const uint32_t ab = s_off[d] + static_cast<uint32_t>(x) * 0x10001u;
-                a = static_cast<int>(ab & 0xFFFFu) - 0x8000;
-                b = static_cast<int>(ab >> 16) - 0x8000;
-            } else {
-                const int4 t = s_cols[d];
-                a = col_int(t.x, t.z, x);
-                b = col_int(t.y, t.w, x);
-            }
-            if (static_cast<unsigned>(a) < static_cast<unsigned>(w)) atomicMax(&keyL[a], key);
-            if (static_cast<unsigned>(b) < static_cast<unsigned>(w)) atomicMax(&keyR[b], key);
+            const int4 t = s_cols[d];
+            const uint32_t a = min(static_cast<uint32_t>(col_int(t.x, t.z, x)), uw);
+            const uint32_t b = min(static_cast<uint32_t>(col_int(t.y, t.w, x)), uw);
+            red_max_shared(sa_kl + 4 * a, key);
+            red_max_shared(sa_kr + 4 * b, key);
+        }
+        // the rest: both columns from one add on the packed biased offsets
+        for (; x < w; x += blockDim.x) {
+            const uint32_t d = lds_u8(sa_d + x);
+            const uint32_t key = ((d + 1u) << 22) | (kXMask - static_cast<uint32_t>(x));
+            const uint32_t ab = lds_u32(sa_off + 4 * d) + static_cast<uint32_t>(x) * 0x10001u;
+            const uint32_t a = min((ab & 0xFFFFu) - 0x8000u, uw);
+            const uint32_t b = min((ab >> 16) - 0x8000u, uw);
+            red_max_shared(sa_kl + 4 * a, key);
+            red_max_shared(sa_kr + 4 * b, key);
         }
         __syncthreads();
         const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
@@ -515,10 +545,10 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     // the winning source column, or the zero slot for an unsplatted destination
-                    vl[k] = s_rgb[min(~kla[k] & kXMask, wz)];
-                    vr[k] = s_rgb[min(~kra[k] & kXMask, wz)];
-                    mL |= (kla[k] == 0u ? 1u : 0u) << k;
-                    mR |= (kra[k] == 0u ? 1u : 0u) << k;
+                    vl[k] = s_rgb[~kla[k] & kXMask];
+                    vr[k] = s_rgb[~kra[k] & kXMask];
+                    mL |= (kla[k] < 0x400000u ? 1u : 0u) << k;
+                    mR |= (kra[k] < 0x400000u ? 1u : 0u) << k;
                 }
                 auto bytes = [](uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, unsigned sel) {
                     return __byte_perm(__byte_perm(v0, v1, sel), __byte_perm(v2, v3, sel), 0x5410);
@@ -526,8 +556,8 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
                 const uint32_t oR = bytes(vl[0], vl[1], vl[2], vl[3], 0x0040);
                 const uint32_t oG = bytes(vr[0], vr[1], vr[2], vr[3], 0x0051);
                 const uint32_t oB = bytes(vr[0], vr[1], vr[2], vr[3], 0x0062);
-                // pixels x >= w have zero keys (never splatted); their mask bits are dropped
-                // below instead of testing x per pixel
+                // pixels x >= w (never a destination except the dump slot) have their mask
+                // bits dropped below instead of testing x per pixel
                 if (x0 + 4 > w) {
                     const unsigned valid = x0 >= w ? 0u : (1u << (w - x0)) - 1u;
                     mL &= valid;
@@ -688,7 +718,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
         // interleaved source + interleaved anaglyph: the quad kernel's ILV variant only
         const bool ok = cols && !backward && gm.w % 16 == 0 && left.plane[0] && right.plane[1] &&
                         right.plane[2] && left.mask_bits && right.mask_bits && left.list && right.list &&
-                        static_cast<size_t>((gm.w + 15) & ~15) * 13 + 16 <= kDibrMaxSmem && src_ipitch > 0;
+                        static_cast<size_t>((gm.w + 15) & ~15) * 13 + 48 <= kDibrMaxSmem && src_ipitch > 0;
         if (!ok) return cudaErrorInvalidValue;
     }
     if (yb < 0 || yb > gm.h) yb = gm.h;
@@ -733,7 +763,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
                        static_cast<uintptr_t>(left.pitch) | static_cast<uintptr_t>(right.pitch)) & 3) == 0;
     const bool ilv = left.stride == 3;  // checked above: the quad kernel's ILV variant
     if (ilv || (cols && !backward && left.mask_bits && right.mask_bits && left.list && right.list &&
-                vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 + 16 <= kMax)) {
+                vec == 2 && ((ana && aligned) || six) && static_cast<size_t>(wpad) * 13 + 48 <= kMax)) {
         void (*qk)(const uint8_t*, const uint8_t*, const uint8_t*, const uint8_t*, int, int, int,
                    const int4*, EyeOut, EyeOut, int, int, int) =
             ilv ? k_dibr_quad<0, true> : ana ? k_dibr_quad<0> : k_dibr_quad<1>;
@@ -743,7 +773,7 @@ cudaError_t dibr(const uint8_t* r, const uint8_t* g, const uint8_t* b, const uin
             cudaFuncSetAttribute(k_dibr_quad<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
             cudaFuncSetAttribute(k_dibr_quad<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMax);
         });
-        const size_t qsmem = static_cast<size_t>(wpad) * 13 + 16;
+        const size_t qsmem = static_cast<size_t>(wpad) * 13 + 48;
         int qper = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&qper, qk, 256, qsmem);
         if (qper < 1) qper = 1;
