@@ -356,18 +356,21 @@ __global__ void __launch_bounds__(256) k_dibr_ana(const uint8_t* __restrict__ R,
     }
 }
 
+// Shared-window loads of arrays the splat only reads (not volatile: the compiler may hoist
+// them across the reductions, which touch only the key rows; the barriers order everything
+// else) and the z-buffer reduction itself (its result is read after a barrier).
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
     uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ void red_max_shared(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+    asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 
 // Forward DIBR + anaglyph, quad version (the default route): the same z-buffer and output
@@ -521,16 +524,28 @@ __global__ void __launch_bounds__(256) k_dibr_quad(const uint8_t* __restrict__ R
             red_max_shared(sa_kl + 4 * a, key);
             red_max_shared(sa_kr + 4 * b, key);
         }
-        // the rest: both columns from one add on the packed biased offsets
-        for (; x < w; x += blockDim.x) {
-            const uint32_t d = lds_u8(sa_d + x);
-            const uint32_t key = ((d + 1u) << 22) | (kXMask - static_cast<uint32_t>(x));
-            const uint32_t ab = lds_u32(sa_off + 4 * d) + static_cast<uint32_t>(x) * 0x10001u;
-            const uint32_t a = min((ab & 0xFFFFu) - 0x8000u, uw);
-            const uint32_t b = min((ab >> 16) - 0x8000u, uw);
-            red_max_shared(sa_kl + 4 * a, key);
-            red_max_shared(sa_kr + 4 * b, key);
+        // the rest: both columns from one add on the packed biased offsets; two sources per
+        // iteration, so their dependent loads (depth, then offsets) overlap
+        const int step = static_cast<int>(blockDim.x);
+        auto splat_fast = [&](int xx) {
+            const uint32_t d = lds_u8(sa_d + xx);
+            const uint32_t key = ((d + 1u) << 22) | (kXMask - static_cast<uint32_t>(xx));
+            const uint32_t ab = lds_u32(sa_off + 4 * d) + static_cast<uint32_t>(xx) * 0x10001u;
+            red_max_shared(sa_kl + 4 * min((ab & 0xFFFFu) - 0x8000u, uw), key);
+            red_max_shared(sa_kr + 4 * min((ab >> 16) - 0x8000u, uw), key);
+        };
+        for (; x + step < w; x += 2 * step) {
+            const uint32_t d0 = lds_u8(sa_d + x), d1 = lds_u8(sa_d + x + step);
+            const uint32_t ab0 = lds_u32(sa_off + 4 * d0) + static_cast<uint32_t>(x) * 0x10001u;
+            const uint32_t ab1 = lds_u32(sa_off + 4 * d1) + static_cast<uint32_t>(x + step) * 0x10001u;
+            const uint32_t k0 = ((d0 + 1u) << 22) | (kXMask - static_cast<uint32_t>(x));
+            const uint32_t k1 = ((d1 + 1u) << 22) | (kXMask - static_cast<uint32_t>(x + step));
+            red_max_shared(sa_kl + 4 * min((ab0 & 0xFFFFu) - 0x8000u, uw), k0);
+            red_max_shared(sa_kr + 4 * min((ab0 >> 16) - 0x8000u, uw), k0);
+            red_max_shared(sa_kl + 4 * min((ab1 & 0xFFFFu) - 0x8000u, uw), k1);
+            red_max_shared(sa_kr + 4 * min((ab1 >> 16) - 0x8000u, uw), k1);
         }
+        if (x < w) splat_fast(x);
         __syncthreads();
         const uint32_t row_base = static_cast<uint32_t>(y) * static_cast<uint32_t>(w);
         for (int qb = warp * 32; qb < nqr; qb += blockDim.x) {
