@@ -770,7 +770,26 @@ def main():
         for i in range(16):
             p1.run(ring1[i % n1].addr, timed=True)
         st1, n1r = p1.timing_sum(reset=True)
+        # e2e at 1080p: p3s_convert on pinned images + the anaglyph read on the host
+        imgs1 = [p3s.Image(p3s.synthetic_frame(W1, H1, frame_seed(i))) for i in range(8)]
+        r1, o1 = C.c_void_p(), C.c_void_p()
+        for i in range(8):
+            p3s._check(L.p3s_convert(imgs1[i].h, cfg.h, C.byref(r1)))
+            L.p3s_result_free(r1)
+        ne1 = 64
+        dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(ne1):
+            p3s._check(L.p3s_convert(imgs1[i % 8].h, cfg.h, C.byref(r1)))
+            p3s._check(L.p3s_result_output(r1, 1, C.byref(o1)))
+            L.p3s_result_free(r1)
+        (e1,) = dist.max(time.perf_counter() - t0)
+        del imgs1
         extra["image_1080p"] = {"config": "BASELINE configs[0]", "frames_per_s": nf1 * world / (ms1 / 1e3),
+                                "e2e": {"value": ne1 * world / e1, "unit": "frames/s",
+                                        "h2d_bytes_per_step": 3 * W1 * H1, "d2h_bytes_per_step": 3 * W1 * H1,
+                                        "path": "p3s_convert + p3s_result_output on pinned 1080p images, "
+                                                "one synchronous call per frame"},
                                 "stages_ms": {k: v / n1r / 1e6 for k, v in st1.items()},
                                 "l2": f"ring of {n1} distinct frames ({n1 * 3 * W1 * H1 / 1e6:.0f} MB "
                                       f"> 3 x 126 MB L2): HBM-resident",
