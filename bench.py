@@ -554,36 +554,63 @@ def main():
                           "median of 3 runs"}
 
     # ---- parallax sweep (configs[1]: "max parallax sweep"; one GPU) ----
+    # frames/s per B the way `value` is measured (4 plans/streams, graph replay, inpaint on a
+    # quarter of the SMs per plan) plus the single-stream rate; the stage times from a
+    # separate event-timed pass on one plan
     sweep = {}
     if not args.no_sweep and world == 1:
         for b in SWEEP:
-            pb = p3s.Pipeline(W4K, H4K, p3s.Config(base=b))
+            cb = p3s.Config(base=b)
+            sl = [p3s.Pipeline(W4K, H4K, cb) for _ in range(len(lanes))]
+            for ln in sl:
+                if len(sl) > 1:
+                    ln.set_inpaint_ctas(inpaint_ctas)
+                for i in range(RING):
+                    ln.run(ring[i].addr)
+            p3s.device_sync()
+            ns = 40
+            a, z = p3s.Event(), p3s.Event()
+            ends = [p3s.Event() for _ in sl]
+            a.record(sl[0].stream)
+            for ln in sl[1:]:
+                a.wait(ln.stream)
+            for i in range(ns):
+                sl[i % len(sl)].run(ring[i % RING].addr)
+            for ln, e in zip(sl, ends):
+                e.record(ln.stream)
+                e.wait(sl[0].stream)
+            z.record(sl[0].stream)
+            p3s.stream_sync(sl[0].stream)
+            fps_b = ns / (a.elapsed_ms(z) / 1e3)
+            pb = p3s.Pipeline(W4K, H4K, cb)
             for i in range(3):
                 pb.run(ring[i % RING].addr, timed=True)
             p3s.stream_sync(pb.stream)
             pb.timing_sum(reset=True)
-            a, z = p3s.Event(), p3s.Event()
-            ns = 20
-            a.record(pb.stream)
-            for i in range(ns):
+            a1, z1 = p3s.Event(), p3s.Event()
+            n1 = 12
+            a1.record(pb.stream)
+            for i in range(n1):
                 pb.run(ring[i % RING].addr, timed=True)
-            z.record(pb.stream)
+            z1.record(pb.stream)
             p3s.stream_sync(pb.stream)
             st, n = pb.timing_sum(reset=True)
             passes = pb.inpaint_stats()
-            sweep[str(b)] = {"frames_per_s": ns / (a.elapsed_ms(z) / 1e3),
+            sweep[str(b)] = {"frames_per_s": fps_b,
+                             "frames_per_s_single_stream": n1 / (a1.elapsed_ms(z1) / 1e3),
                              "inpaint_ms": (st["inpaint_left_ns"] + st["inpaint_right_ns"]) / n / 1e6,
                              "dibr_ms": st["dibr_ns"] / n / 1e6,
                              "inpaint_passes": [int(passes[0]), int(passes[3])]}
             d = next((v for v in digests.values() if v["w"] == W4K and v["seed"] == seeds[0]
                       and v["cfg"].get("base") == b and v["cfg"].get("formats", 1) == 1), None)
             if d is not None and seeds[0] == 1:
-                pb.run(ring[0].addr)
-                _, _, ana = pb.download()
-                if sha(ana) != d["anaglyph"]:
-                    raise SystemExit(f"bench: parity gate failed: sweep B={b}")
+                for ln in sl + [pb]:
+                    ln.run(ring[0].addr)
+                    _, _, ana = ln.download()
+                    if sha(ana) != d["anaglyph"]:
+                        raise SystemExit(f"bench: parity gate failed: sweep B={b}")
                 sweep[str(b)]["parity"] = "= reference digest"
-            del pb
+            del pb, sl
 
     # ---- the other BASELINE configs, measured alongside (not the headline) ----
     extra = {}
