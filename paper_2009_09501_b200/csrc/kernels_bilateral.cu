@@ -22,10 +22,13 @@
 // reference's single-sided update bit for bit. Clipping in y is done by the row loop
 // bounds. Rows of a warp's window where only some outputs are inside their window are
 // run with warp-uniform per-output predicates; the bulk rows run branch-free.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
 #include "p3s_cu.h"
+
+#include <type_traits>
 
 namespace p3s {
 namespace cu {
@@ -381,14 +384,20 @@ constexpr int kF32Copies = 32;  // LDS.32, one copy per lane: conflict-free
 //  * table: entries k = gq - gi + 255 in [0, 510] hold R(|k - 255|) as float, 511..766 are
 //    0; 32 copies, lane l reads copy l (bank l);
 //  * depth u8 -> float without the XU pipe: PRMT builds 0x4B0000dd = 2^23 + d, FADD2 -2^23.
+// Rows fold into float-pair accumulators: (N_a, N_b) = sy * (SV_a, SV_b) + (N_a, N_b), one
+// FFMA2 per row and output (and likewise D); the halves meet once, in FP64, for the quotient.
+// (Folding each row in FP64 instead — add the halves, F2F, DFMA — stalled every warp at each
+// row's end on the F2F -> DFMA latency: 9 % of the bulk rows' samples with no LDS issued.)
 // Error bound (u = 2^-24, every term >= 0, d exact in float). Weight-sum terms: sx (1
 // rounding), R (1), the product is exact inside the FFMA; value-sum terms: sx (1), R (1),
-// sx*d (1). Accumulation adds <= 16 roundings (FFMA chain), the half-row combine 1, sy 1.
-// So every term of N and D is within gamma_21 (+2^-46 for the double-level table, fold and
-// division roundings) of its exact value, |v~ - v| <= v * 42.0001u, and the reference's own
-// FP64 result is within v * 2200 * 2^-53 of v; underflowed float weights add < 1e-35
-// absolute against D >= 1 (the centre tap's weight is exactly 1). A byte is accepted only
-// when v~ + 0.5 is farther than 44u * v~ + 1e-9 from every integer.
+// sx*d (1). The row's FFMA chain adds <= R roundings, float(sy) 1, and the cross-row fold
+// chain (the sy product is exact inside its FFMA) <= 2R + 1. So every term of N and D is
+// within gamma_(3R+5) (+2^-46 for the FP64 half combine, table and division) of its exact
+// value, |v~ - v| <= v * (6R + 10)u (1 + 1e-4), and the reference's own FP64 result is within
+// v * 2200 * 2^-53 of v; underflowed float weights add < 1e-35 absolute against D >= 1 (the
+// centre tap's weight is exactly 1). A byte is accepted only when v~ + 0.5 is farther than
+// (6R + 20)u * v~ + 1e-9 from every integer (r = 16: 116u; ~0.13 % of 4K pixels go to the
+// exact fix-up).
 constexpr int kSepEntries = 767;  // 511 real + 256 zero
 constexpr int kSepOob = 511 * 128;
 
@@ -403,6 +412,7 @@ template <int R, int P>
 struct SepParam {
     unsigned long long sx2[R + 1];  // (float(sx), float(sx)), dx = 0..R
     double sy[2 * R + 1];            // double(float(sy(dy))), dy + R
+    unsigned long long sy2[2 * R + 1];  // (float(sy), float(sy)), dy + R (FOLD)
 };
 
 // One LDS.32 at a shared-window byte address (base already includes the table's address,
@@ -413,10 +423,11 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     return v;
 }
 
-template <int R, int P, bool ALL, int U>
+template <int R, int P, bool ALL, int U, typename Acc>
 __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t* __restrict__ row,
-                                        int t, const uint32_t (&base)[P], double (&ws)[P],
-                                        double (&vs)[P]) {
+                                        int t, const uint32_t (&base)[P], Acc (&ws)[P],
+                                        Acc (&vs)[P]) {
+    constexpr bool FOLD = sizeof(Acc) == 8 && !__is_same(Acc, double);
     unsigned long long SW[P], SV[P];
     {
         const uint32_t c = row[0];
@@ -453,12 +464,20 @@ __device__ __forceinline__ void sep_row(const SepParam<R, P>& sp, const uint32_t
 #pragma unroll
     for (int i = 0; i < P; ++i) {
         if (!ALL && static_cast<unsigned>(t - i) > static_cast<unsigned>(2 * R)) continue;
-        float a0, a1, b0, b1;
-        unpack2(SW[i], a0, a1);
-        unpack2(SV[i], b0, b1);
-        const double sy = sp.sy[t - i];
-        ws[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(a0, a1)), ws[i]);
-        vs[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(b0, b1)), vs[i]);
+        if constexpr (FOLD) {
+            // the row's pair sums folded into float-pair accumulators: sy * row + acc, one
+            // FFMA2 each (the halves meet only in the final quotient, in FP64)
+            const unsigned long long SY2 = sp.sy2[t - i];
+            ws[i] = ffma2(SY2, SW[i], ws[i]);
+            vs[i] = ffma2(SY2, SV[i], vs[i]);
+        } else {
+            float a0, a1, b0, b1;
+            unpack2(SW[i], a0, a1);
+            unpack2(SV[i], b0, b1);
+            const double sy = sp.sy[t - i];
+            ws[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(a0, a1)), ws[i]);
+            vs[i] = __fma_rn(sy, static_cast<double>(__fadd_rn(b0, b1)), vs[i]);
+        }
     }
 }
 
@@ -469,7 +488,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int R, int P, int NW, int U>
+template <int R, int P, int NW, int U, bool FOLD = true>
 __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     const __grid_constant__ SepParam<R, P> sp, const uint8_t* __restrict__ depth,
     const uint8_t* __restrict__ guide, int pitch, int w, int h,
@@ -502,10 +521,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
         }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // certificate: every numerator / denominator term carries <= R + 5 float roundings
-    // (sx, R, sx*d, R half-row adds, the half combine, sy), so |v~ - v| <= 2(R+5)u v (1 + o(u));
-    // accept only beyond (2R + 12)u v + 1e-9 (R = 16: 44u)
-    constexpr double kRel = (2.0 * R + 12.0) / 16777216.0;
+    // certificate (see the error bound above): (6R + 20)u v + 1e-9 with the FP32 row fold;
+    // (2R + 12)u v + 1e-9 when rows fold in FP64 (R + 5 roundings per term)
+    constexpr double kRel = (FOLD ? 6.0 * R + 20.0 : 2.0 * R + 12.0) / 16777216.0;
     // 16-byte chunks of the tile window rows that lie inside the image rows and the pitch;
     // the rest is never read (the packing step marks out-of-image pixels itself)
     auto prefetch = [&](int tile) {
@@ -561,13 +579,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
         const uint32_t* tile_col = s_tile + (warp * P) * SW + lane + R;
         const uint32_t tbl_s = static_cast<uint32_t>(__cvta_generic_to_shared(tbl));
         uint32_t base[P];
-        double ws[P], vs[P];
+        using Acc = typename std::conditional<FOLD, unsigned long long, double>::type;
+        Acc ws[P], vs[P];
 #pragma unroll
         for (int i = 0; i < P; ++i) {
             const int gi = static_cast<int>(tile_col[(i + R) * SW] >> 23) & 0xFF;
             base[i] = tbl_s + static_cast<uint32_t>((255 - gi) * 128 + lane * 4);
-            ws[i] = 0.0;
-            vs[i] = 0.0;
+            ws[i] = 0;
+            vs[i] = 0;
         }
         // Every window row of the band is processed: rows outside the image hold the OOB
         // guide offset (zero weight, exact zeros), so there is no clipping logic. The ramp
@@ -582,7 +601,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
             const bool valid = x < w && y < h;
             bool uncertain = false;
             if (valid) {
-                const double v = __ddiv_rn(vs[i], ws[i]);
+                double v;
+                if constexpr (FOLD) {
+                    float a0, a1, b0, b1;
+                    unpack2(ws[i], a0, a1);
+                    unpack2(vs[i], b0, b1);
+                    v = __ddiv_rn(__dadd_rn(b0, b1), __dadd_rn(a0, a1));
+                } else {
+                    v = __ddiv_rn(vs[i], ws[i]);
+                }
                 const double f = __dadd_rn(v, 0.5);
                 const double r = floor(f);
                 const double dist = fmin(f - r, r + 1.0 - f);
@@ -613,8 +640,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
     }
 }
 
-// Exact recompute of the uncertified pixels (reference order), sized so that every listed
-// pixel gets its own warp in one wave (4 warps per block, ~6 KB of shared memory per warp).
+// Exact recompute of the uncertified pixels (reference order): one warp per listed pixel,
+// one resident wave of CTAs (4 warps each; their windows plus the FP64 range and spatial
+// tables in shared memory, ~24 KB per CTA at r = 16), later pixels by grid stride.
 // The window is staged with 16-byte loads. The terms of a batch of window rows — per row
 // the centre (wc, wc*d), then per dx the mirrored pair (wl + wr, wl*dl + wr*dr) or the single
 // in-image side, each separately rounded — are computed by all lanes in parallel; lane 0
@@ -627,13 +655,21 @@ __global__ void __launch_bounds__(WPB * 32) k_bilateral_fixup2(
     uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
     const uint32_t* __restrict__ count) {
     constexpr int S = 2 * R + 1, SP = (S + 15 + 15) / 16 * 16;  // window side, staged row length
-    constexpr int kBatch = (S + 1) / 2;        // window rows per term batch
+    constexpr int kBatch = 4;                  // window rows per term batch (serial fallback)
     __shared__ __align__(16) uint8_t s_g[WPB][S][SP];
     __shared__ __align__(16) uint8_t s_d[WPB][S][SP];
     __shared__ double2 s_tu[WPB][kBatch][R + 1];
+    // the FP64 range and spatial tables, staged once per CTA: the terms' table reads are
+    // shared-memory gathers instead of L1 lookups (the fix-up was latency-bound on them)
+    __shared__ double s_rng[256];
+    __shared__ double s_sp[S * (R + 1)];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t n = *count;
     const uint32_t nwarps = gridDim.x * WPB;
+    if (blockIdx.x * WPB >= n) return;  // (uniform per CTA: no barrier below is skipped)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_rng[i] = __ldg(range_g + i);
+    for (int i = threadIdx.x; i < S * (R + 1); i += blockDim.x) s_sp[i] = __ldg(spatial + i);
+    __syncthreads();
     for (uint32_t k = blockIdx.x * WPB + wib; k < n; k += nwarps) {
         const uint32_t idx = list[k];
         const int x = static_cast<int>(idx % static_cast<uint32_t>(w));
@@ -677,15 +713,15 @@ __global__ void __launch_bounds__(WPB * 32) k_bilateral_fixup2(
                 if (dy < dy0 || dy > dy1) continue;
                 const uint8_t* gr = &s_g[wib][r][R + off];
                 const uint8_t* dr = &s_d[wib][r][R + off];
-                const double sj = __ldg(spatial + r * (R + 1) + j);
+                const double sj = s_sp[r * (R + 1) + j];
                 double t = 0.0, u = 0.0;
                 if (j == 0) {
-                    t = __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[0], 0)));
+                    t = __dmul_rn(sj, s_rng[__usad(gp, gr[0], 0)]);
                     u = __dmul_rn(t, static_cast<double>(dr[0]));
                 } else {
                     const bool lin = x - j >= 0, rin = x + j < w;
-                    const double wl = lin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[-j], 0))) : 0.0;
-                    const double wr = rin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[j], 0))) : 0.0;
+                    const double wl = lin ? __dmul_rn(sj, s_rng[__usad(gp, gr[-j], 0)]) : 0.0;
+                    const double wr = rin ? __dmul_rn(sj, s_rng[__usad(gp, gr[j], 0)]) : 0.0;
                     if (lin && rin) {
                         t = __dadd_rn(wl, wr);
                         u = __dadd_rn(__dmul_rn(wl, static_cast<double>(dr[-j])),
@@ -729,14 +765,14 @@ __global__ void __launch_bounds__(WPB * 32) k_bilateral_fixup2(
                 if (dy >= dy0 && dy <= dy1) {
                     const uint8_t* gr = &s_g[wib][r][R + off];
                     const uint8_t* dr = &s_d[wib][r][R + off];
-                    const double sj = __ldg(spatial + r * (R + 1) + j);
+                    const double sj = s_sp[r * (R + 1) + j];
                     if (j == 0) {
-                        t = __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[0], 0)));
+                        t = __dmul_rn(sj, s_rng[__usad(gp, gr[0], 0)]);
                         u = __dmul_rn(t, static_cast<double>(dr[0]));
                     } else {
                         const bool lin = x - j >= 0, rin = x + j < w;
-                        const double wl = lin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[-j], 0))) : 0.0;
-                        const double wr = rin ? __dmul_rn(sj, __ldg(range_g + __usad(gp, gr[j], 0))) : 0.0;
+                        const double wl = lin ? __dmul_rn(sj, s_rng[__usad(gp, gr[-j], 0)]) : 0.0;
+                        const double wr = rin ? __dmul_rn(sj, s_rng[__usad(gp, gr[j], 0)]) : 0.0;
                         if (lin && rin) {
                             t = __dadd_rn(wl, wr);
                             u = __dadd_rn(__dmul_rn(wl, static_cast<double>(dr[-j])),
@@ -878,7 +914,7 @@ cudaError_t launch_r(const uint8_t* depth, const uint8_t* guide, Geom gm,
     return cudaGetLastError();
 }
 
-template <int R, int P, int NW, int U = 4>
+template <int R, int P, int NW, int U = 4, bool FOLD = true>
 cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
                             const double* spatial_host, const double* range, uint8_t* out,
                             uint32_t* list, uint32_t* count, uint32_t* tile_ctr, int tr0, int tr1,
@@ -892,7 +928,13 @@ cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
         memcpy(&u, &f, 4);
         sp.sx2[d] = (static_cast<unsigned long long>(u) << 32) | u;
     }
-    for (int dy = -R; dy <= R; ++dy) sp.sy[dy + R] = static_cast<double>(static_cast<float>(row0[dy < 0 ? -dy : dy]));
+    for (int dy = -R; dy <= R; ++dy) {
+        const float f = static_cast<float>(row0[dy < 0 ? -dy : dy]);
+        sp.sy[dy + R] = static_cast<double>(f);
+        unsigned u;
+        memcpy(&u, &f, 4);
+        sp.sy2[dy + R] = (static_cast<unsigned long long>(u) << 32) | u;
+    }
     constexpr int TY = NW * P;
     constexpr int SW = kTX + 2 * R, SH = TY + 2 * R;
     constexpr int RO = ((kTX - R) % 16 + 16) % 16;
@@ -901,11 +943,11 @@ cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
                         2 * static_cast<size_t>(SWR) * SH;
     static std::atomic<unsigned long long> configured{0};
     once_per_device(configured, [smem] {
-        cudaFuncSetAttribute(k_bilateral_sep<R, P, NW, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_bilateral_sep<R, P, NW, U, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
     });
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_sep<R, P, NW, U>, NW * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_sep<R, P, NW, U, FOLD>, NW * 32, smem);
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     const int tiles_x = (gm.w + kTX - 1) / kTX;
     const int tiles_y = (gm.h + TY - 1) / TY;
@@ -914,7 +956,7 @@ cudaError_t launch_sep_main(const uint8_t* depth, const uint8_t* guide, Geom gm,
     const int t0 = tr0 * tiles_x, t1 = tr1 * tiles_x;
     const int grid = min(t1 - t0, per_sm * sm_count());
     note_launch(st);
-    k_bilateral_sep<R, P, NW, U><<<grid, NW * 32, smem, st>>>(
+    k_bilateral_sep<R, P, NW, U, FOLD><<<grid, NW * 32, smem, st>>>(
         sp, depth, guide, gm.pitch, gm.w, gm.h, range, out, list, count, tiles_x, t0, t1, tile_ctr,
         table);
     return cudaGetLastError();
@@ -928,7 +970,10 @@ cudaError_t launch_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm
     // 4 warps per block up to R = 16 (static smem < 48 KB), 2 beyond; by default enough
     // warps for every listed pixel of a 4K frame in one wave
     constexpr int WPB = R <= 16 ? 4 : 2;
-    int ctas = sm_count() * 32 / WPB;
+    // one resident wave (a second, partial one only adds its tail)
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_fixup2<R, WPB>, WPB * 32, 0);
+    int ctas = sm_count() * std::max(1, std::min(per_sm, 32 / WPB));
     if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
     note_launch(st);
     k_bilateral_fixup2<R, WPB><<<ctas, WPB * 32, 0, st>>>(

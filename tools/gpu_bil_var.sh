@@ -1,11 +1,11 @@
 #!/bin/bash
 # A/B of bilateral variants on the GPU box: parity tests, then 4K stage times per variant.
-# usage: bash tools/gpu_bil_var.sh TAG "0 1 2 3"  (P3S_BIL_VAR kernel variants)
+# usage: [EV=P3S_BIL_FOLD] bash tools/gpu_bil_var.sh TAG "0 1"  (env-selected kernel variants, default P3S_BIL_VAR)
 TAG=${1:-ab}; VARS=${2:-"1 3"}
 mkdir -p gpurun_out
 for V in $VARS; do
-  echo "var $V parity: $(P3S_BIL_VAR=$V timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k 'golden or random or sweep or 4k' 2>&1 | tail -1)"
-  P3S_BIL_VAR=$V timeout 300 python bench.py --steps 60 --warmup 5 --no-sweep --no-cpu-baseline --no-extra \
+  echo "var $V parity: $(env "${EV:-P3S_BIL_VAR}=$V" timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k 'golden or random or sweep or 4k' 2>&1 | tail -1)"
+  env "${EV:-P3S_BIL_VAR}=$V" timeout 300 python bench.py --steps 60 --warmup 5 --no-sweep --no-cpu-baseline --no-extra \
       > gpurun_out/bench_${TAG}_v$V.json 2> gpurun_out/bench_${TAG}_v$V.err
   python - "$V" "gpurun_out/bench_${TAG}_v$V.json" <<'PY'
 import json, sys
