@@ -970,10 +970,14 @@ cudaError_t launch_sep_fixup(const uint8_t* depth, const uint8_t* guide, Geom gm
     // 4 warps per block up to R = 16 (static smem < 48 KB), 2 beyond; by default enough
     // warps for every listed pixel of a 4K frame in one wave
     constexpr int WPB = R <= 16 ? 4 : 2;
-    // one resident wave (a second, partial one only adds its tail)
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bilateral_fixup2<R, WPB>, WPB * 32, 0);
-    int ctas = sm_count() * std::max(1, std::min(per_sm, 32 / WPB));
+    // one resident wave (a second, partial one only adds its tail); the occupancy query is
+    // made once per radius (same answer on every sm_100a device)
+    static const int per_sm = [] {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bilateral_fixup2<R, WPB>, WPB * 32, 0);
+        return std::max(1, std::min(n, 32 / WPB));
+    }();
+    int ctas = sm_count() * per_sm;
     if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
     note_launch(st);
     k_bilateral_fixup2<R, WPB><<<ctas, WPB * 32, 0, st>>>(

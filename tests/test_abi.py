@@ -201,3 +201,20 @@ def test_no_cpu_fallback_without_gpu(p3s):
     with pytest.raises(p3s.P3SError) as e:
         p3s.convert(img, p3s.Config())
     assert e.value.status == 4 and "no CUDA device" in e.value.message
+
+
+def test_bilateral_sass_keeps_uniform_operands(p3s):
+    """Build-artifact guard (CPU, no GPU call): the certified bilateral's SW accumulations take
+    the sx pairs as uniform-register FFMA2 operands and hold no local-memory spills. ptxas
+    dropped those operands to vector registers after two unrelated epilogue edits in round 2,
+    and the kernel ran 20-25 % slower with the same instruction mix (profiles/r2/summary.md)."""
+    tool = "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", p3s.LIB_PATH], capture_output=True, text=True).stdout
+    m = re.search(r"Function : \S*k_bilateral_sepILi16ELi8ELi16ELi16E\S*\n(.*?)(?=\n\s+Function : |\Z)", sass, re.S)
+    assert m, "k_bilateral_sep<16, 8, 16, 16> not found in the library"
+    body = m.group(1)
+    ur_ffma2 = len(re.findall(r"FFMA2 [^;]*UR\d+", body))
+    assert ur_ffma2 >= 1000, ur_ffma2
+    assert "STL" not in body and "LDL" not in body
