@@ -708,6 +708,38 @@ __global__ void __launch_bounds__(WPB * 32) k_bilateral_fixup2(
             constexpr int kN = S * (R + 1);
             constexpr int kM = (kN + 31) / 32;
             double wsp = 0.0, vsp = 0.0;
+            if (x >= R && x + R < w && y >= R && y + R < h) {
+                // interior pixel (nearly all of them): every tap is in the image, so the terms
+                // need no side tests; the centre is a pair with a zero right weight (t = wl + 0
+                // and u = wl * d + 0 * d are the reference's wl and wl * d exactly). Two
+                // accumulators per lane interleave the terms' FP64 chains (any order is covered
+                // by the bound below: <= kM terms per lane chain).
+                double w0 = 0.0, v0 = 0.0, w1 = 0.0, v1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < kM; ++k) {
+                    const int e = lane + 32 * k;
+                    if (e >= kN) break;
+                    const int r = e / (R + 1), j = e - r * (R + 1);
+                    const uint8_t* gr = &s_g[wib][r][R + off];
+                    const uint8_t* dr = &s_d[wib][r][R + off];
+                    const double sj = s_sp[e];
+                    const double wl = __dmul_rn(sj, s_rng[__usad(gp, gr[-j], 0)]);
+                    const double wq = __dmul_rn(sj, s_rng[__usad(gp, gr[j], 0)]);
+                    const double wr = j ? wq : 0.0;
+                    const double t = __dadd_rn(wl, wr);
+                    const double u = __dadd_rn(__dmul_rn(wl, static_cast<double>(dr[-j])),
+                                               __dmul_rn(wr, static_cast<double>(dr[j])));
+                    if (k & 1) {
+                        w1 = __dadd_rn(w1, t);
+                        v1 = __dadd_rn(v1, u);
+                    } else {
+                        w0 = __dadd_rn(w0, t);
+                        v0 = __dadd_rn(v0, u);
+                    }
+                }
+                wsp = __dadd_rn(w0, w1);
+                vsp = __dadd_rn(v0, v1);
+            } else
             for (int e = lane; e < kN; e += 32) {
                 const int r = e / (R + 1), j = e - r * (R + 1), dy = r - R;
                 if (dy < dy0 || dy > dy1) continue;
