@@ -558,15 +558,39 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
         if (threadIdx.x == 0)
             s_next[it & 1] = tile_begin + static_cast<int>(gridDim.x) + static_cast<int>(atomicAdd(tile_ctr, 1u));
         __syncthreads();  // raw bytes of this tile landed; the previous tile's compute is done
-        for (int e = threadIdx.x; e < SH * SW; e += blockDim.x) {
-            const int sy = e / SW, sx = e - sy * SW;
-            const int gy = ty0 - R + sy, gx = tx0 - R + sx;
-            uint32_t v = static_cast<uint32_t>(kSepOob) << 16;
-            if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-                const int ri = sy * SWR + sx + RO;
-                v = (static_cast<uint32_t>(s_raw[ri]) << 23) | s_raw[SH * SWR + ri];
+        if constexpr (RO % 4 == 0 && SW % 4 == 0) {
+            // 4 window columns per step: one 4-byte load per plane (the 4 bytes lie in one
+            // 16-byte chunk, fetched whole or not at all) and one 16-byte store
+            constexpr uint32_t kOobWord = static_cast<uint32_t>(kSepOob) << 16;
+            for (int e4 = threadIdx.x; e4 < SH * SW / 4; e4 += blockDim.x) {
+                const int e = 4 * e4;
+                const int sy = e / SW, sx = e - sy * SW;
+                const int gy = ty0 - R + sy, gx = tx0 - R + sx;
+                uint4 o = make_uint4(kOobWord, kOobWord, kOobWord, kOobWord);
+                if (gy >= 0 && gy < h && gx + 3 >= 0 && gx < w) {
+                    const int ri = sy * SWR + sx + RO;
+                    const uint32_t g4 = *reinterpret_cast<const uint32_t*>(s_raw + ri);
+                    const uint32_t d4 = *reinterpret_cast<const uint32_t*>(s_raw + SH * SWR + ri);
+                    auto px = [&](int k) {
+                        return static_cast<unsigned>(gx + k) < static_cast<unsigned>(w)
+                                   ? (((g4 >> (8 * k)) & 0xFFu) << 23) | ((d4 >> (8 * k)) & 0xFFu)
+                                   : kOobWord;
+                    };
+                    o = make_uint4(px(0), px(1), px(2), px(3));
+                }
+                *reinterpret_cast<uint4*>(s_tile + e) = o;
             }
-            s_tile[e] = v;
+        } else {
+            for (int e = threadIdx.x; e < SH * SW; e += blockDim.x) {
+                const int sy = e / SW, sx = e - sy * SW;
+                const int gy = ty0 - R + sy, gx = tx0 - R + sx;
+                uint32_t v = static_cast<uint32_t>(kSepOob) << 16;
+                if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
+                    const int ri = sy * SWR + sx + RO;
+                    v = (static_cast<uint32_t>(s_raw[ri]) << 23) | s_raw[SH * SWR + ri];
+                }
+                s_tile[e] = v;
+            }
         }
         __syncthreads();
         const int next = s_next[it & 1];
