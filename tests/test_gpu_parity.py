@@ -612,3 +612,37 @@ def test_concurrent_convert_threads(p3s, checker):
     for t in threads:
         t.join()
     assert not errors, errors[:5]
+
+
+def _near_tie_cases(w, h):
+    """Depth/guide pairs built to put the filtered value on or next to a .5 boundary: flat
+    guides make the weights purely spatial, so two-level depth patterns average to k + 0.5
+    up to the centre tap's and the window edges' asymmetry."""
+    yy, xx = np.mgrid[0:h, 0:w]
+    flat = np.full((h, w), 128, np.uint8)
+    cases = {
+        "checker": ((100 + ((xx + yy) & 1)).astype(np.uint8), flat),
+        "row_stripes": ((40 + (yy & 1)).astype(np.uint8), flat),
+        "col_stripes": ((200 + (xx & 1)).astype(np.uint8), flat),
+        "wide_steps": ((10 * ((xx // 3) % 2) + 77).astype(np.uint8), flat),
+        # a two-level guide: the range weights split the window into two classes
+        "guide_edge": ((60 + ((xx + yy) & 1)).astype(np.uint8),
+                       np.where(xx < w // 2, 90, 91).astype(np.uint8)),
+        "saturated": (np.where((xx + yy) & 1, 255, 254).astype(np.uint8), flat),
+    }
+    return cases
+
+
+@pytest.mark.parametrize("sigma_s", [8.0, 3.5, 11.7])
+def test_bilateral_near_ties_vs_oracle(p3s, checker, sigma_s):
+    """The certified FP32 filter (k_bilateral_sep, FP32 row folds) must defer every pixel it
+    cannot prove to the exact FP64 fix-up: on inputs whose filtered values sit on or next to
+    .5 boundaries the bytes still equal the reference's (bilateral.cpp:40-85)."""
+    import oracle
+    w, h = 213, 149
+    cfg = p3s.Config(sigma_spatial=sigma_s, sigma_range=16.0)
+    ocfg = oracle.Cfg(sigma_spatial=sigma_s, sigma_range=16.0)
+    for name, (depth, guide) in _near_tie_cases(w, h).items():
+        got = p3s.cross_bilateral(depth, guide, cfg)
+        ref = checker.cross_bilateral(depth, guide, ocfg, threads=NCPU)
+        assert np.array_equal(got, ref), (name, int((got != ref).sum()))
