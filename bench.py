@@ -469,19 +469,24 @@ def main():
             raise SystemExit("bench: parity gate failed: p3s_convert output differs from the reference digest")
         parity["e2e"] = f"p3s_convert seed {seeds[0]}: = reference digest"
     e2e_steps = max(60, min(args.steps, 100))  # >= 60 calls: stable against per-call jitter
-    dist.barrier()
-    t0 = time.perf_counter()
+    # three timed runs of e2e_steps calls each; the reported value is the median run (host
+    # wall clock around synchronous calls jitters by ~2 % run to run), all three are listed
     checksum = 0
-    for i in range(e2e_steps):
-        p3s._check(L.p3s_convert(images[i % RING].h, cfg.h, C.byref(res)))
-        p3s._check(L.p3s_result_output(res, 1, C.byref(ana_ptr)))
-        plane = C.cast(L.p3s_image_plane(ana_ptr, 0), C.POINTER(C.c_uint8))
-        checksum += plane[(i * 7919) % N]  # touch the host result
-        L.p3s_result_free(res)
-    e2e_s = time.perf_counter() - t0
-    dist.barrier()
-    (e2e_max,) = dist.max(e2e_s)
-    e2e_fps = e2e_steps * world / e2e_max
+    e2e_runs = []
+    for rep in range(3):
+        dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            p3s._check(L.p3s_convert(images[i % RING].h, cfg.h, C.byref(res)))
+            p3s._check(L.p3s_result_output(res, 1, C.byref(ana_ptr)))
+            plane = C.cast(L.p3s_image_plane(ana_ptr, 0), C.POINTER(C.c_uint8))
+            checksum += plane[(i * 7919) % N]  # touch the host result
+            L.p3s_result_free(res)
+        e2e_s = time.perf_counter() - t0
+        dist.barrier()
+        (e2e_max,) = dist.max(e2e_s)
+        e2e_runs.append(e2e_steps * world / e2e_max)
+    e2e_fps = sorted(e2e_runs)[1]
 
     # ---- the same synchronous call from several long-lived host threads at once (a server
     # answering concurrent requests; plans are cached per thread, so each thread warms its
@@ -903,6 +908,7 @@ def main():
         ],
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 3 * N,
                 "d2h_bytes_per_step": 3 * N, "steps": e2e_steps,
+                "runs": [round(v, 1) for v in e2e_runs], "statistic": "median of 3 timed runs",
                 "path": "p3s_convert (C ABI, one synchronous call per frame) on a pinned "
                         "p3s_image, then p3s_result_output(anaglyph) read on the host; depth "
                         "and filtered depth stay on the GPU until p3s_result_depth asks"},
