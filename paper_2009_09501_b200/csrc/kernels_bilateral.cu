@@ -325,23 +325,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_bilateral_r(
     }
 }
 
-// ---- certified FP32 fast path (radius 16) ------------------------------------------------
+// ---- certified FP32 fast path (radii 7..24) ----------------------------------------------
 // Computes every output approximately and proves, per pixel, that the approximation rounds
 // to the same byte as the reference's exact FP64 sequence; pixels it cannot prove are
-// recomputed exactly (k_bilateral_fixup, reference order). The output bytes are therefore
-// identical to the reference's — only the arithmetic that decides them changes.
-//
-// Arithmetic: per window row, the left and right half-rows are accumulated as FP32 pairs
-// with packed sm_100 instructions — W = (s,s) * (R[kl], R[kr]) (FMUL2), SW += W (FADD2),
-// SV = W * (dl, dr) + SV (FFMA2) — then folded into FP64 totals per row.
-// Error bound (u = 2^-24, terms are non-negative): every weight carries <= 3 roundings
-// (float(s), float(R), product), a half-row sum <= 17 more, the half-row combine 1, the FP64
-// row accumulation and division < 1e-13 relative. So N~ = N(1+eN), D~ = D(1+eD) with
-// |eN| <= 21u+, |eD| <= 20u+, hence |v~ - v| <= v * 42u (+ FP64 slack). The reference's
-// own FP64 result is within v * 2200 * 2^-53 of v. Taps whose FP32 weight underflows add
-// an absolute error < 1e-33 against D >= 1 (the centre tap has weight exactly 1). We use
-// bound(v) = 44u * v + 1e-9 and accept floor(v~ + 0.5) only when v~ + 0.5 is farther than
-// bound(v) from every integer.
+// recomputed exactly (k_bilateral_fixup2, reference order). The output bytes are therefore
+// identical to the reference's — only the arithmetic that decides them changes. The packed
+// f32x2 helpers below carry two taps (the mirrored pair of a window row) per instruction;
+// the error bound and certificate are documented at k_bilateral_sep.
 __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
     unsigned long long r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
@@ -370,20 +360,19 @@ __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsign
 constexpr int kF32Copies = 32;  // LDS.32, one copy per lane: conflict-free
 
 // ---- certified FP32, separable spatial factor (radius 16) ---------------------------------
-// Same certificate idea as k_bilateral_f32, cheaper per tap. The spatial weight factors as
+// The spatial weight factors as
 // s(dx,dy) = sx(dx) * sy(dy) (exp of a sum; host tables, each rounded to float), so inside a
 // window row a tap contributes sx(dx)*R(|gi-gq|) to the weight sum and (sx(dx)*d_q)*R to the
 // value sum: sx(dx) and sx(dx)*d_q depend only on the tap and are shared by the thread's P
 // outputs (one FMUL2 per tap pair), leaving per tap pair and output 2 address adds
 // (LEA.HI), 2 conflict-free LDS.32 range lookups and 2 FFMA2. The row's FP32 sums are
-// scaled by sy(dy) when they are folded into the FP64 totals (float x float is exact in
-// double; the fold is one DFMA).
+// scaled by sy(dy) when they are folded (below).
 //  * tile element (u32): (goff << 16) | depth, goff = guide * 128 (byte offset of the range
 //    row), or 511 * 128 for pixels outside the image: base_i + goff then lands in the zero
 //    tail of the table for every centre guide, so image borders need no clipping code;
 //  * table: entries k = gq - gi + 255 in [0, 510] hold R(|k - 255|) as float, 511..766 are
 //    0; 32 copies, lane l reads copy l (bank l);
-//  * depth u8 -> float without the XU pipe: PRMT builds 0x4B0000dd = 2^23 + d, FADD2 -2^23.
+//  * depth u8 -> float: byte-select I2F.U8 on the XU pipe (otherwise idle in this loop).
 // Rows fold into float-pair accumulators: (N_a, N_b) = sy * (SV_a, SV_b) + (N_a, N_b), one
 // FFMA2 per row and output (and likewise D); the halves meet once, in FP64, for the quotient.
 // (Folding each row in FP64 instead — add the halves, F2F, DFMA — stalled every warp at each
