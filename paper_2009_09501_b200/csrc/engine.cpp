@@ -750,11 +750,7 @@ struct Pipeline::Impl {
         for (int i = 0; i < n; ++i) tot += cal_share[i];
         for (int i = 0; i < n; ++i) ms[i] = tot > 0 ? static_cast<float>(joint * cal_share[i] / tot) : 0.f;
         if (tot <= 0) ms[1] = joint;
-        if (back) {  // nothing runs between the join and the inpaint
-            float gap = 0.f;
-            CK(cudaEventElapsedTime(&gap, ev[2], ev[3]));
-            ms[2] += gap;
-        }
+        // (fused routes: nothing runs between the join and the inpaint; ev[2] is both)
     }
 
     // The stage shares for banded_stage_ms: an event-timed, unbanded run of the frame now in
@@ -783,9 +779,14 @@ struct Pipeline::Impl {
         StageTimings t;
         CK(cudaEventSynchronize(ev[5]));
         float ms[5] = {0, 0, 0, 0, 0};
-        for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
-        if (banded) {
+        if (banded && band_back()) {
+            // the banded fused routes record no ev[3] (ev[2] is the join and the inpaint start)
+            CK(cudaEventElapsedTime(&ms[3], ev[2], ev[4]));
+            CK(cudaEventElapsedTime(&ms[4], ev[4], ev[5]));
             banded_stage_ms(ev, ms);
+        } else {
+            for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+            if (banded) banded_stage_ms(ev, ms);
         }
         t.depth_gen_ns = ms_to_ns(ms[0]);
         t.filter_ns = ms_to_ns(ms[1]);
@@ -1110,12 +1111,16 @@ struct Pipeline::Impl {
             prev = b;
         }
         for (int k = 0; k < K; ++k) CK(cudaStreamWaitEvent(st, ev_join[k], 0));
-        record_event(ev[6], st);
+        // (each event record is a graph node on the tail's critical path: the fused routes,
+        // where nothing runs between the join and the inpaint, record the join once and
+        // stage_times reads it as both ev[2] and ev[3]; ev[6] only for P3S_DEBUG_CONV)
+        if (!ev_dbg.empty()) record_event(ev[6], st);
         record_event(ev[2], st);
-        if (!back)
+        if (!back) {
             CK(cu::dibr(src_plane(s, 0), src_plane(s, 1), src_plane(s, 2), filt, gm, shift, cols,
                         backward, eo[0], eo[1], st, 0, -1, wide_keys));
-        record_event(ev[3], st);
+            record_event(ev[3], st);
+        }
         enq_inpaint(st, true);  // the copy engines are busy with the bands' downloads
         record_event(ev[4], st);
         enq_formats(st);
