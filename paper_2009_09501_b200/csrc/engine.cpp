@@ -780,9 +780,9 @@ struct Pipeline::Impl {
         CK(cudaEventSynchronize(ev[5]));
         float ms[5] = {0, 0, 0, 0, 0};
         if (banded && band_back()) {
-            // the banded fused routes record no ev[3] (ev[2] is the join and the inpaint start)
-            CK(cudaEventElapsedTime(&ms[3], ev[2], ev[4]));
-            CK(cudaEventElapsedTime(&ms[4], ev[4], ev[5]));
+            // the banded fused routes record no ev[3] / ev[4]: ev[2] is the join and the
+            // inpaint's start, ev[5] its end (the formats were written by the DIBR)
+            CK(cudaEventElapsedTime(&ms[3], ev[2], ev[5]));
             banded_stage_ms(ev, ms);
         } else {
             for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
@@ -1122,8 +1122,11 @@ struct Pipeline::Impl {
             record_event(ev[3], st);
         }
         enq_inpaint(st, true);  // the copy engines are busy with the bands' downloads
-        record_event(ev[4], st);
-        enq_formats(st);
+        if (!back) {
+            record_event(ev[4], st);
+            enq_formats(st);
+        }
+        // (fused routes: the formats were written by the DIBR, so the inpaint's end is the end)
         record_event(ev[5], st);
     }
 
@@ -1971,7 +1974,7 @@ ConversionResult convert_image_deferred(const ImageRGB8& src, const ConversionCo
             float e01 = 0, e06 = 0, e64 = 0, e05 = 0;
             cudaEventElapsedTime(&e01, p->conv_ev[0], p->conv_ev[1]);
             cudaEventElapsedTime(&e06, p->conv_ev[0], p->conv_ev[6]);
-            cudaEventElapsedTime(&e64, p->conv_ev[6], p->conv_ev[4]);
+            cudaEventElapsedTime(&e64, p->conv_ev[6], p->conv_ev[5]);
             cudaEventElapsedTime(&e05, p->conv_ev[0], p->conv_ev[5]);
             std::fprintf(stderr, "[p3s] convert: enqueue %.1f us, wait %.1f us, total %.1f us | gpu: depth0 %.1f, "
                          "filter+dibr end %.1f, inpaint %.1f, all %.1f us\n", us(t0, t1), us(t1, t2), us(t0, t2),
