@@ -1033,7 +1033,8 @@ struct Pipeline::Impl {
         }
     }
 
-    void enq_inpaint(cudaStream_t st, bool zero_by_kernel = false) {
+    // zero: 0 memsets, 1 a kernel, 2 none (enq_inpaint_zero ran earlier in stream order)
+    void enq_inpaint(cudaStream_t st, int zero = 0) {
         if (backward) return;
         cu::EyeOut eo[2];
         dibr_eyes(eo);
@@ -1051,7 +1052,15 @@ struct Pipeline::Impl {
             ie[e].repair = reinterpret_cast<uint32_t*>(ipa);
         }
         CK(cu::inpaint(ie[0], ie[1], gm, static_cast<uint32_t>(npix()), ctl, stats, st, inpaint_ctas,
-                       zero_by_kernel));
+                       zero));
+    }
+
+    // The inpaint's control-word zeroing on its own (a kernel: see the banded body)
+    void enq_inpaint_zero(cudaStream_t st) {
+        if (backward) return;
+        cu::InpaintEye left{};
+        left.repair = reinterpret_cast<uint32_t*>(ipa);
+        CK(cu::inpaint_zero(left, gm, ctl, stats, st, true));
     }
 
     // bil_count layout: [0, K) per-band uncertified counts, [K, 2K) tile-claim counters;
@@ -1081,6 +1090,9 @@ struct Pipeline::Impl {
         dibr_eyes(eo);
         CK(cudaEventRecord(ev_start, st));
         CK(cudaStreamWaitEvent(depth_stream, ev_start, 0));
+        // the inpaint's control words are zeroed now, while the bands run, so the tail after
+        // the last band is DIBR -> inpaint with no zeroing node between them
+        enq_inpaint_zero(st);
         Band prev{0, 0, 0, 0, 0};
         for (int k = 0; k < K; ++k) {
             const Band& b = bands[k];
@@ -1121,7 +1133,7 @@ struct Pipeline::Impl {
                         backward, eo[0], eo[1], st, 0, -1, wide_keys));
             record_event(ev[3], st);
         }
-        enq_inpaint(st, true);  // the copy engines are busy with the bands' downloads
+        enq_inpaint(st, 2);  // zeroed at the body's start (enq_inpaint_zero)
         if (!back) {
             record_event(ev[4], st);
             enq_formats(st);

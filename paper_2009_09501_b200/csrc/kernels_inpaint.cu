@@ -785,9 +785,32 @@ size_t inpaint_scratch_bytes(int w, int h) {
     return 2 * slot_bytes(w, h) + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 128 + 2 * tiles * 4 + 256;
 }
 
+namespace {
+// the work-counter words inside the inpaint arena (same layout as inpaint() builds)
+uint32_t* work_counters(const InpaintEye& left, Geom gm) {
+    const int tiles_x = (gm.w + kT - 1) / kT, tiles_y = (gm.h + kT - 1) / kT;
+    const size_t tiles = static_cast<size_t>(tiles_x) * tiles_y;
+    unsigned char* flags = reinterpret_cast<unsigned char*>(left.repair) + 2 * slot_bytes(gm.w, gm.h);
+    return reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4);
+}
+}  // namespace
+
+cudaError_t inpaint_zero(InpaintEye left, Geom gm, uint32_t* scratch, long long* stats,
+                         cudaStream_t st, bool by_kernel) {
+    ZeroRanges z{};
+    z.p[0] = scratch;
+    z.words[0] = kCtlWords;
+    z.p[1] = work_counters(left, gm);  // [0..15]; [16] (the launch epoch) persists
+    z.words[1] = 16;
+    z.p[2] = stats ? stats + 6 : nullptr;  // per-eye busy ns
+    z.words[2] = stats ? 4u : 0u;
+    z.n = 3;
+    return zero(z, st, by_kernel);
+}
+
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
                     uint32_t* scratch, long long* stats, cudaStream_t st, int max_ctas,
-                    bool zero_by_kernel) {
+                    int zero_mode) {
     (void)capacity;
     // scratch: ctl (kCtlWords u32, zeroed here: pass counts + the barrier counter); the damage
     // slots, tile flags and work lists live in the engine-provided inpaint arena
@@ -807,16 +830,10 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     wk.counters = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4);
     wk.heavy = reinterpret_cast<uint32_t*>(flags + 2 * tiles * 4 + 3 * 2 * tiles * 4 + 128);
     wk.cap = static_cast<int>(2 * tiles);
-    ZeroRanges z{};
-    z.p[0] = scratch;
-    z.words[0] = kCtlWords;
-    z.p[1] = wk.counters;  // [0..15]; [16] (the launch epoch) persists
-    z.words[1] = 16;
-    z.p[2] = stats ? stats + 6 : nullptr;  // per-eye busy ns
-    z.words[2] = stats ? 4u : 0u;
-    z.n = 3;
-    cudaError_t e = zero(z, st, zero_by_kernel);
-    if (e != cudaSuccess) return e;
+    if (zero_mode != 2) {
+        const cudaError_t e = inpaint_zero(left, gm, scratch, stats, st, zero_mode == 1);
+        if (e != cudaSuccess) return e;
+    }
     const size_t smem = kWarps * sizeof(WarpSmem);
     static std::atomic<unsigned long long> configured{0};
     once_per_device(configured, [smem] {
@@ -848,7 +865,7 @@ cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacit
     }
     if (want) cudaMemsetAsync(rdbg, 0, (4 * kDbgRounds + 4) * sizeof(unsigned long long), st);
     note_launch(st);
-    e = cudaLaunchCooperativeKernel(kern, dim3(blocks),
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(blocks),
                                     dim3(kThreads), args, smem, st);
 #ifdef P3S_INPAINT_PHASES
     if (e == cudaSuccess) {

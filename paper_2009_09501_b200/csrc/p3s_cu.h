@@ -198,10 +198,15 @@ struct InpaintEye {
     uint32_t* repair;      // left eye: inpaint arena
 };
 size_t inpaint_scratch_bytes(int w, int h);
+// zero: 0 = the call zeroes its control words with memsets, 1 = with a kernel, 2 = not at
+// all (the caller ran inpaint_zero earlier in stream order, off the critical path)
 cudaError_t inpaint(InpaintEye left, InpaintEye right, Geom gm, uint32_t capacity,
                     uint32_t* scratch /* >= 128 words, zeroed by the call */, long long* stats,
                     cudaStream_t st, int max_ctas = 0 /* 0: one CTA per SM */,
-                    bool zero_by_kernel = false);
+                    int zero = 0);
+// The control-word zeroing inpaint() would do (pass counts, barrier, work counters, busy ns)
+cudaError_t inpaint_zero(InpaintEye left, Geom gm, uint32_t* scratch, long long* stats,
+                         cudaStream_t st, bool by_kernel);
 
 // Formats from materialised eyes (stereo_format.cpp:8-73).
 cudaError_t anaglyph(const uint8_t* const* left, const uint8_t* const* right, Geom gm,
