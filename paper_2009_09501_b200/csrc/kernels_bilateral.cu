@@ -385,7 +385,7 @@ constexpr int kF32Copies = 32;  // LDS.32, one copy per lane: conflict-free
 // value, |v~ - v| <= v * (6R + 10)u (1 + 1e-4), and the reference's own FP64 result is within
 // v * 2200 * 2^-53 of v; underflowed float weights add < 1e-35 absolute against D >= 1 (the
 // centre tap's weight is exactly 1). A byte is accepted only when v~ + 0.5 is farther than
-// (6R + 20)u * v~ + 1e-9 from every integer (r = 16: 116u; ~0.13 % of 4K pixels go to the
+// (6R + 12)u * v~ + 1e-9 from every integer (r = 16: 108u; ~0.12 % of 4K pixels go to the
 // exact fix-up).
 constexpr int kSepEntries = 767;  // 511 real + 256 zero
 constexpr int kSepOob = 511 * 128;
@@ -510,9 +510,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_bilateral_sep(
         }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // certificate (see the error bound above): (6R + 20)u v + 1e-9 with the FP32 row fold;
+    // certificate (see the error bound above): (6R + 12)u v + 1e-9 with the FP32 row fold;
     // (2R + 12)u v + 1e-9 when rows fold in FP64 (R + 5 roundings per term)
-    constexpr double kRel = (FOLD ? 6.0 * R + 20.0 : 2.0 * R + 12.0) / 16777216.0;
+    constexpr double kRel = (FOLD ? 6.0 * R + 12.0 : 2.0 * R + 12.0) / 16777216.0;
     // 16-byte chunks of the tile window rows that lie inside the image rows and the pitch;
     // the rest is never read (the packing step marks out-of-image pixels itself)
     auto prefetch = [&](int tile) {
