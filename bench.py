@@ -473,7 +473,7 @@ def main():
     # wall clock around synchronous calls jitters by ~2 % run to run), all three are listed
     checksum = 0
     e2e_runs = []
-    for rep in range(3):
+    for rep in range(int(os.environ.get("P3S_BENCH_E2E_RUNS", "3"))):
         dist.barrier()
         t0 = time.perf_counter()
         for i in range(e2e_steps):
@@ -486,7 +486,7 @@ def main():
         dist.barrier()
         (e2e_max,) = dist.max(e2e_s)
         e2e_runs.append(e2e_steps * world / e2e_max)
-    e2e_fps = sorted(e2e_runs)[1]
+    e2e_fps = sorted(e2e_runs)[len(e2e_runs) // 2]
 
     # ---- the same synchronous call from several long-lived host threads at once (a server
     # answering concurrent requests; plans are cached per thread, so each thread warms its
