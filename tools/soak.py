@@ -2,7 +2,7 @@
 plain path) and the certified bilateral stage against the CPU oracle over many random sizes
 and configs, including every certified radius (sigma_s in (3, 12]). Not a unit test (it runs
 for minutes); prints one line per failure and a summary.
-usage: python tools/soak.py [seconds] [seed]"""
+usage: python tools/soak.py [seconds] [seed] [size scale, default 1]"""
 import os
 import sys
 import time
@@ -15,6 +15,7 @@ import paper_2009_09501_b200 as p3s  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
+scale = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
 chk = oracle.load("best")
 ncpu = os.cpu_count() or 1
 p3s.set_device(0)
@@ -23,7 +24,7 @@ runs = fails = 0
 while time.time() < t_end:
     kind = rng.integers(0, 3)
     if kind == 0:  # whole conversion, sizes that take the banded path when tall enough
-        w, h = int(rng.integers(16, 1400)), int(rng.integers(8, 900))
+        w, h = int(rng.integers(16, int(1400 * scale))), int(rng.integers(8, int(900 * scale)))
         over = dict(base=int(rng.choice([-1, 0, 2, 16, 30, 60, 120])),
                     sigma_spatial=float(rng.uniform(0.5, 12.0)),
                     sigma_range=float(rng.choice([4.0, 16.0, 40.0])),
