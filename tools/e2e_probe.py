@@ -1,5 +1,6 @@
 """p3s_convert e2e probe: frames/s of synchronous calls on pinned 4K frames (the bench's e2e
-leg), optionally for an experiment library (P3S_LIB_PATH). usage: python tools/e2e_probe.py [n]"""
+leg), optionally for an experiment library (P3S_LIB_PATH); P3S_PROBE_SIZE=WxH picks another size.
+usage: python tools/e2e_probe.py [n]"""
 import ctypes as C
 import os
 import sys
@@ -9,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2009_09501_b200 as p3s  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 60
-W, H = 3840, 2160
+W, H = (int(v) for v in os.environ.get("P3S_PROBE_SIZE", "3840x2160").split("x"))
 L = p3s.lib()
 cfg = p3s.Config()
 imgs = [p3s.Image(p3s.synthetic_frame(W, H, s)) for s in range(1, 9)]
