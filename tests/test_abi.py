@@ -218,3 +218,12 @@ def test_bilateral_sass_keeps_uniform_operands(p3s):
     ur_ffma2 = len(re.findall(r"FFMA2 [^;]*UR\d+", body))
     assert ur_ffma2 >= 1000, ur_ffma2
     assert "STL" not in body and "LDL" not in body
+    # every certified radius: the weight accumulations (about half of all FFMA2) take sx
+    # from a uniform register
+    for r in range(7, 25):
+        m = re.search(rf"Function : \S*k_bilateral_sepILi{r}ELi8ELi16ELi{r}E\S*\n(.*?)(?=\n\s+Function : |\Z)", sass, re.S)
+        assert m, f"k_bilateral_sep<{r}> not found"
+        body = m.group(1)
+        ur, tot = len(re.findall(r"FFMA2 [^;]*UR\d+", body)), len(re.findall(r"FFMA2 ", body))
+        assert ur >= 0.45 * tot, (r, ur, tot)
+        assert "STL" not in body, r
